@@ -1,0 +1,270 @@
+"""ORACLE (test infrastructure only) -- Algorithm 1 request scheduler, step by step.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline leg may
+import this.  Shares no code with the C++ controller it checks.
+
+Follows PAPER.md Algorithm 1 and §III-D:
+  * FIFO within a stage; decode has the highest priority and co-runs with the
+    front stage; vision and prefill never co-run; prefill before vision.
+  * decode uses in-flight batching: a request that becomes decode-ready while
+    a decode iteration runs waits in Q_d and joins the next iteration
+    (Merge(Q_d, req)); vision/prefill are never batched.
+  * line 3-4: count pending requests, adjust the partition with Eq. 5; the
+    partition is applied per forward pass.
+Readings (R13-R17):
+  * events of one tick: completions before arrivals, then by request id;
+  * N_pend = |Q_v| + running vision + waiting/running prefill;
+  * front dispatch first, then decode; decode ctx = DV (vision running),
+    DP (prefill running) or SOLO (no front stage; decode takes every SM);
+    a front pass gets total - s_dec, or every SM (SOLO) when no decode work
+    exists at its dispatch;
+  * decode batch = decode-ready requests in decode-join order, capped at B_max;
+  * gen_len counts the prefill token, decode iterations = gen_len - 1.
+  * SERIAL (Serial-RR, the BASELINE comparison): one pass at a time on all SMs,
+    alternating a decode iteration and a front pass when both are ready.
+The same state machine drives `simulate` (virtual time, durations from curves),
+which checks the worked example of SURVEY.md §8(c) c6 by hand values.
+"""
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass, field
+
+from .planner import adaptive_sm
+
+SERIAL, STATIC, ADAPTIVE = 0, 1, 2
+CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
+# event kinds (order = tie-break class: completions first)
+EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
+# decision kinds
+D_VISION, D_PREFILL, D_DECODE, D_FINISH = 0, 1, 2, 3
+
+
+@dataclass
+class Policy:
+    mode: int = ADAPTIVE
+    total_sms: int = 148
+    granularity: int = 8
+    sm_decode_dv: int = 72      # STATIC
+    sm_decode_dp: int = 72
+    sm_op_dv: int = 48          # ADAPTIVE (Eq. 5)
+    sm_op_dp: int = 48
+    sm_min: int = 16
+    alpha_dv: float = 8.0
+    alpha_dp: float = 8.0
+    b_max: int = 16
+
+
+@dataclass
+class Req:
+    rid: int
+    gen_len: int
+    emitted: int = 0
+    join_seq: int = -1
+
+
+class Alg1:
+    """Algorithm 1 state machine; `tick(events)` returns the decisions taken."""
+
+    def __init__(self, policy: Policy):
+        self.p = policy
+        self.reqs: dict[int, Req] = {}
+        self.q_v: deque[int] = deque()
+        self.prefill_wait: deque[int] = deque()
+        self.vision_running: int | None = None
+        self.prefill_running: int | None = None
+        self.decode_running: list[int] | None = None
+        self.q_d: list[int] = []            # decode-ready, kept in join order
+        self.join_counter = 0
+        self.last_pass = None               # SERIAL alternation
+        self.log: list[tuple] = []
+
+    # -- Eq. 5 / static split for a co-run context
+    def split(self, ctx: int, n_pend: int) -> int:
+        p = self.p
+        if ctx == CTX_SOLO:
+            return p.total_sms
+        if p.mode == STATIC:
+            return p.sm_decode_dv if ctx == CTX_DV else p.sm_decode_dp
+        if ctx == CTX_DV:
+            return adaptive_sm(p.sm_op_dv, p.sm_min, p.alpha_dv, n_pend, p.granularity)
+        return adaptive_sm(p.sm_op_dp, p.sm_min, p.alpha_dp, n_pend, p.granularity)
+
+    def n_pend(self) -> int:
+        return (len(self.q_v) + (self.vision_running is not None) + len(self.prefill_wait)
+                + (self.prefill_running is not None))
+
+    def front_running(self) -> bool:
+        return self.vision_running is not None or self.prefill_running is not None
+
+    def busy(self) -> bool:
+        return self.front_running() or self.decode_running is not None
+
+    def _decode_ready(self, rid: int):
+        r = self.reqs[rid]
+        if r.join_seq < 0:
+            r.join_seq = self.join_counter
+            self.join_counter += 1
+        self.q_d.append(rid)
+        self.q_d.sort(key=lambda x: self.reqs[x].join_seq)
+
+    def _emit(self, rid: int, out: list):
+        r = self.reqs[rid]
+        r.emitted += 1
+        if r.emitted >= r.gen_len:
+            out.append((D_FINISH, (rid,), CTX_SOLO, 0))
+        else:
+            self._decode_ready(rid)
+
+    def add_request(self, rid: int, gen_len: int):
+        self.reqs[rid] = Req(rid, gen_len)
+
+    def tick(self, events: list[tuple]) -> list[tuple]:
+        """events: (kind, key, payload) -- payload rid (or list of rids for DECODE_DONE)."""
+        out: list[tuple] = []
+        for kind, _, payload in sorted(events, key=lambda e: (e[0] == EV_ARRIVAL, e[1], e[0])):
+            if kind == EV_ARRIVAL:
+                self.q_v.append(payload)
+            elif kind == EV_VISION_DONE:
+                self.vision_running = None
+                self.prefill_wait.append(payload)
+                self.last_pass = "front"
+            elif kind == EV_PREFILL_DONE:
+                self.prefill_running = None
+                self.last_pass = "front"
+                self._emit(payload, out)
+            elif kind == EV_DECODE_DONE:
+                self.decode_running = None
+                self.last_pass = "decode"
+                for rid in payload:
+                    self._emit(rid, out)
+        npend = self.n_pend()
+        if self.p.mode == SERIAL:
+            self._dispatch_serial(out)
+        else:
+            self._dispatch_corun(out, npend)
+        self.log.extend(out)
+        return out
+
+    def _dispatch_front(self, out, ctx_fn):
+        if self.prefill_wait:
+            rid = self.prefill_wait.popleft()
+            self.prefill_running = rid
+            ctx, s = ctx_fn(CTX_DP)
+            out.append((D_PREFILL, (rid,), ctx, s))
+        elif self.q_v:
+            rid = self.q_v.popleft()
+            self.vision_running = rid
+            ctx, s = ctx_fn(CTX_DV)
+            out.append((D_VISION, (rid,), ctx, s))
+
+    def _dispatch_decode(self, out, ctx, s):
+        batch = self.q_d[: self.p.b_max]
+        self.q_d = self.q_d[self.p.b_max:]
+        self.decode_running = batch
+        out.append((D_DECODE, tuple(batch), ctx, s))
+
+    def _dispatch_corun(self, out, npend):
+        if not self.front_running():
+            has_decode = self.decode_running is not None or bool(self.q_d)
+            self._dispatch_front(out, lambda c: (c, self.split(c, npend)) if has_decode else (CTX_SOLO, 0))
+        if self.decode_running is None and self.q_d:
+            if self.vision_running is not None:
+                ctx = CTX_DV
+            elif self.prefill_running is not None:
+                ctx = CTX_DP
+            else:
+                ctx = CTX_SOLO
+            self._dispatch_decode(out, ctx, self.split(ctx, npend))
+
+    def _dispatch_serial(self, out):
+        if self.busy():
+            return
+        front_ready = bool(self.prefill_wait or self.q_v)
+        dec_ready = bool(self.q_d)
+        if front_ready and (not dec_ready or self.last_pass == "decode"):
+            self._dispatch_front(out, lambda c: (CTX_SOLO, 0))
+        elif dec_ready:
+            self._dispatch_decode(out, CTX_SOLO, self.p.total_sms)
+
+
+# ------------------------------------------------------------------ virtual-time simulation
+@dataclass
+class SimCurves:
+    """Durations in ns.  Split-indexed tables give the co-run time with decode on s SMs;
+    *_solo are the all-SM times.  Decode may grow linearly with batch: t*(1+beta(B-1))."""
+    splits: list[int]
+    t_v: list[int]
+    t_p: list[int]
+    t_d_dv: list[int]
+    t_d_dp: list[int]
+    t_v_solo: int
+    t_p_solo: int
+    t_d_solo: int
+    beta: float = 0.0
+
+    def idx(self, s):
+        return self.splits.index(s)
+
+
+@dataclass
+class SimRequest:
+    rid: int
+    arrival_ns: int
+    gen_len: int
+    vis_scale: float = 1.0
+    pre_scale: float = 1.0
+
+
+def simulate(policy: Policy, curves: SimCurves, requests: list[SimRequest]):
+    """Run Alg. 1 in virtual integer-ns time.  Returns (decision log, token times per rid)."""
+    alg = Alg1(policy)
+    for r in requests:
+        alg.add_request(r.rid, r.gen_len)
+    byid = {r.rid: r for r in requests}
+    arrivals = sorted(requests, key=lambda r: (r.arrival_ns, r.rid))
+    ai = 0
+    pending: list[tuple] = []     # (t_done, kind, key, payload)
+    tokens: dict[int, list[int]] = {r.rid: [] for r in requests}
+    done = 0
+    t = 0
+    while done < len(requests):
+        cands = [p[0] for p in pending]
+        if ai < len(arrivals):
+            cands.append(arrivals[ai].arrival_ns)
+        t = min(cands)
+        evs = []
+        for p in [p for p in pending if p[0] == t]:
+            pending.remove(p)
+            evs.append(p[1:])
+        while ai < len(arrivals) and arrivals[ai].arrival_ns == t:
+            evs.append((EV_ARRIVAL, arrivals[ai].rid, arrivals[ai].rid))
+            ai += 1
+        for kind, _, payload in evs:
+            if kind == EV_PREFILL_DONE:
+                tokens[payload].append(t)
+            elif kind == EV_DECODE_DONE:
+                for rid in payload:
+                    tokens[rid].append(t)
+        for kind, rids, ctx, s in alg.tick(evs):
+            if kind == D_FINISH:
+                done += 1
+                continue
+            if kind == D_VISION:
+                base = curves.t_v_solo if ctx == CTX_SOLO else curves.t_v[curves.idx(s)]
+                dur = int(round(base * byid[rids[0]].vis_scale))
+                pending.append((t + dur, EV_VISION_DONE, rids[0], rids[0]))
+            elif kind == D_PREFILL:
+                base = curves.t_p_solo if ctx == CTX_SOLO else curves.t_p[curves.idx(s)]
+                dur = int(round(base * byid[rids[0]].pre_scale))
+                pending.append((t + dur, EV_PREFILL_DONE, rids[0], rids[0]))
+            else:
+                if ctx == CTX_SOLO:
+                    base = curves.t_d_solo
+                elif ctx == CTX_DV:
+                    base = curves.t_d_dv[curves.idx(s)]
+                else:
+                    base = curves.t_d_dp[curves.idx(s)]
+                dur = int(round(base * (1.0 + curves.beta * (len(rids) - 1))))
+                pending.append((t + dur, EV_DECODE_DONE, min(rids), list(rids)))
+    return alg.log, tokens
