@@ -1,0 +1,248 @@
+/* nova.h -- C ABI of the Nova co-execution engine (libnova.so).
+ *
+ * What it does: serves agentic-VLM requests (a screenshot + an instruction,
+ * PAPER.md §II-C) through three stages -- vision encode, LLM prefill,
+ * LLM greedy decode (§II-A) -- that co-execute on disjoint SM
+ * partitions of one B200 (§III-B).  A request scheduler implements
+ * Algorithm 1; the decode share of the SMs follows Eq. 5
+ * with SM_op from the Eq. 1-3 planner; ViT weights may
+ * be offloaded layer-wise with the Eq. 7 swap-in ring (§III-E).
+ * The paper's libsmctrl stream masks are replaced by CUDA green
+ * contexts: one family of partitions built at nova_finalize, selected per
+ * forward pass, never rebuilt.
+ *
+ * Conventions
+ *   - Every call returns nova_status (0 = NOVA_OK, negative = error); no C++
+ *     exception crosses the ABI.  nova_last_error(e) returns an engine-owned,
+ *     NUL-terminated message for the last failure on that engine (NULL engine:
+ *     the last creation error).
+ *   - Ownership: the caller owns every pointer it passes.  Inputs are copied
+ *     (or H2D-enqueued from the caller's memory) before the call returns.
+ *     Device buffers in nova_buffers are allocated by the caller (e.g. torch)
+ *     and BORROWED until nova_destroy; they must stay alive and untouched.
+ *   - Threading: nova_submit may be called from any thread.  All other calls
+ *     on one engine must come from a single driver thread.
+ *   - After a CUDA error the engine latches FAILED: later calls return
+ *     NOVA_E_STATE.  Sizes/shapes outside the configured maxima -> NOVA_E_INVAL.
+ *   - Times are int64 nanoseconds of CLOCK_MONOTONIC (GPU backend) or of the
+ *     virtual clock (Sim backend).
+ */
+#ifndef NOVA_H
+#define NOVA_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nova_engine nova_engine;
+typedef int32_t nova_status;
+enum {
+  NOVA_OK = 0,
+  NOVA_E_INVAL = -1,     /* bad argument / shape outside configured maxima        */
+  NOVA_E_NOMEM = -2,     /* buffers too small / host allocation failed            */
+  NOVA_E_CUDA = -3,      /* CUDA runtime or driver error (engine latches FAILED)   */
+  NOVA_E_AGAIN = -4,     /* no free request slot: retry after requests finish     */
+  NOVA_E_NOTFOUND = -5,  /* unknown request id / tensor name                       */
+  NOVA_E_PARTITION = -6, /* SM budget not realisable at the partition granularity  */
+  NOVA_E_STATE = -7      /* engine FAILED, or call out of order                    */
+};
+
+/* Model shape (Qwen2-VL family; SURVEY.md §8 shape legend). */
+typedef struct {
+  int32_t vit_depth, vit_dim, vit_heads, vit_mlp, patch, temporal_patch, merge, in_ch;
+  int32_t llm_layers, llm_dim, llm_heads, llm_kv_heads, head_dim, llm_ffn, vocab, tie_embed;
+  int32_t mrope_section[3];
+  float vit_theta, llm_theta, ln_eps, rms_eps;
+} nova_model_config;
+
+enum { NOVA_BACKEND_GPU = 0, NOVA_BACKEND_SIM = 1 };
+
+typedef struct {
+  int32_t backend;              /* NOVA_BACKEND_GPU or NOVA_BACKEND_SIM (virtual time, no GPU)  */
+  int32_t device;               /* CUDA device ordinal                                         */
+  int32_t max_requests;         /* concurrent requests (slots)                                 */
+  int32_t max_decode_batch;     /* B_max <= 16                                                 */
+  int32_t kv_pages;             /* KV pool size in 64-token pages                              */
+  int32_t max_patches;          /* max ViT patches per image (N)                               */
+  int32_t max_prompt;           /* max prompt tokens                                           */
+  int32_t max_gen;              /* max generated tokens per request (gen_len)                  */
+  int32_t vit_resident_layers;  /* K physical ViT layer slots (Eq. 7); 0 = all layers resident */
+  int32_t use_green_ctx;        /* 1: SM partitions via green contexts; 0: primary context only */
+  int32_t debug_keep_logits;    /* keep every step's f32 logits for nova_debug_logits          */
+  int32_t reserved;
+} nova_engine_config;
+
+/* Device buffer sizes the caller must provide (GPU backend); pinned_host_bytes is
+ * allocated by the engine itself (offload arena). */
+nova_status nova_query_memory(const nova_model_config* m, const nova_engine_config* c, uint64_t* weights_bytes,
+                              uint64_t* kv_bytes, uint64_t* workspace_bytes, uint64_t* pinned_host_bytes);
+
+typedef struct {
+  void* weights_dev;   uint64_t weights_bytes;    /* engine weight layout (filled by nova_load_tensor) */
+  void* kv_dev;        uint64_t kv_bytes;         /* paged KV pool                                      */
+  void* workspace_dev; uint64_t workspace_bytes;  /* activations of the three roles                      */
+} nova_buffers;
+
+/* Create an engine.  GPU backend: buffers required; Sim backend: buffers may be NULL. */
+nova_status nova_create(const nova_model_config* m, const nova_engine_config* c, const nova_buffers* b,
+                        nova_engine** out);
+/* Place one weight tensor, given by its HF Qwen2-VL state_dict name, as bf16 bits
+ * (row-major [out][in]); src is host (src_on_device = 0) or device memory.  q/k/v
+ * are fused and gate/up interleaved by the engine (layout only, no arithmetic). */
+nova_status nova_load_tensor(nova_engine* e, const char* name, const void* src, uint64_t nbytes,
+                             int32_t src_on_device);
+/* After all tensors: preload the K offload slots, build the partition family,
+ * start the role workers.  The engine is then ready for nova_submit. */
+nova_status nova_finalize(nova_engine* e);
+nova_status nova_destroy(nova_engine* e);
+const char* nova_last_error(nova_engine* e);
+
+/* SMs of the device, partition granularity (8 on sm_100 green contexts), and the
+ * number of decode splits s in {g, 2g, ..., (n_groups-1) g}. */
+nova_status nova_query_sms(nova_engine* e, int32_t* total_sms, int32_t* granularity, int32_t* n_splits);
+
+/* ------------------------------------------------------------------ requests */
+typedef struct {
+  const uint16_t* pixels_bf16; /* [3][height][width] bf16 bits, host memory                    */
+  int32_t height, width;       /* multiples of patch * merge (28)                               */
+  const int32_t* prompt_ids;   /* host [n_prompt], each < vocab                                 */
+  int32_t n_prompt;
+  int32_t gen_len;             /* >= 1 tokens to emit, counting the prefill token (no EOS)      */
+  int64_t arrival_ns;          /* 0 = now (GPU); virtual arrival time (Sim)                     */
+  uint64_t user_tag;
+  /* Sim backend only: duration scale factors for this request's front passes */
+  float sim_vision_scale, sim_prefill_scale;
+} nova_request;
+/* Thread-safe.  Copies the prompt, enqueues the pixel H2D copy; returns the id. */
+nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* req_id);
+
+/* ------------------------------------------------------------------ partition policy */
+enum { NOVA_MODE_SERIAL = 0, NOVA_MODE_STATIC = 1, NOVA_MODE_ADAPTIVE = 2 };
+enum { NOVA_CTX_DV = 0, NOVA_CTX_DP = 1, NOVA_CTX_SOLO = 2 };
+typedef struct {
+  int32_t mode;                        /* NOVA_MODE_*                                           */
+  int32_t sm_decode_dv, sm_decode_dp;  /* STATIC: decode SMs while co-running with vision/prefill */
+  int32_t sm_op_dv, sm_op_dp, sm_min;  /* ADAPTIVE (Eq. 5)                                       */
+  float alpha_dv, alpha_dp;
+  int32_t b_max;                       /* decode batch cap (<= max_decode_batch)                 */
+} nova_partition_policy;
+/* Takes effect at each role's next forward pass.  `applied` (may be NULL)
+ * receives the values rounded down to the granularity.  NOVA_E_PARTITION if a
+ * budget rounds to 0 or leaves the front stage no SM group. */
+nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, nova_partition_policy* applied);
+
+/* ------------------------------------------------------------------ scheduler tick */
+typedef struct {
+  int32_t events;        /* completions + arrivals processed in this tick   */
+  int32_t dispatched;    /* passes launched in this tick                    */
+  int32_t n_pending;     /* N_pend (vision/prefill queued or running)       */
+  int32_t sm_decode;     /* decode SMs of the last decode dispatch          */
+  int32_t context;       /* NOVA_CTX_* of the last decode dispatch          */
+  int32_t decode_batch;  /* size of the last decode batch                   */
+  int32_t active;        /* requests admitted and not finished              */
+  int32_t finished;      /* requests finished so far                        */
+  int64_t now_ns;        /* tick time                                        */
+} nova_step_info;
+/* One Algorithm 1 iteration: process completed passes and arrivals, recount
+ * N_pend, apply Eq. 5, dispatch.  Blocks up to max_wait_us for an event when
+ * there is none (GPU); the Sim backend advances virtual time to the next event. */
+nova_status nova_step(nova_engine* e, int64_t max_wait_us, nova_step_info* out);
+
+enum { NOVA_TOK_FIRST = 1, NOVA_TOK_LAST = 2 };
+typedef struct {
+  uint64_t req_id;
+  int32_t index;     /* 0 = the prefill token */
+  int32_t token;
+  int64_t t_emit_ns; /* time the host observed the token */
+  int32_t flags;     /* NOVA_TOK_FIRST | NOVA_TOK_LAST   */
+  int32_t pad;
+} nova_token;
+/* Drain up to cap emitted tokens (FIFO). */
+nova_status nova_poll_tokens(nova_engine* e, nova_token* buf, int32_t cap, int32_t* n_out);
+
+typedef struct {
+  int64_t arrival, vis_start, vis_end, pre_start, pre_end, first_tok, last_tok;
+  int32_t split_at_vis, split_at_pre; /* decode SMs at the front dispatch (0 = front alone) */
+  int32_t n_tokens, finished;
+} nova_req_stats;
+nova_status nova_request_stats(nova_engine* e, uint64_t req_id, nova_req_stats* out);
+
+/* Decision log of Algorithm 1 (for replay against the oracle). */
+enum { NOVA_DEC_VISION = 0, NOVA_DEC_PREFILL = 1, NOVA_DEC_DECODE = 2, NOVA_DEC_FINISH = 3 };
+enum { NOVA_EV_VISION_DONE = 0, NOVA_EV_PREFILL_DONE = 1, NOVA_EV_DECODE_DONE = 2, NOVA_EV_ARRIVAL = 3 };
+typedef struct {
+  int64_t t_ns;
+  int32_t tick;      /* tick sequence number                                     */
+  int32_t is_event;  /* 1: an input event of the tick, 0: a decision              */
+  int32_t kind;      /* NOVA_EV_* or NOVA_DEC_*                                  */
+  int32_t ctx;       /* decisions: NOVA_CTX_*                                     */
+  int32_t s_dec;     /* decisions: decode SMs (0 = front alone)                   */
+  int32_t n_ids;
+  uint64_t ids[16];  /* request ids (batch for decode)                            */
+} nova_log_record;
+/* Copy log records [start, start + cap) ; n_out = records copied; total = all records. */
+nova_status nova_decision_log(nova_engine* e, int64_t start, nova_log_record* buf, int32_t cap, int32_t* n_out,
+                              int64_t* total);
+
+/* ------------------------------------------------------------------ debug / parity */
+/* f32 logits of token `index` of a request (needs debug_keep_logits). */
+nova_status nova_debug_logits(nova_engine* e, uint64_t req_id, int32_t index, float* out, int32_t vocab);
+/* Teacher forcing: decode step k (k >= 1) consumes tokens[k-1] instead of the argmax
+ * of step k-1.  Must be called right after nova_submit. */
+nova_status nova_debug_force_tokens(nova_engine* e, uint64_t req_id, const int32_t* tokens, int32_t n);
+
+/* ------------------------------------------------------------------ curves + planner */
+/* Time one forward pass with the SM split s (decode SMs; front gets the rest,
+ * s = 0: solo on all SMs).  stage 0 = vision (grid gh x gw), 1 = prefill
+ * (S = n_v + n_prompt), 2 = decode iteration (batch B at context ctx).  With
+ * corun = 1 the front stage runs while decode iterations (batch B) loop on the
+ * complementary partition; out_ms[0] = front pass, out_ms[1] = mean decode
+ * iteration.  Uses internal profiling slots; do not call while serving. */
+nova_status nova_time_pass(nova_engine* e, int32_t stage, int32_t s, int32_t gh, int32_t gw, int32_t n_prompt,
+                           int32_t B, int32_t ctx, int32_t corun, int32_t iters, double* out_ms);
+
+typedef struct {
+  int32_t n;             /* number of splits                                   */
+  const int32_t* s;      /* decode SMs per split (ascending)                   */
+  const double* t_v;     /* ms, vision pass on the front partition (total - s) */
+  const double* t_p;     /* ms, prefill pass on the front partition            */
+  const double* t_d_dv;  /* ms, decode iteration on s SMs co-running vision    */
+  const double* t_d_dp;  /* ms, decode iteration on s SMs co-running prefill   */
+  double t_d_full;       /* ms, decode iteration alone on all SMs              */
+} nova_curves;
+typedef struct {
+  int32_t s_v, s_p;      /* P_v, P_p: decode SMs in the two co-run contexts     */
+  double e2e_ms;         /* Eq. 1                                               */
+  double thr_rps;        /* Eq. 4                                               */
+  int32_t on_frontier;   /* Pareto frontier membership                          */
+  int32_t pad;
+} nova_plan_point;
+/* Eqs. 1-4 over all split pairs, Pareto frontier, Eq. 3 argmin (ties -> more decode
+ * SMs), SM_min (smallest s with co-run decode <= tau * t_d_full) and
+ * alpha = (SM_op - SM_min) / 3 (R9-R12).  Pure host function. */
+nova_status nova_plan(const nova_curves* c, double gen_len, double tau, nova_plan_point* pts, int32_t cap,
+                      int32_t* n_out, nova_plan_point* best, int32_t* sm_min_out, double* alpha_dv_out,
+                      double* alpha_dp_out);
+/* Eq. 5: max(SM_min, floor_g(SM_op - alpha (max(N_pend, 1) - 1))). */
+int32_t nova_adaptive_sm(int32_t sm_op, int32_t sm_min, double alpha, int32_t n_pending, int32_t granularity);
+/* Eq. 7 and Eq. 8 (offload ring). */
+int32_t nova_next_logical_layer(int32_t cur, int32_t K, int32_t L);
+double nova_required_bandwidth(double bytes, double forward_s, int32_t L, int32_t K);
+
+/* Sim backend: per-split durations (ns) the virtual executor uses; same layout as
+ * nova_curves (t_v/t_p indexed by decode split, *_solo on all SMs). beta: decode
+ * time grows by (1 + beta (B - 1)). */
+typedef struct {
+  int32_t n;
+  const int32_t* s;
+  const int64_t *t_v, *t_p, *t_d_dv, *t_d_dp;
+  int64_t t_v_solo, t_p_solo, t_d_solo;
+  double beta;
+  int32_t total_sms, granularity;
+} nova_sim_curves;
+nova_status nova_sim_set_curves(nova_engine* e, const nova_sim_curves* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

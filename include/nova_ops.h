@@ -1,0 +1,103 @@
+/* nova_ops.h -- C ABI of the individual sm_100a stage kernels (libnova.so).
+ *
+ * These are the building blocks of the Nova stage programs (vision encode,
+ * LLM prefill, LLM decode; §II-A, Table resource_stage
+ * P:130-145), exposed one by one for per-kernel parity tests against the CPU
+ * oracle and for roofline micro-benchmarks.  The engine ABI is nova.h.
+ *
+ * Conventions (all calls):
+ *   - Every pointer is a DEVICE pointer owned by the caller (allocated e.g. by
+ *     torch); the call only enqueues work on `stream` (a cudaStream_t passed as
+ *     void*, NULL = legacy default stream) and never synchronises.
+ *   - Matrices are row-major with leading dimensions in ELEMENTS; "bf16" is
+ *     IEEE bfloat16 bits (uint16), "f32" IEEE float.  Weights are [out][in].
+ *   - Return 0 on success, or the negative CUDA error code of the failed
+ *     launch (-1 = cudaErrorInvalidValue for unsupported shapes).  Errors of
+ *     the asynchronous execution surface on the caller's next synchronisation.
+ */
+#ifndef NOVA_OPS_H
+#define NOVA_OPS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Epilogues shared by GEMM and GEMV:  R = A . W^T + bias  (f32 accumulate)          */
+enum {
+  NOVA_EPI_BF16 = 0,          /* C bf16 = R                                          */
+  NOVA_EPI_BF16_QGELU = 1,    /* C bf16 = R * sigmoid(1.702 R)     (ViT MLP, QuickGELU) */
+  NOVA_EPI_BF16_GELU = 2,     /* C bf16 = GELU_erf(R)              (patch merger)      */
+  NOVA_EPI_BF16_SILUMUL = 3,  /* W rows interleaved [16 gate | 16 up]*; C[:, N/2] bf16 = silu(gate) * up */
+  NOVA_EPI_F32_RESID = 4,     /* C f32 += R                        (residual add)     */
+  NOVA_EPI_F32_STORE = 5      /* C f32 = R                                            */
+};
+
+/* Dense linear of the vision encoder / prefill: tcgen05 +
+ * TMEM + TMA persistent GEMM.  A [M][K] bf16 (lda), W [N][K] bf16 (ldw), bias
+ * bf16 [N] or NULL, C per epilogue (ldc).  Requires N % 64 == 0, lda/ldw/ldc % 8
+ * == 0; M, K arbitrary (TMA zero-fills tails).  max_ctas = SM budget (grid cap).
+ * Bitwise independent of max_ctas. */
+int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
+                 int K, int epi, int max_ctas, void* stream);
+
+/* Decode linear (a7): Y[b][n] = sum_k X[b][k] W[n][k] (+bias) for B <= 16 rows.
+ * X bf16 (x_f32 = 0) or f32 (x_f32 = 1).  N % 32 == 0, K % 32 == 0, ldx % 8 == 0.
+ * Epilogues NOVA_EPI_BF16 / _SILUMUL / _F32_RESID / _F32_STORE.  Row b of Y is
+ * bitwise independent of B and of the other rows. */
+int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias,
+                 int B, int epi, void* stream);
+
+/* Flash attention (a5 ViT: causal = 0, KV = H; a6 prefill: causal = 1, GQA).
+ * qkv [S][(H + 2 KV) hd] bf16 (ld): q heads, then k heads, then v heads; out
+ * [S][H hd] bf16 (ldo); scale hd^-1/2; hd in {16, 32, 64, 80, 128}. */
+int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int S, int H, int KV, int hd, int causal,
+                       void* stream);
+
+/* Row descriptor of one decode request (device memory, 16 bytes). */
+typedef struct {
+  int32_t slot; /* request slot: row of block_tables and of last_tok       */
+  int32_t ctx;  /* tokens already cached = cache index of this step's token */
+  int32_t pos;  /* M-RoPE position of this step's token (t = h = w)         */
+  int32_t pad;
+} nova_decode_row;
+
+/* Paged decode attention (a7).  Keys 0..ctx (inclusive) of each row.  kv_pool
+ * bf16 [layers][n_pages][2][KV][64][hd]; block_tables int32 [slots][max_pages];
+ * ws f32 workspace of B*H*ceil((max_ctx+1)/256)*(hd+2) floats. */
+int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
+                        int H, int KV, int hd, const int32_t* block_tables, int max_pages, const nova_decode_row* rows,
+                        int B, int max_ctx, float* ws, void* stream);
+
+/* LayerNorm (ViT, mean/biased variance) and RMSNorm (LLM) of f32 rows [M][d]. */
+int nova_op_layernorm(const float* x, int ldx, const void* gamma, const void* beta, void* y, int ldy, int M, int d,
+                      float eps, void* stream);
+int nova_op_rmsnorm(const float* x, int ldx, const void* gamma, void* y, int y_f32, int ldy, int M, int d, float eps,
+                    void* stream);
+
+/* Patchify (a1): pixels bf16 [C][H][W] -> X0 bf16 [N][C*T*P*P], merge-group-major rows. */
+int nova_op_patchify(const void* pix, int C, int H, int W, int P, int T, int merge, void* X0, void* stream);
+
+/* ViT 2D RoPE in place on q, k of qkv [N][3][heads][hd]; image grid gw patches wide. */
+int nova_op_vit_rope(void* qkv, int N, int heads, int hd, int gw, int merge, float theta, void* stream);
+
+/* LLM M-RoPE in place on q, k of nrows qkv rows, then K and V into the paged
+ * cache.  Prefill: rows == NULL, positions pos3 int32 [3][ld_pos], cache index
+ * ctx0 + r of request `slot`.  Decode: positions / cache index from rows[r]. */
+int nova_op_llm_rope_kv(void* qkv, int ld, int nrows, int H, int KV, int hd, float theta, int sec0, int sec1,
+                        const int32_t* pos3, int ld_pos, const nova_decode_row* rows, int slot, int ctx0,
+                        void* kv_pool, int layer, int n_pages, const int32_t* block_tables, int max_pages,
+                        void* stream);
+
+/* Embedding gather into f32 rows: ids[r] (or last_tok[rows[r].slot] when ids == NULL). */
+int nova_op_embed(const void* table, int d, const int32_t* ids, const nova_decode_row* rows, const int32_t* last_tok,
+                  float* out, int ldo, int n, void* stream);
+
+/* Greedy pick: argmax of each f32 row (ties -> lowest index) -> out_tok[r]; also
+ * last_tok[rows[r].slot] (rows != NULL) or last_tok[single_slot] (>= 0). */
+int nova_op_argmax(const float* logits, int ldl, int V, int n, int32_t* out_tok, const nova_decode_row* rows,
+                   int32_t* last_tok, int single_slot, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

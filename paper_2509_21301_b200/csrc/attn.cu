@@ -1,0 +1,345 @@
+// Attention kernels (PAPER.md P:139-141 Table resource_stage "Attention" row; the
+// paper used FlashInfer on sm_86).
+//
+// flash_attn: ViT bidirectional MHA (a5) and LLM prefill causal GQA (a6) over a
+//   fused qkv buffer, FA2-style online softmax with warp-level mma.sync
+//   (m16n8k16, bf16 in / f32 accumulate).  64 query rows per CTA (16 per warp),
+//   64-key K/V tiles double-buffered through cp.async.
+// decode_attn: paged GQA decode attention (a7): one CTA per (request, KV head,
+//   256-token chunk); the GQA group shares every K/V load; chunk partials are
+//   merged by a second kernel in fixed chunk order (deterministic; the chunking
+//   depends only on the context length).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nova {
+namespace {
+
+constexpr float LOG2E = 1.4426950408889634f;
+
+template <int HD>
+struct FaCfg {
+  static constexpr int BQ = 64, BKV = 64, HDP = HD + 8;
+  static constexpr int SMEM = (BQ + 4 * BKV) * HDP * 2;
+};
+
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(128) flash_attn_kernel(const bf16* __restrict__ qkv, int ld, bf16* __restrict__ out,
+                                                         int ldo, int S, int H, int KV, float scale_log2) {
+  using C = FaCfg<HD>;
+  constexpr int HDP = C::HDP, BKV = C::BKV;
+  constexpr int KT = HD / 16;  // k-steps of QK^T
+  constexpr int DT = HD / 8;   // n-tiles of O
+  extern __shared__ __align__(16) uint8_t fa_smem[];
+  bf16* sQ = reinterpret_cast<bf16*>(fa_smem);
+  bf16* sK = sQ + C::BQ * HDP;  // [2][BKV][HDP]
+  bf16* sV = sK + 2 * BKV * HDP;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int qt = blockIdx.x, h = blockIdx.y;
+  const int kvh = h / (H / KV);
+  const int q0 = qt * C::BQ;
+  const bf16* qbase = qkv + (size_t)h * HD;
+  const bf16* kbase = qkv + (size_t)(H + kvh) * HD;
+  const bf16* vbase = qkv + (size_t)(H + KV + kvh) * HD;
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+
+  for (int i = tid; i < C::BQ * CH; i += 128) {
+    const int r = i / CH, cc = i % CH;
+    const int row = q0 + r;
+    cp_async16(sQ + r * HDP + cc * 8, qbase + (size_t)(row < S ? row : 0) * ld + cc * 8, row < S);
+  }
+  auto load_kv = [&](int tile, int buf) {
+    const int k0 = tile * BKV;
+    for (int i = tid; i < BKV * CH; i += 128) {
+      const int r = i / CH, cc = i % CH;
+      const int row = k0 + r;
+      const size_t off = (size_t)(row < S ? row : 0) * ld + cc * 8;
+      cp_async16(sK + (buf * BKV + r) * HDP + cc * 8, kbase + off, row < S);
+      cp_async16(sV + (buf * BKV + r) * HDP + cc * 8, vbase + off, row < S);
+    }
+  };
+  const int n_tiles_all = (S + BKV - 1) / BKV;
+  const int n_tiles = CAUSAL ? min(n_tiles_all, (q0 + C::BQ + BKV - 1) / BKV) : n_tiles_all;
+  load_kv(0, 0);
+  cp_async_commit();
+
+  float o[DT][4];
+#pragma unroll
+  for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-1e30f, -1e30f}, l_r[2] = {0.f, 0.f};
+  uint32_t qa[KT][4];
+  const int row_a = q0 + warp * 16 + g, row_b = row_a + 8;
+
+  for (int t = 0; t < n_tiles; ++t) {
+    if (t + 1 < n_tiles) load_kv(t + 1, (t + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk)
+        ldmatrix_x4(qa[kk], smem_u32(sQ + (warp * 16 + (lane & 15)) * HDP + kk * 16 + (lane >> 4) * 8));
+    }
+    const bf16* kt = sK + (t & 1) * BKV * HDP;
+    const bf16* vt = sV + (t & 1) * BKV * HDP;
+    float s[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk) {
+        uint32_t b[2];
+        ldmatrix_x2(b, smem_u32(kt + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
+        mma_bf16_16816(s[nt], qa[kk], b);
+      }
+    }
+    // mask + online softmax (rows row_a: s[.][0..1], row_b: s[.][2..3])
+    const int k0 = t * BKV;
+    float mx[2] = {-1e30f, -1e30f};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int key = k0 + nt * 8 + 2 * c + (j & 1);
+        const int row = (j < 2) ? row_a : row_b;
+        bool valid = key < S;
+        if (CAUSAL) valid = valid && key <= row;
+        const float v = valid ? s[nt][j] * scale_log2 : -1e30f;
+        s[nt][j] = v;
+        mx[j >> 1] = fmaxf(mx[j >> 1], v);
+      }
+    }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(m_r[r], mx[r]);
+      corr[r] = exp2f(m_r[r] - mn);
+      m_r[r] = mn;
+    }
+    float ls[2] = {0.f, 0.f};
+    uint32_t pa[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] - m_r[0]), p1 = exp2f(s[nt][1] - m_r[0]);
+      const float p2 = exp2f(s[nt][2] - m_r[1]), p3 = exp2f(s[nt][3] - m_r[1]);
+      ls[0] += p0 + p1;
+      ls[1] += p2 + p3;
+      const int kk = nt >> 1, hi = nt & 1;
+      pa[kk][hi * 2 + 0] = pack_bf16(p0, p1);
+      pa[kk][hi * 2 + 1] = pack_bf16(p2, p3);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) l_r[r] = l_r[r] * corr[r] + ls[r];
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      o[dt][0] *= corr[0];
+      o[dt][1] *= corr[0];
+      o[dt][2] *= corr[1];
+      o[dt][3] *= corr[1];
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      // A fragment order a0:(g, k0-7) a1:(g+8, k0-7) a2:(g, k8-15) a3:(g+8, k8-15)
+      const uint32_t a[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        uint32_t b[2];
+        ldmatrix_x2_trans(b, smem_u32(vt + (kk * 16 + (lane & 15)) * HDP + dt * 8));
+        mma_bf16_16816(o[dt], a, b);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
+  const float inv_a = 1.f / l_r[0], inv_b = 1.f / l_r[1];
+#pragma unroll
+  for (int dt = 0; dt < DT; ++dt) {
+    const int col = h * HD + dt * 8 + 2 * c;
+    if (row_a < S)
+      *reinterpret_cast<uint32_t*>(out + (size_t)row_a * ldo + col) = pack_bf16(o[dt][0] * inv_a, o[dt][1] * inv_a);
+    if (row_b < S)
+      *reinterpret_cast<uint32_t*>(out + (size_t)row_b * ldo + col) = pack_bf16(o[dt][2] * inv_b, o[dt][3] * inv_b);
+  }
+}
+
+template <int HD>
+cudaError_t fa_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int causal, cudaStream_t s) {
+  const float sl2 = LOG2E / sqrtf((float)HD);
+  dim3 grid((S + 63) / 64, H), block(128);
+  const int smem = FaCfg<HD>::SMEM;
+  if (causal) {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(flash_attn_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      set = true;
+    }
+    flash_attn_kernel<HD, true><<<grid, block, smem, s>>>(qkv, ld, out, ldo, S, H, KV, sl2);
+  } else {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(flash_attn_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      set = true;
+    }
+    flash_attn_kernel<HD, false><<<grid, block, smem, s>>>(qkv, ld, out, ldo, S, H, KV, sl2);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- decode attention
+constexpr int DCHUNK = 256;
+constexpr int MAXG = 8;  // max GQA group size
+
+template <int HD>
+__global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __restrict__ qkv, int ld,
+                                                              const bf16* __restrict__ pool, int layer, int n_pages,
+                                                              int H, int KV, const int* __restrict__ bt, int max_pages,
+                                                              const DecodeRow* __restrict__ rows, float* __restrict__ ws,
+                                                              int n_chunks, float scale_log2) {
+  const int b = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z;
+  const int G = H / KV;
+  const DecodeRow rr = rows[b];
+  const int L = rr.ctx + 1;
+  const int j0 = ch * DCHUNK;
+  if (j0 >= L) return;
+  const int nj = min(DCHUNK, L - j0);
+  __shared__ float sq[MAXG][HD];
+  __shared__ float sp[MAXG][DCHUNK];
+  __shared__ float smax[MAXG], ssum[MAXG];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < G * HD; i += DCHUNK) {
+    const int gg = i / HD, d = i % HD;
+    sq[gg][d] = __bfloat162float(qkv[(size_t)b * ld + (size_t)(kvh * G + gg) * HD + d]) * scale_log2;
+  }
+  __syncthreads();
+  const size_t kv_stride_page = (size_t)2 * KV * 64 * HD;
+  const bf16* lbase = pool + (size_t)layer * n_pages * kv_stride_page;
+  const int* btr = bt + (size_t)rr.slot * max_pages;
+  if (tid < nj) {
+    const int j = j0 + tid;
+    const bf16* kp = lbase + (size_t)btr[j >> 6] * kv_stride_page + ((size_t)kvh * 64 + (j & 63)) * HD;
+    float acc[MAXG];
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg) acc[gg] = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < HD; d += 8) {
+      uint4 u = *reinterpret_cast<const uint4*>(kp + d);
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = unpack_bf16(w[e]);
+#pragma unroll
+        for (int gg = 0; gg < MAXG; ++gg)
+          if (gg < G) acc[gg] += f.x * sq[gg][d + 2 * e] + f.y * sq[gg][d + 2 * e + 1];
+      }
+    }
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg)
+      if (gg < G) sp[gg][tid] = acc[gg];
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int gg = warp; gg < G; gg += DCHUNK / 32) {
+    float m = -1e30f;
+    for (int j = lane; j < nj; j += 32) m = fmaxf(m, sp[gg][j]);
+    m = warp_max(m);
+    float sum = 0.f;
+    for (int j = lane; j < nj; j += 32) {
+      const float p = exp2f(sp[gg][j] - m);
+      sp[gg][j] = p;
+      sum += p;
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) {
+      smax[gg] = m;
+      ssum[gg] = sum;
+    }
+  }
+  __syncthreads();
+  // o[g][d] = sum_j p[g][j] v[j][d]
+  const size_t wbase = ((size_t)b * H + kvh * G) * n_chunks + ch;
+  for (int i = tid; i < G * HD; i += DCHUNK) {
+    const int gg = i / HD, d = i % HD;
+    float acc = 0.f;
+    for (int j = 0; j < nj; ++j) {
+      const int jj = j0 + j;
+      const bf16* vp =
+          lbase + (size_t)btr[jj >> 6] * kv_stride_page + ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + d;
+      acc += sp[gg][j] * __bfloat162float(*vp);
+    }
+    float* w = ws + (wbase + (size_t)gg * n_chunks) * (HD + 2);
+    w[2 + d] = acc;
+    if (d == 0) {
+      w[0] = smax[gg];
+      w[1] = ssum[gg];
+    }
+  }
+}
+
+template <int HD>
+__global__ void decode_attn_combine(const float* __restrict__ ws, const DecodeRow* __restrict__ rows, bf16* out,
+                                    int ldo, int H, int n_chunks) {
+  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  const int L = rows[b].ctx + 1;
+  const int nc = (L + DCHUNK - 1) / DCHUNK;
+  const float* w = ws + ((size_t)b * H + h) * n_chunks * (HD + 2);
+  float M = -1e30f;
+  for (int c = 0; c < nc; ++c) M = fmaxf(M, w[c * (HD + 2)]);
+  float num = 0.f, den = 0.f;
+  for (int c = 0; c < nc; ++c) {
+    const float f = exp2f(w[c * (HD + 2)] - M);
+    den += f * w[c * (HD + 2) + 1];
+    if (d < HD) num += f * w[c * (HD + 2) + 2 + d];
+  }
+  if (d < HD) out[(size_t)b * ldo + (size_t)h * HD + d] = __float2bfloat16_rn(num / den);
+}
+
+template <int HD>
+cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
+                      int KV, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx, float* ws,
+                      cudaStream_t s) {
+  if (H / KV > MAXG) return cudaErrorInvalidValue;
+  const int n_chunks = (max_ctx + 1 + DCHUNK - 1) / DCHUNK;
+  const float sl2 = LOG2E / sqrtf((float)HD);
+  decode_attn_partial<HD><<<dim3(B, KV, n_chunks), DCHUNK, 0, s>>>(qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages,
+                                                                    rows, ws, n_chunks, sl2);
+  decode_attn_combine<HD><<<dim3(B, H), HD, 0, s>>>(ws, rows, out, ldo, H, n_chunks);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t flash_attn(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
+                       cudaStream_t s) {
+  if (S <= 0) return cudaSuccess;
+  if (ld % 8 || H % KV) return cudaErrorInvalidValue;
+  switch (hd) {
+    case 16: return fa_launch<16>(qkv, ld, out, ldo, S, H, KV, causal, s);
+    case 32: return fa_launch<32>(qkv, ld, out, ldo, S, H, KV, causal, s);
+    case 64: return fa_launch<64>(qkv, ld, out, ldo, S, H, KV, causal, s);
+    case 80: return fa_launch<80>(qkv, ld, out, ldo, S, H, KV, causal, s);
+    case 128: return fa_launch<128>(qkv, ld, out, ldo, S, H, KV, causal, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t decode_attn(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
+                        int KV, int hd, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx,
+                        float* ws, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  switch (hd) {
+    case 32: return da_launch<32>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, s);
+    case 64: return da_launch<64>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, s);
+    case 128:
+      return da_launch<128>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace nova

@@ -1,0 +1,301 @@
+// tcgen05 / TMEM / TMA persistent bf16 GEMM with fused epilogues (vision encode and
+// LLM prefill linears, PAPER.md Table resource_stage: the stage's dense
+// contractions).
+//
+//   C[M][N] (epilogue) = A[M][K] . W[N][K]^T + bias
+//
+// One CTA per SM (persistent, grid = min(tiles, SM budget of the partition)).
+// Warp roles: w0 = TMA producer (one lane), w1 = MMA issuer (one lane),
+// w2 = TMEM allocator, w4..w7 = epilogue (TMEM lanes 0..127 = tile rows).
+// Tile 128 x BN x 64, SWIZZLE_128B K-major operands, STAGES-deep smem ring,
+// two TMEM accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Output of a tile depends only on (A rows, W rows, K order): bitwise invariant to
+// the grid size (the SM budget), which co-exec == serial parity relies on.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nova {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+struct GemmArgs {
+  void* C;
+  const bf16* bias;
+  int M, N, K, ldc;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = BN == 256 ? 512 : (BN == 128 ? 256 : 128);
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+NOVA_DEV float quick_gelu(float z) { return z / (1.0f + __expf(-1.702f * z)); }
+NOVA_DEV float gelu_erf(float z) { return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f)); }
+NOVA_DEV float silu(float z) { return z / (1.0f + __expf(-z)); }
+
+// Epilogue for 32 consecutive columns n0..n0+31 of row m (v = accumulators).
+template <int EPI>
+NOVA_DEV void epilogue32(const GemmArgs& g, int m, int n0, float* v) {
+  if (g.bias != nullptr) {
+    const uint4* bp = reinterpret_cast<const uint4*>(g.bias + n0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u = bp[q];
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = unpack_bf16(w[j]);
+        v[q * 8 + 2 * j] += f.x;
+        v[q * 8 + 2 * j + 1] += f.y;
+      }
+    }
+  }
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_QGELU || EPI == EPI_BF16_GELU) {
+    bf16* c = reinterpret_cast<bf16*>(g.C) + (size_t)m * g.ldc + n0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float z = v[q * 8 + j];
+        if constexpr (EPI == EPI_BF16_QGELU) z = quick_gelu(z);
+        if constexpr (EPI == EPI_BF16_GELU) z = gelu_erf(z);
+        t[j] = z;
+      }
+      uint4 o = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]), pack_bf16(t[6], t[7]));
+      reinterpret_cast<uint4*>(c)[q] = o;
+    }
+  } else if constexpr (EPI == EPI_BF16_SILUMUL) {
+    // columns n0..n0+15 are gate rows, n0+16..n0+31 the matching up rows
+    bf16* c = reinterpret_cast<bf16*>(g.C) + (size_t)m * g.ldc + n0 / 2;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      float t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] = silu(v[q * 8 + j]) * v[16 + q * 8 + j];
+      uint4 o = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]), pack_bf16(t[6], t[7]));
+      reinterpret_cast<uint4*>(c)[q] = o;
+    }
+  } else {
+    float* c = reinterpret_cast<float*>(g.C) + (size_t)m * g.ldc + n0;
+    float4* c4 = reinterpret_cast<float4*>(c);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      if constexpr (EPI == EPI_F32_RESID) {
+        float4 r = c4[q];
+        o.x += r.x;
+        o.y += r.y;
+        o.z += r.z;
+        o.w += r.w;
+      }
+      c4[q] = o;
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (g.M + BM - 1) / BM;
+  const int num_n = g.N / BN;
+  const int tiles = num_m * num_n;
+  const int kblocks = (g.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int mb = t % num_m, nb = t / num_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
+          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16_ss(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                         (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue
+    const int row = (warp - 4) * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int mb = t % num_m, nb = t / num_m;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int m = mb * BM + row;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + acc * BN + c * 32, v);
+        if (m < g.M) epilogue32<EPI>(g, m, nb * BN + c * 32, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const bf16* ptr, int rows, int cols, int ld, int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int EPI>
+cudaError_t launch_bn(const bf16* A, int lda, const bf16* W, int ldw, const GemmArgs& g, int max_ctas,
+                      cudaStream_t s) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, g.M, g.K, lda, BM) || !make_map(&mb, W, g.N, g.K, ldw, BN)) return cudaErrorInvalidValue;
+  auto kern = gemm_tc_kernel<BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
+  int grid = tiles < max_ctas ? tiles : max_ctas;
+  if (grid < 1) grid = 1;
+  kern<<<grid, 256, GemmCfg<BN>::SMEM, s>>>(ma, mb, g);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t dispatch_epi(const bf16* A, int lda, const bf16* W, int ldw, const GemmArgs& g, int epi, int max_ctas,
+                         cudaStream_t s) {
+  switch (epi) {
+    case EPI_BF16: return launch_bn<BN, EPI_BF16>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_BF16_QGELU: return launch_bn<BN, EPI_BF16_QGELU>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_BF16_GELU: return launch_bn<BN, EPI_BF16_GELU>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_BF16_SILUMUL: return launch_bn<BN, EPI_BF16_SILUMUL>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_F32_RESID: return launch_bn<BN, EPI_F32_RESID>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_F32_STORE: return launch_bn<BN, EPI_F32_STORE>(A, lda, W, ldw, g, max_ctas, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M, int N,
+                    int K, int epi, int max_ctas, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (N % 64 != 0 || K <= 0 || (lda % 8) || (ldw % 8) || (ldc % 8)) return cudaErrorInvalidValue;
+  GemmArgs g{C, bias, M, N, K, ldc};
+  if (N % 256 == 0) return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
+  if (N % 128 == 0) return dispatch_epi<128>(A, lda, W, ldw, g, epi, max_ctas, s);
+  return dispatch_epi<64>(A, lda, W, ldw, g, epi, max_ctas, s);
+}
+
+}  // namespace nova

@@ -1,0 +1,221 @@
+// Decode GEMV (the decode linears
+// are memory-bound, ~75% of decode time, >40% long-scoreboard stalls on A6000).
+//
+//   Y[b][n] (epilogue) = sum_k X[b][k] W[n][k] + bias[n],   B <= 16 rows
+//
+// Swap-AB on the legacy tensor core (mma.sync m16n8k16): the weight rows are the
+// M side, the batch the N side, so one instruction covers 16 weight rows x 8
+// batch rows x 16 k.  Each thread loads 16 contiguous bytes of a weight row
+// (128-bit, L1::no_allocate streaming) and of the matching x row; the k order
+// inside the 32-wide chunk is permuted identically for both operands, which
+// leaves the dot product unchanged.  A CTA owns 32 weight rows (two m16 tiles:
+// gate and up of an interleaved SiLU block land in the same CTA) and splits K
+// over its 8 warps; partials are reduced through shared memory in fixed warp
+// order.  The split depends only on K, never on the grid or the batch size, so
+// results are bitwise invariant to the SM budget and to the batch composition.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nova {
+namespace {
+
+constexpr int WARPS = 8;
+constexpr int ROWS = 32;
+constexpr int UNROLL = 4;
+
+NOVA_DEV float silu_f(float z) { return z / (1.0f + __expf(-z)); }
+
+template <int NT, bool XF32>
+struct XFrag {
+  uint4 v[NT];  // bf16 x (or hi part)
+  uint4 lo[XF32 ? NT : 1];
+};
+
+template <int NT, bool XF32>
+NOVA_DEV void load_x(XFrag<NT, XF32>& f, const void* X, int ldx, int B, int g, int k) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int b = nt * 8 + g;
+    if constexpr (!XF32) {
+      f.v[nt] = b < B ? *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(X) + (size_t)b * ldx + k)
+                      : make_uint4(0, 0, 0, 0);
+    } else {
+      if (b < B) {
+        const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X) + (size_t)b * ldx + k);
+        float4 x0 = p[0], x1 = p[1];
+        float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          bf16 h0 = __float2bfloat16_rn(xs[2 * j]), h1 = __float2bfloat16_rn(xs[2 * j + 1]);
+          float r0 = xs[2 * j] - __bfloat162float(h0), r1 = xs[2 * j + 1] - __bfloat162float(h1);
+          __nv_bfloat162 hh = __halves2bfloat162(h0, h1);
+          hi[j] = *reinterpret_cast<uint32_t*>(&hh);
+          lo[j] = pack_bf16(r0, r1);
+        }
+        f.v[nt] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        f.lo[nt] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      } else {
+        f.v[nt] = make_uint4(0, 0, 0, 0);
+        f.lo[nt] = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+}
+
+// acc[mt][nt][4] += W rows (wg: row g, wg8: row g+8 of each m tile) . x
+template <int NT, bool XF32>
+NOVA_DEV void mma_chunk(float (*acc)[NT][4], const uint4* wg, const uint4* wg8, const XFrag<NT, XF32>& f) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const uint32_t a1[4] = {wg[mt].x, wg8[mt].x, wg[mt].y, wg8[mt].y};
+    const uint32_t a2[4] = {wg[mt].z, wg8[mt].z, wg[mt].w, wg8[mt].w};
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint32_t b1[2] = {f.v[nt].x, f.v[nt].y};
+      const uint32_t b2[2] = {f.v[nt].z, f.v[nt].w};
+      mma_bf16_16816(acc[mt][nt], a1, b1);
+      mma_bf16_16816(acc[mt][nt], a2, b2);
+      if constexpr (XF32) {
+        const uint32_t c1[2] = {f.lo[nt].x, f.lo[nt].y};
+        const uint32_t c2[2] = {f.lo[nt].z, f.lo[nt].w};
+        mma_bf16_16816(acc[mt][nt], a1, c1);
+        mma_bf16_16816(acc[mt][nt], a2, c2);
+      }
+    }
+  }
+}
+
+template <int NT, bool XF32, int EPI>
+__global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict__ X, int ldx,
+                                                          const bf16* __restrict__ W, int N, int K,
+                                                          void* __restrict__ Y, int ldy,
+                                                          const bf16* __restrict__ bias, int B, int kslice) {
+  __shared__ float red[WARPS][2][NT][32][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int r0 = blockIdx.x * ROWS;
+  float acc[2][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[mt][nt][j] = 0.f;
+
+  const int kbeg = warp * kslice;
+  const int kend = min(K, kbeg + kslice);
+  const bf16* wrow[4] = {W + (size_t)(r0 + g) * K, W + (size_t)(r0 + g + 8) * K, W + (size_t)(r0 + 16 + g) * K,
+                         W + (size_t)(r0 + 24 + g) * K};
+  int k = kbeg;
+  for (; k + UNROLL * 32 <= kend; k += UNROLL * 32) {
+    uint4 wg[UNROLL][2], wg8[UNROLL][2];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int kk = k + u * 32 + 8 * c;
+      wg[u][0] = ld_nc_v4(wrow[0] + kk);
+      wg8[u][0] = ld_nc_v4(wrow[1] + kk);
+      wg[u][1] = ld_nc_v4(wrow[2] + kk);
+      wg8[u][1] = ld_nc_v4(wrow[3] + kk);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      XFrag<NT, XF32> f;
+      load_x<NT, XF32>(f, X, ldx, B, g, k + u * 32 + 8 * c);
+      mma_chunk<NT, XF32>(acc, wg[u], wg8[u], f);
+    }
+  }
+  for (; k < kend; k += 32) {
+    const int kk = k + 8 * c;
+    uint4 wg[2] = {ld_nc_v4(wrow[0] + kk), ld_nc_v4(wrow[2] + kk)};
+    uint4 wg8[2] = {ld_nc_v4(wrow[1] + kk), ld_nc_v4(wrow[3] + kk)};
+    XFrag<NT, XF32> f;
+    load_x<NT, XF32>(f, X, ldx, B, g, kk);
+    mma_chunk<NT, XF32>(acc, wg, wg8, f);
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[warp][mt][nt][lane][j] = acc[mt][nt][j];
+  __syncthreads();
+  if (warp != 0) return;
+  // fixed-order reduction over the K slices
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float s = red[0][mt][nt][lane][j];
+#pragma unroll
+        for (int w = 1; w < WARPS; ++w) s += red[w][mt][nt][lane][j];
+        acc[mt][nt][j] = s;
+      }
+  // c0:(row g, col 2c) c1:(g, 2c+1) c2:(g+8, 2c) c3:(g+8, 2c+1); rows = n, cols = batch
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int b = nt * 8 + 2 * c + (j & 1);
+      const int ro = g + ((j >> 1) << 3);
+      if (b >= B) continue;
+      if constexpr (EPI == EPI_BF16_SILUMUL) {
+        const float gt = acc[0][nt][j], up = acc[1][nt][j];
+        reinterpret_cast<bf16*>(Y)[(size_t)b * ldy + r0 / 2 + ro] = __float2bfloat16_rn(silu_f(gt) * up);
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int n = r0 + mt * 16 + ro;
+          float v = acc[mt][nt][j];
+          if (bias != nullptr) v += __bfloat162float(bias[n]);
+          if constexpr (EPI == EPI_BF16) {
+            reinterpret_cast<bf16*>(Y)[(size_t)b * ldy + n] = __float2bfloat16_rn(v);
+          } else if constexpr (EPI == EPI_F32_RESID) {
+            reinterpret_cast<float*>(Y)[(size_t)b * ldy + n] += v;
+          } else {
+            reinterpret_cast<float*>(Y)[(size_t)b * ldy + n] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int NT, bool XF32>
+cudaError_t launch_nt(const void* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
+                      int epi, cudaStream_t s) {
+  const int kslice = ((K + WARPS * 32 - 1) / (WARPS * 32)) * 32;
+  dim3 grid(N / ROWS), block(WARPS * 32);
+  switch (epi) {
+    case EPI_BF16:
+      gemv_kernel<NT, XF32, EPI_BF16><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
+      break;
+    case EPI_BF16_SILUMUL:
+      gemv_kernel<NT, XF32, EPI_BF16_SILUMUL><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
+      break;
+    case EPI_F32_RESID:
+      gemv_kernel<NT, XF32, EPI_F32_RESID><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
+      break;
+    case EPI_F32_STORE:
+      gemv_kernel<NT, XF32, EPI_F32_STORE><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias,
+                 int B, int epi, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  if (B > 16 || N % ROWS || K % 32 || ldx % 8) return cudaErrorInvalidValue;
+  if (x_f32) return B <= 8 ? launch_nt<1, true>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s)
+                           : launch_nt<2, true>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s);
+  return B <= 8 ? launch_nt<1, false>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s)
+                : launch_nt<2, false>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s);
+}
+
+}  // namespace nova

@@ -1,0 +1,73 @@
+// Internal host-side launchers for the sm_100a stage kernels (L1).  Plain
+// pointers and sizes; every call enqueues on `stream` and returns the launch
+// status.  Layouts: activations row-major, weights [out][in] (HF convention),
+// residual stream f32, GEMM operands bf16, accumulation f32.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace nova {
+
+typedef __nv_bfloat16 bf16;
+
+// GEMM / GEMV epilogues (C = A . W^T + bias, then):
+enum Epi {
+  EPI_BF16 = 0,         // out bf16
+  EPI_BF16_QGELU = 1,   // out bf16, QuickGELU (ViT MLP)
+  EPI_BF16_GELU = 2,    // out bf16, GELU(erf) (merger)
+  EPI_BF16_SILUMUL = 3, // W rows interleaved gate/up in blocks of 16; out[:, N/2] = silu(g) * u
+  EPI_F32_RESID = 4,    // out f32 += result (residual add)
+  EPI_F32_STORE = 5,    // out f32 = result
+};
+
+// tcgen05/TMEM/TMA persistent GEMM. A [M][K] (lda), W [N][K] (ldw), C [M][N] (ldc elems).
+// grid = min(tiles, max_ctas): max_ctas is the SM budget of the partition.
+cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M,
+                    int N, int K, int epi, int max_ctas, cudaStream_t s);
+
+// Decode GEMV (B <= 16 rows): Y[b][n] = sum_k X[b][k] W[n][k] (+bias), epilogue as above.
+// X bf16 (x_f32 = 0) or f32 (x_f32 = 1, split hi/lo on the tensor core).
+cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K, void* Y, int ldy,
+                 const bf16* bias, int B, int epi, cudaStream_t s);
+
+// Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).
+// out [S][H * hd] (ldo).  causal: key j <= query i.  Query head h reads KV head h / (H / KV).
+cudaError_t flash_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
+                       cudaStream_t s);
+
+// Paged KV cache: pool [L][P][2][KV][64][hd] bf16; block table per request slot [max_pages].
+struct DecodeRow {
+  int slot;   // request slot (block table row, last-token cell)
+  int ctx;    // tokens already in the cache = cache index of this step's token
+  int pos;    // M-RoPE position (t = h = w for generated text)
+  int pad;
+};
+cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf16* kv_pool, int layer, int n_pages,
+                        int H, int KV, int hd, const int* block_tables, int max_pages, const DecodeRow* rows, int B,
+                        int max_ctx, float* ws, cudaStream_t s);
+
+cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d,
+                      float eps, cudaStream_t s);
+cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
+                    cudaStream_t s);
+
+// pixels bf16 [C][H][W] -> X0 [N][C*T*P*P] merge-group-major rows
+cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int merge, bf16* X0, cudaStream_t s);
+// ViT 2D RoPE in place on the q and k parts of qkv [N][3][heads][hd]; grid gw patches wide
+cudaError_t vit_rope(bf16* qkv, int N, int heads, int hd, int gw, int merge, float theta, cudaStream_t s);
+// LLM M-RoPE in place on q/k of qkv rows + write k, v to the paged cache.
+// Row r: positions pos3[0][r], pos3[1][r], pos3[2][r]  (pos3 may be null -> rows[] give pos),
+// cache index (ctx0 + r) for prefill (rows == null), or rows[r].ctx for decode.
+cudaError_t llm_rope_kv(bf16* qkv, int ldqkv, int nrows, int H, int KV, int hd, float theta, int sec0, int sec1,
+                        const int* pos3, int ld_pos, const DecodeRow* rows, int slot, int ctx0, bf16* kv_pool,
+                        int layer, int n_pages, const int* block_tables, int max_pages, cudaStream_t s);
+// hidden f32 rows <- bf16 table rows; ids from `ids` or from last_tok[rows[b].slot]
+cudaError_t embed(const bf16* table, int d, const int* ids, const DecodeRow* rows, const int* last_tok, float* out,
+                  int ldo, int n, cudaStream_t s);
+// argmax over each row (lowest index on ties); writes out_tok[r] and last_tok[rows[r].slot] (if rows)
+cudaError_t argmax_rows(const float* logits, int ldl, int V, int n, int* out_tok, const DecodeRow* rows,
+                        int* last_tok, int single_slot, cudaStream_t s);
+
+}  // namespace nova

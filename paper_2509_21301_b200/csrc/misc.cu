@@ -1,0 +1,272 @@
+// Row-wise and elementwise kernels of the stage programs (SURVEY.md §8(a) rows a1,
+// a5-a7): patchify, LayerNorm / RMSNorm ("kernel fusion ... RoPE and
+// RMSNorm"), ViT 2D RoPE, LLM M-RoPE fused with the paged KV-cache write,
+// embedding gather, deterministic argmax.  All are HBM/latency-bound row kernels.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nova {
+namespace {
+
+// ---------------------------------------------------------------- norms (one warp per row)
+__global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm,
+                                 const bf16* __restrict__ bt, bf16* __restrict__ y, int ldy, int M, int d, float eps) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + (size_t)row * ldx;
+  float s = 0.f;
+  for (int i = lane * 4; i < d; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    s += (v.x + v.y) + (v.z + v.w);
+  }
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+  for (int i = lane * 4; i < d; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    const float a = v.x - mu, b = v.y - mu, c = v.z - mu, e = v.w - mu;
+    q += (a * a + b * b) + (c * c + e * e);
+  }
+  const float rs = rsqrtf(warp_sum(q) / d + eps);
+  bf16* yr = y + (size_t)row * ldy;
+  for (int i = lane * 4; i < d; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    const float2 g01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i));
+    const float2 g23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i + 2));
+    const float2 b01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(bt + i));
+    const float2 b23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(bt + i + 2));
+    uint2 o;
+    o.x = pack_bf16((v.x - mu) * rs * g01.x + b01.x, (v.y - mu) * rs * g01.y + b01.y);
+    o.y = pack_bf16((v.z - mu) * rs * g23.x + b23.x, (v.w - mu) * rs * g23.y + b23.y);
+    *reinterpret_cast<uint2*>(yr + i) = o;
+  }
+}
+
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm, void* __restrict__ y,
+                               int y_f32, int ldy, int M, int d, float eps) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + (size_t)row * ldx;
+  float q = 0.f;
+  for (int i = lane * 4; i < d; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    q += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
+  }
+  const float rs = rsqrtf(warp_sum(q) / d + eps);
+  for (int i = lane * 4; i < d; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    const float2 g01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i));
+    const float2 g23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i + 2));
+    const float o0 = v.x * rs * g01.x, o1 = v.y * rs * g01.y, o2 = v.z * rs * g23.x, o3 = v.w * rs * g23.y;
+    if (y_f32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + (size_t)row * ldy + i) = make_float4(o0, o1, o2, o3);
+    } else {
+      uint2 o;
+      o.x = pack_bf16(o0, o1);
+      o.y = pack_bf16(o2, o3);
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(y) + (size_t)row * ldy + i) = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- patchify
+// Row r (merge-group-major): group = r / m^2 over the (gh/m) x (gw/m) group grid, row-major;
+// inside the group (di, dj) row-major.  Column = ((c*T + t)*P + py)*P + px, frame duplicated over t.
+__global__ void patchify_kernel(const bf16* __restrict__ pix, int C, int H, int W, int P, int T, int m,
+                                bf16* __restrict__ X0) {
+  const int r = blockIdx.x;
+  const int gw = W / P;
+  const int grp = r / (m * m), in = r % (m * m);
+  const int gi = grp / (gw / m), gj = grp % (gw / m);
+  const int pi = gi * m + in / m, pj = gj * m + in % m;
+  const int K = C * T * P * P;
+  for (int col = threadIdx.x; col < K; col += blockDim.x) {
+    const int px = col % P, py = (col / P) % P, ch = col / (T * P * P);
+    X0[(size_t)r * K + col] = pix[((size_t)ch * H + pi * P + py) * W + pj * P + px];
+  }
+}
+
+// ---------------------------------------------------------------- RoPE
+// ViT: angle for pair i (< hd/2): i < hd/4 -> h * inv[i], else w * inv[i - hd/4]; inv[j] = theta^(-4j/hd).
+__global__ void vit_rope_kernel(bf16* __restrict__ qkv, int heads, int hd, int gw, int m, float log2_theta) {
+  const int r = blockIdx.x;
+  const int grp = r / (m * m), in = r % (m * m);
+  const int gi = grp / (gw / m), gj = grp % (gw / m);
+  const float ph = (float)(gi * m + in / m), pw = (float)(gj * m + in % m);
+  const int half = hd / 2, quarter = hd / 4;
+  bf16* row = qkv + (size_t)r * 3 * heads * hd;
+  for (int idx = threadIdx.x; idx < 2 * heads * half; idx += blockDim.x) {
+    const int hh = idx / half, i = idx % half;  // hh < heads: q, else k
+    const int j = i < quarter ? i : i - quarter;
+    const float inv = exp2f(-(4.0f * j / hd) * log2_theta);
+    const float ang = (i < quarter ? ph : pw) * inv;
+    float sn, cs;
+    sincosf(ang, &sn, &cs);
+    bf16* v = row + (size_t)hh * hd;  // q heads then k heads are contiguous
+    const float x1 = __bfloat162float(v[i]), x2 = __bfloat162float(v[i + half]);
+    v[i] = __float2bfloat16_rn(x1 * cs - x2 * sn);
+    v[i + half] = __float2bfloat16_rn(x2 * cs + x1 * sn);
+  }
+}
+
+// LLM M-RoPE (sections sec0 | sec1 | rest over the hd/2 frequencies) + paged KV write.
+__global__ void llm_rope_kv_kernel(bf16* __restrict__ qkv, int ld, int H, int KV, int hd, float log2_theta, int sec0,
+                                   int sec1, const int* __restrict__ pos3, int ld_pos,
+                                   const DecodeRow* __restrict__ rows, int slot, int ctx0, bf16* __restrict__ pool,
+                                   int layer, int n_pages, const int* __restrict__ bt, int max_pages) {
+  const int r = blockIdx.x;
+  int p[3], cidx, sl;
+  if (rows) {
+    const DecodeRow rr = rows[r];
+    p[0] = p[1] = p[2] = rr.pos;
+    cidx = rr.ctx;
+    sl = rr.slot;
+  } else {
+    p[0] = pos3[r];
+    p[1] = pos3[ld_pos + r];
+    p[2] = pos3[2 * ld_pos + r];
+    cidx = ctx0 + r;
+    sl = slot;
+  }
+  const int half = hd / 2;
+  bf16* row = qkv + (size_t)r * ld;
+  for (int idx = threadIdx.x; idx < (H + KV) * half; idx += blockDim.x) {
+    const int hh = idx / half, i = idx % half;
+    const int comp = i < sec0 ? 0 : (i < sec0 + sec1 ? 1 : 2);
+    const float inv = exp2f(-(2.0f * i / hd) * log2_theta);
+    const float ang = (float)p[comp] * inv;
+    float sn, cs;
+    sincosf(ang, &sn, &cs);
+    bf16* v = row + (size_t)hh * hd;
+    const float x1 = __bfloat162float(v[i]), x2 = __bfloat162float(v[i + half]);
+    v[i] = __float2bfloat16_rn(x1 * cs - x2 * sn);
+    v[i + half] = __float2bfloat16_rn(x2 * cs + x1 * sn);
+  }
+  __syncthreads();
+  // K (rotated) and V into page bt[slot][cidx / 64], offset cidx % 64
+  const size_t page_stride = (size_t)2 * KV * 64 * hd;
+  bf16* pg = pool + ((size_t)layer * n_pages + bt[(size_t)sl * max_pages + (cidx >> 6)]) * page_stride;
+  const int off = cidx & 63;
+  for (int idx = threadIdx.x; idx < 2 * KV * hd; idx += blockDim.x) {
+    const int kv = idx / (KV * hd), rem = idx % (KV * hd);
+    const int hh = rem / hd, d = rem % hd;
+    pg[(((size_t)kv * KV + hh) * 64 + off) * hd + d] = row[(size_t)(H + kv * KV + hh) * hd + d];
+  }
+}
+
+// ---------------------------------------------------------------- embedding, argmax
+__global__ void embed_kernel(const bf16* __restrict__ table, int d, const int* __restrict__ ids,
+                             const DecodeRow* __restrict__ rows, const int* __restrict__ last_tok, float* __restrict__ out,
+                             int ldo) {
+  const int r = blockIdx.x;
+  const int id = ids ? ids[r] : last_tok[rows[r].slot];
+  const bf16* src = table + (size_t)id * d;
+  float* dst = out + (size_t)r * ldo;
+  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
+    const float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(src + i));
+    dst[i] = f.x;
+    dst[i + 1] = f.y;
+  }
+}
+
+__global__ void argmax_kernel(const float* __restrict__ logits, int ldl, int V, int* __restrict__ out_tok,
+                              const DecodeRow* __restrict__ rows, int* __restrict__ last_tok, int single_slot) {
+  const int r = blockIdx.x;
+  const float* l = logits + (size_t)r * ldl;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = l[i];
+    if (v > best) {  // strictly greater keeps the lowest index within a thread
+      best = v;
+      bi = i;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    best = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      out_tok[r] = bi;
+      if (rows) last_tok[rows[r].slot] = bi;
+      else if (single_slot >= 0 && last_tok) last_tok[single_slot] = bi;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d, float eps,
+                      cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 4) return cudaErrorInvalidValue;
+  layernorm_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, g, b, y, ldy, M, d, eps);
+  return cudaGetLastError();
+}
+cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
+                    cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 4) return cudaErrorInvalidValue;
+  rmsnorm_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, g, y, y_f32, ldy, M, d, eps);
+  return cudaGetLastError();
+}
+cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int merge, bf16* X0, cudaStream_t s) {
+  const int N = (H / P) * (W / P);
+  if (N <= 0) return cudaSuccess;
+  patchify_kernel<<<N, 256, 0, s>>>(pix, C, H, W, P, T, merge, X0);
+  return cudaGetLastError();
+}
+cudaError_t vit_rope(bf16* qkv, int N, int heads, int hd, int gw, int merge, float theta, cudaStream_t s) {
+  if (N <= 0) return cudaSuccess;
+  vit_rope_kernel<<<N, 256, 0, s>>>(qkv, heads, hd, gw, merge, log2f(theta));
+  return cudaGetLastError();
+}
+cudaError_t llm_rope_kv(bf16* qkv, int ld, int nrows, int H, int KV, int hd, float theta, int sec0, int sec1,
+                        const int* pos3, int ld_pos, const DecodeRow* rows, int slot, int ctx0, bf16* pool, int layer,
+                        int n_pages, const int* bt, int max_pages, cudaStream_t s) {
+  if (nrows <= 0) return cudaSuccess;
+  llm_rope_kv_kernel<<<nrows, 256, 0, s>>>(qkv, ld, H, KV, hd, log2f(theta), sec0, sec1, pos3, ld_pos, rows, slot,
+                                           ctx0, pool, layer, n_pages, bt, max_pages);
+  return cudaGetLastError();
+}
+cudaError_t embed(const bf16* table, int d, const int* ids, const DecodeRow* rows, const int* last_tok, float* out,
+                  int ldo, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  embed_kernel<<<n, 256, 0, s>>>(table, d, ids, rows, last_tok, out, ldo);
+  return cudaGetLastError();
+}
+cudaError_t argmax_rows(const float* logits, int ldl, int V, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
+                        int single_slot, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  argmax_kernel<<<n, 1024, 0, s>>>(logits, ldl, V, out_tok, rows, last_tok, single_slot);
+  return cudaGetLastError();
+}
+
+}  // namespace nova

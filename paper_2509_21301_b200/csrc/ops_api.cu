@@ -1,0 +1,61 @@
+// C ABI of the individual kernels (include/nova_ops.h): argument marshalling only.
+#include "../../include/nova_ops.h"
+#include "kernels.h"
+
+using namespace nova;
+
+static int st(cudaError_t e) { return e == cudaSuccess ? 0 : -(int)e; }
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static_assert(sizeof(nova_decode_row) == sizeof(DecodeRow), "row layout");
+
+extern "C" {
+
+int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
+                 int K, int epi, int max_ctas, void* stream) {
+  return st(gemm_tc((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, (const bf16*)bias, M, N, K, epi, max_ctas,
+                    S(stream)));
+}
+int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias,
+                 int B, int epi, void* stream) {
+  return st(gemv(X, x_f32, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, S(stream)));
+}
+int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int Sq, int H, int KV, int hd, int causal,
+                       void* stream) {
+  return st(flash_attn((const bf16*)qkv, ld, (bf16*)out, ldo, Sq, H, KV, hd, causal, S(stream)));
+}
+int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
+                        int H, int KV, int hd, const int32_t* bt, int max_pages, const nova_decode_row* rows, int B,
+                        int max_ctx, float* ws, void* stream) {
+  return st(decode_attn((const bf16*)qkv, ld, (bf16*)out, ldo, (const bf16*)kv_pool, layer, n_pages, H, KV, hd, bt,
+                        max_pages, (const DecodeRow*)rows, B, max_ctx, ws, S(stream)));
+}
+int nova_op_layernorm(const float* x, int ldx, const void* g, const void* b, void* y, int ldy, int M, int d, float eps,
+                      void* stream) {
+  return st(layernorm(x, ldx, (const bf16*)g, (const bf16*)b, (bf16*)y, ldy, M, d, eps, S(stream)));
+}
+int nova_op_rmsnorm(const float* x, int ldx, const void* g, void* y, int y_f32, int ldy, int M, int d, float eps,
+                    void* stream) {
+  return st(rmsnorm(x, ldx, (const bf16*)g, y, y_f32, ldy, M, d, eps, S(stream)));
+}
+int nova_op_patchify(const void* pix, int C, int H, int W, int P, int T, int merge, void* X0, void* stream) {
+  return st(patchify((const bf16*)pix, C, H, W, P, T, merge, (bf16*)X0, S(stream)));
+}
+int nova_op_vit_rope(void* qkv, int N, int heads, int hd, int gw, int merge, float theta, void* stream) {
+  return st(vit_rope((bf16*)qkv, N, heads, hd, gw, merge, theta, S(stream)));
+}
+int nova_op_llm_rope_kv(void* qkv, int ld, int nrows, int H, int KV, int hd, float theta, int sec0, int sec1,
+                        const int32_t* pos3, int ld_pos, const nova_decode_row* rows, int slot, int ctx0,
+                        void* kv_pool, int layer, int n_pages, const int32_t* bt, int max_pages, void* stream) {
+  return st(llm_rope_kv((bf16*)qkv, ld, nrows, H, KV, hd, theta, sec0, sec1, pos3, ld_pos, (const DecodeRow*)rows,
+                        slot, ctx0, (bf16*)kv_pool, layer, n_pages, bt, max_pages, S(stream)));
+}
+int nova_op_embed(const void* table, int d, const int32_t* ids, const nova_decode_row* rows, const int32_t* last_tok,
+                  float* out, int ldo, int n, void* stream) {
+  return st(embed((const bf16*)table, d, ids, (const DecodeRow*)rows, last_tok, out, ldo, n, S(stream)));
+}
+int nova_op_argmax(const float* logits, int ldl, int V, int n, int32_t* out_tok, const nova_decode_row* rows,
+                   int32_t* last_tok, int single_slot, void* stream) {
+  return st(argmax_rows(logits, ldl, V, n, out_tok, (const DecodeRow*)rows, last_tok, single_slot, S(stream)));
+}
+
+}  // extern "C"

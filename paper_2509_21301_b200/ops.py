@@ -1,0 +1,79 @@
+"""Python binding of include/nova_ops.h: same names, argument marshalling only.
+
+Tensors are torch CUDA tensors (device memory plumbing); every computation runs
+in libnova.so kernels on the current torch stream.
+"""
+from __future__ import annotations
+
+import torch
+
+from ._lib import lib, check
+
+EPI_BF16, EPI_BF16_QGELU, EPI_BF16_GELU, EPI_BF16_SILUMUL, EPI_F32_RESID, EPI_F32_STORE = range(6)
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _s(stream=None):
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+def nova_op_gemm(A, W, C, bias, M, N, K, epi, max_ctas=148, lda=None, ldw=None, ldc=None, stream=None):
+    check(lib().nova_op_gemm(_p(A), lda or A.stride(0), _p(W), ldw or W.stride(0), _p(C), ldc or C.stride(0),
+                             _p(bias), M, N, K, epi, max_ctas, _s(stream)), "gemm")
+
+
+def nova_op_gemv(X, W, Y, bias, N, K, B, epi, x_f32=None, ldx=None, ldy=None, stream=None):
+    xf = int(X.dtype == torch.float32) if x_f32 is None else x_f32
+    check(lib().nova_op_gemv(_p(X), xf, ldx or X.stride(0), _p(W), N, K, _p(Y), ldy or Y.stride(0), _p(bias), B,
+                             epi, _s(stream)), "gemv")
+
+
+def nova_op_flash_attn(qkv, out, S, H, KV, hd, causal, stream=None):
+    check(lib().nova_op_flash_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), S, H, KV, hd, int(causal),
+                                   _s(stream)), "flash_attn")
+
+
+def nova_op_decode_attn(qkv, out, kv_pool, layer, n_pages, H, KV, hd, block_tables, rows, B, max_ctx, ws,
+                        stream=None):
+    check(lib().nova_op_decode_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), _p(kv_pool), layer, n_pages,
+                                    H, KV, hd, _p(block_tables), block_tables.shape[1], _p(rows), B, max_ctx, _p(ws),
+                                    _s(stream)), "decode_attn")
+
+
+def nova_op_layernorm(x, gamma, beta, y, M, d, eps, stream=None):
+    check(lib().nova_op_layernorm(_p(x), x.stride(0), _p(gamma), _p(beta), _p(y), y.stride(0), M, d, eps,
+                                  _s(stream)), "layernorm")
+
+
+def nova_op_rmsnorm(x, gamma, y, M, d, eps, stream=None):
+    check(lib().nova_op_rmsnorm(_p(x), x.stride(0), _p(gamma), _p(y), int(y.dtype == torch.float32), y.stride(0),
+                                M, d, eps, _s(stream)), "rmsnorm")
+
+
+def nova_op_patchify(pix, P, T, merge, X0, stream=None):
+    Cc, H, W = pix.shape
+    check(lib().nova_op_patchify(_p(pix), Cc, H, W, P, T, merge, _p(X0), _s(stream)), "patchify")
+
+
+def nova_op_vit_rope(qkv, N, heads, hd, gw, merge, theta, stream=None):
+    check(lib().nova_op_vit_rope(_p(qkv), N, heads, hd, gw, merge, theta, _s(stream)), "vit_rope")
+
+
+def nova_op_llm_rope_kv(qkv, nrows, H, KV, hd, theta, sec0, sec1, pos3, rows, slot, ctx0, kv_pool, layer, n_pages,
+                        block_tables, stream=None):
+    check(lib().nova_op_llm_rope_kv(_p(qkv), qkv.stride(0), nrows, H, KV, hd, theta, sec0, sec1, _p(pos3),
+                                    0 if pos3 is None else pos3.stride(0), _p(rows), slot, ctx0, _p(kv_pool), layer,
+                                    n_pages, _p(block_tables), block_tables.shape[1], _s(stream)), "llm_rope_kv")
+
+
+def nova_op_embed(table, d, ids, rows, last_tok, out, n, stream=None):
+    check(lib().nova_op_embed(_p(table), d, _p(ids), _p(rows), _p(last_tok), _p(out), out.stride(0), n,
+                              _s(stream)), "embed")
+
+
+def nova_op_argmax(logits, V, n, out_tok, rows=None, last_tok=None, single_slot=-1, stream=None):
+    check(lib().nova_op_argmax(_p(logits), logits.stride(0), V, n, _p(out_tok), _p(rows), _p(last_tok),
+                               single_slot, _s(stream)), "argmax")

@@ -1,0 +1,258 @@
+"""Per-kernel parity (GPU): each libnova kernel vs the oracle's op on the same bf16
+inputs, through the C ABI (include/nova_ops.h).  Tolerances (SURVEY.md §8(c) c6,
+DESIGN.md "Tolerances"): bf16 outputs rel-inf <= 8e-3 (~2 output ulps), f32
+outputs rel-inf <= 1e-4 (accumulation-order only); argmax/indices exact; grid
+and batch invariance bitwise."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import vlm as V
+from tests.gpu_util import bf16_dev, bf16_host, rand_bf16, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2509_21301_b200 import ops as O
+
+
+def interleave_gate_up(wg: np.ndarray, wu: np.ndarray, blk: int = 16) -> np.ndarray:
+    F, K = wg.shape
+    out = np.empty((2 * F, K), wg.dtype)
+    for b in range(F // blk):
+        out[2 * b * blk:(2 * b + 1) * blk] = wg[b * blk:(b + 1) * blk]
+        out[(2 * b + 1) * blk:(2 * b + 2) * blk] = wu[b * blk:(b + 1) * blk]
+    return out
+
+
+GEMM_SHAPES = [(16, 64, 64), (12, 256, 128), (200, 384, 1176), (1286, 4608, 3584), (777, 1280, 5120), (4888, 3840, 1280)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_tc_epilogues(M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    A = rand_bf16(rng, (M, K))
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    b = rand_bf16(rng, (N,), 0.1)
+    ref = V.linear(A.astype(np.float64), W.astype(np.float64), b.astype(np.float64))
+    dA, dW, db = bf16_dev(A), bf16_dev(W), bf16_dev(b)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    for epi, f in [(O.EPI_BF16, lambda z: z), (O.EPI_BF16_QGELU, V.quick_gelu), (O.EPI_BF16_GELU, V.gelu_erf)]:
+        O.nova_op_gemm(dA, dW, C, db, M, N, K, epi)
+        torch.cuda.synchronize()
+        assert rel_inf(bf16_host(C), f(ref)) <= 8e-3, epi
+    R0 = torch.from_numpy(rng.standard_normal((M, N)).astype(np.float32)).cuda()
+    R = R0.clone()
+    O.nova_op_gemm(dA, dW, R, db, M, N, K, O.EPI_F32_RESID)
+    torch.cuda.synchronize()
+    assert rel_inf(R.cpu().numpy(), R0.cpu().numpy() + ref) <= 1e-4
+    Fo = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    O.nova_op_gemm(dA, dW, Fo, None, M, N, K, O.EPI_F32_STORE)
+    torch.cuda.synchronize()
+    ref_nb = V.linear(A.astype(np.float64), W.astype(np.float64))
+    assert rel_inf(Fo.cpu().numpy(), ref_nb) <= 1e-4
+
+
+def test_gemm_silu_mul_and_grid_invariance():
+    rng = np.random.default_rng(7)
+    M, F, K = 300, 512, 384
+    A = rand_bf16(rng, (M, K))
+    Wg, Wu = rand_bf16(rng, (F, K), K ** -0.5), rand_bf16(rng, (F, K), K ** -0.5)
+    Wi = interleave_gate_up(Wg, Wu)
+    a64 = A.astype(np.float64)
+    ref = V.silu(a64 @ Wg.T.astype(np.float64)) * (a64 @ Wu.T.astype(np.float64))
+    dA, dW = bf16_dev(A), bf16_dev(Wi)
+    outs = []
+    for ctas in (148, 37, 5, 1):
+        C = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_gemm(dA, dW, C, None, M, 2 * F, K, O.EPI_BF16_SILUMUL, max_ctas=ctas)
+        torch.cuda.synchronize()
+        outs.append(C.view(torch.int16).cpu())
+    assert rel_inf(bf16_host(C), ref) <= 8e-3
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])           # bitwise SM-budget invariance
+
+
+@pytest.mark.parametrize("N,K", [(256, 128), (4608, 3584), (3584, 18944), (512, 128), (2048, 1536)])
+def test_gemv_and_batch_invariance(N, K):
+    rng = np.random.default_rng(N + K)
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    b = rand_bf16(rng, (N,), 0.1)
+    X = rand_bf16(rng, (16, K))
+    dW, db, dX = bf16_dev(W), bf16_dev(b), bf16_dev(X)
+    ref = V.linear(X.astype(np.float64), W.astype(np.float64), b.astype(np.float64))
+    rows = {}
+    for B in (1, 3, 8, 11, 16):
+        Y = torch.empty(B, N, dtype=torch.float32, device="cuda")
+        O.nova_op_gemv(dX[:B], dW, Y, db, N, K, B, O.EPI_F32_STORE)
+        torch.cuda.synchronize()
+        y = Y.cpu().numpy()
+        assert rel_inf(y, ref[:B]) <= 1e-4
+        rows[B] = y
+    for B in (3, 8, 11, 16):
+        assert np.array_equal(rows[B][0], rows[1][0])   # bitwise batch invariance
+    Yb = torch.empty(5, N, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_gemv(dX[:5], dW, Yb, db, N, K, 5, O.EPI_BF16)
+    torch.cuda.synchronize()
+    assert rel_inf(bf16_host(Yb), ref[:5]) <= 8e-3
+    R0 = torch.randn(5, N, device="cuda")
+    R = R0.clone()
+    O.nova_op_gemv(dX[:5], dW, R, db, N, K, 5, O.EPI_F32_RESID)
+    torch.cuda.synchronize()
+    assert rel_inf(R.cpu().numpy(), R0.cpu().numpy() + ref[:5]) <= 1e-4
+
+
+def test_gemv_f32_input_and_silu():
+    rng = np.random.default_rng(3)
+    N, K = 512, 256
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    Xf = rng.standard_normal((4, K)).astype(np.float32)     # f32 activations (lm_head input)
+    Y = torch.empty(4, N, dtype=torch.float32, device="cuda")
+    O.nova_op_gemv(torch.from_numpy(Xf).cuda(), bf16_dev(W), Y, None, N, K, 4, O.EPI_F32_STORE)
+    torch.cuda.synchronize()
+    ref = Xf.astype(np.float64) @ W.T.astype(np.float64)
+    assert rel_inf(Y.cpu().numpy(), ref) <= 2e-4             # hi/lo split keeps ~16 bits of x
+    F = 256
+    Wg, Wu = rand_bf16(rng, (F, K), K ** -0.5), rand_bf16(rng, (F, K), K ** -0.5)
+    X = rand_bf16(rng, (9, K))
+    Yb = torch.empty(9, F, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_gemv(bf16_dev(X), bf16_dev(interleave_gate_up(Wg, Wu)), Yb, None, 2 * F, K, 9, O.EPI_BF16_SILUMUL)
+    torch.cuda.synchronize()
+    x64 = X.astype(np.float64)
+    ref = V.silu(x64 @ Wg.T.astype(np.float64)) * (x64 @ Wu.T.astype(np.float64))
+    assert rel_inf(bf16_host(Yb), ref) <= 8e-3
+
+
+@pytest.mark.parametrize("S,H,KV,hd,causal", [(16, 4, 4, 16, 0), (300, 4, 4, 16, 0), (12, 4, 2, 32, 1),
+                                               (1286, 12, 2, 128, 1), (777, 16, 16, 80, 0), (130, 28, 4, 128, 1),
+                                               (4888, 2, 2, 80, 0)])
+def test_flash_attn(S, H, KV, hd, causal):
+    rng = np.random.default_rng(S + hd)
+    qkv = rand_bf16(rng, (S, (H + 2 * KV) * hd))
+    d = bf16_dev(qkv)
+    out = torch.empty(S, H * hd, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_flash_attn(d, out, S, H, KV, hd, causal)
+    torch.cuda.synchronize()
+    q = qkv[:, :H * hd].reshape(S, H, hd).astype(np.float64)
+    k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd).astype(np.float64)
+    v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd).astype(np.float64)
+    if causal:
+        ref = V.attention_causal_gqa(q, k, v, hd ** -0.5, 0)
+    else:
+        ref = V.attention_full(q, np.repeat(k, H // KV, 1), np.repeat(v, H // KV, 1), hd ** -0.5)
+    assert rel_inf(bf16_host(out).reshape(S, H, hd), ref) <= 2e-2   # P rounded to bf16 before PV
+
+
+def _pool_setup(rng, L, n_pages, KV, hd):
+    return torch.zeros(L, n_pages, 2, KV, 64, hd, dtype=torch.bfloat16, device="cuda")
+
+
+def test_llm_rope_kv_and_decode_attention():
+    rng = np.random.default_rng(11)
+    H, KV, hd, L, n_pages = 8, 2, 32, 2, 16
+    sec = (4, 6, 6)
+    S = 150
+    qkv = rand_bf16(rng, (S, (H + 2 * KV) * hd))
+    pos3 = V.mrope_positions(8, 6, S - 12, 2)          # 12 vision tokens + text
+    bt = torch.tensor([[5, 9, 2, 7], [1, 3, 11, 0]], dtype=torch.int32, device="cuda")
+    pool = _pool_setup(rng, L, n_pages, KV, hd)
+    d = bf16_dev(qkv)
+    O.nova_op_llm_rope_kv(d, S, H, KV, hd, 1e6, sec[0], sec[1], torch.from_numpy(pos3.astype(np.int32)).cuda(),
+                          None, 0, 0, pool, 1, n_pages, bt)
+    torch.cuda.synchronize()
+    c, s = V.mrope_tables(pos3, hd, 1e6, sec, np.float64)
+    q = qkv[:, :H * hd].reshape(S, H, hd).astype(np.float64)
+    k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd).astype(np.float64)
+    v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd)
+    qr, kr = V.apply_rope(q, c, s), V.apply_rope(k, c, s)
+    got = bf16_host(d)
+    assert rel_inf(got[:, :H * hd].reshape(S, H, hd), qr) <= 8e-3
+    assert rel_inf(got[:, H * hd:(H + KV) * hd].reshape(S, KV, hd), kr) <= 8e-3
+    P = bf16_host(pool[1])                              # [pages][2][KV][64][hd]
+    btn = bt.cpu().numpy()[0]
+    kc = np.stack([P[btn[t // 64], 0, :, t % 64] for t in range(S)])
+    vc = np.stack([P[btn[t // 64], 1, :, t % 64] for t in range(S)])
+    assert np.array_equal(kc, got[:, H * hd:(H + KV) * hd].reshape(S, KV, hd))
+    assert np.array_equal(vc, v)
+    # one decode step for slot 0 at cache index S-1 (keys 0..S-1) using the cached K/V
+    qd = rand_bf16(rng, (1, (H + 2 * KV) * hd))
+    rows = torch.tensor([[0, S - 1, 0, 0]], dtype=torch.int32, device="cuda")
+    out = torch.empty(1, H * hd, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(64 * H * (hd + 2), dtype=torch.float32, device="cuda")
+    O.nova_op_decode_attn(bf16_dev(qd), out, pool, 1, n_pages, H, KV, hd, bt, rows, 1, S - 1, ws)
+    torch.cuda.synchronize()
+    ref = V.attention_causal_gqa(qd[:, :H * hd].reshape(1, H, hd).astype(np.float64), kc.astype(np.float64),
+                                 vc.astype(np.float64), hd ** -0.5, S - 1)
+    assert rel_inf(bf16_host(out).reshape(1, H, hd), ref) <= 8e-3
+
+
+def test_decode_attention_long_context_7b_shape():
+    rng = np.random.default_rng(12)
+    H, KV, hd, n_pages = 28, 4, 128, 128
+    ctxs = [1333, 17, 640, 2047]
+    B = len(ctxs)
+    pool_np = rand_bf16(rng, (1, n_pages, 2, KV, 64, hd))
+    pool = bf16_dev(pool_np)
+    perm = rng.permutation(n_pages).astype(np.int32)
+    bt = torch.from_numpy(perm.reshape(4, 32).copy()).cuda()
+    qd = rand_bf16(rng, (B, (H + 2 * KV) * hd))
+    rows = torch.tensor([[b, ctxs[b], 0, 0] for b in range(B)], dtype=torch.int32, device="cuda")
+    out = torch.empty(B, H * hd, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(B * H * 9 * (hd + 2), dtype=torch.float32, device="cuda")
+    O.nova_op_decode_attn(bf16_dev(qd), out, pool, 0, n_pages, H, KV, hd, bt, rows, B, max(ctxs), ws)
+    torch.cuda.synchronize()
+    btn = bt.cpu().numpy()
+    for b, ctx in enumerate(ctxs):
+        kc = np.stack([pool_np[0, btn[b, t // 64], 0, :, t % 64] for t in range(ctx + 1)]).astype(np.float64)
+        vc = np.stack([pool_np[0, btn[b, t // 64], 1, :, t % 64] for t in range(ctx + 1)]).astype(np.float64)
+        ref = V.attention_causal_gqa(qd[b:b + 1, :H * hd].reshape(1, H, hd).astype(np.float64), kc, vc,
+                                     hd ** -0.5, ctx)
+        assert rel_inf(bf16_host(out[b:b + 1]).reshape(1, H, hd), ref) <= 8e-3
+
+
+def test_norms_patchify_vitrope_embed_argmax():
+    rng = np.random.default_rng(5)
+    M, d = 37, 1280
+    x = rng.standard_normal((M, d)).astype(np.float32) * 3
+    g, b = rand_bf16(rng, (d,), 0.1) + 1, rand_bf16(rng, (d,), 0.05)
+    y = torch.empty(M, d, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_layernorm(torch.from_numpy(x).cuda(), bf16_dev(g), bf16_dev(b), y, M, d, 1e-6)
+    torch.cuda.synchronize()
+    assert rel_inf(bf16_host(y), V.layer_norm(x.astype(np.float64), g, b, 1e-6)) <= 8e-3
+    yf = torch.empty(M, d, dtype=torch.float32, device="cuda")
+    O.nova_op_rmsnorm(torch.from_numpy(x).cuda(), bf16_dev(g), yf, M, d, 1e-6)
+    torch.cuda.synchronize()
+    assert rel_inf(yf.cpu().numpy(), V.rms_norm(x.astype(np.float64), g, 1e-6)) <= 1e-5
+    # patchify: grid 6 x 8 patches of 14 px
+    from synth import TINY
+    pix = rand_bf16(rng, (3, 6 * 14, 8 * 14))
+    X0 = torch.empty(48, 1176, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_patchify(bf16_dev(pix), 14, 2, 2, X0)
+    torch.cuda.synchronize()
+    ref, _, hp, wp = V.patchify(pix, TINY)
+    assert np.array_equal(bf16_host(X0), ref)
+    # ViT rope on qkv [48][3][4][16]
+    qkv = rand_bf16(rng, (48, 3 * 4 * 16))
+    dq = bf16_dev(qkv)
+    O.nova_op_vit_rope(dq, 48, 4, 16, 8, 2, 1e4)
+    torch.cuda.synchronize()
+    c, s = V.vit_rope_tables(hp, wp, 16, 1e4, np.float64)
+    t = qkv.reshape(48, 3, 4, 16).astype(np.float64)
+    got = bf16_host(dq).reshape(48, 3, 4, 16)
+    assert rel_inf(got[:, 0], V.apply_rope(t[:, 0], c, s)) <= 8e-3
+    assert rel_inf(got[:, 1], V.apply_rope(t[:, 1], c, s)) <= 8e-3
+    assert np.array_equal(got[:, 2], t[:, 2])
+    # embedding + argmax (ties -> lowest index)
+    table = rand_bf16(rng, (100, 64))
+    ids = torch.tensor([3, 99, 0, 3], dtype=torch.int32, device="cuda")
+    out = torch.empty(4, 64, dtype=torch.float32, device="cuda")
+    O.nova_op_embed(bf16_dev(table), 64, ids, None, None, out, 4)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), table[[3, 99, 0, 3]])
+    lg = rng.standard_normal((3, 152064)).astype(np.float32)
+    lg[1, 7] = lg[1, 150000] = lg[1].max() + 1       # tie
+    tok = torch.empty(3, dtype=torch.int32, device="cuda")
+    O.nova_op_argmax(torch.from_numpy(lg).cuda(), 152064, 3, tok)
+    torch.cuda.synchronize()
+    assert tok.cpu().tolist() == [V.argmax_lowest(r) for r in lg]
+    assert tok.cpu().tolist()[1] == 7
