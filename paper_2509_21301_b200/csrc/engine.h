@@ -1,0 +1,256 @@
+// Nova engine internals: model/weight layout (L2 stage programs), partition
+// executor (L3, green contexts + role workers), Algorithm 1 controller (L4) and the
+// virtual-time Sim backend.  The public ABI is include/nova.h.
+#pragma once
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/nova.h"
+#include "kernels.h"
+
+namespace nova {
+
+int64_t mono_ns();
+
+// ------------------------------------------------------------------ model shape
+struct Dims {
+  nova_model_config m;
+  int vit_hd, patch_dim, merge_dim, qkv_n, vit_layer_elems;
+  int llm_qkv_n;  // (H + 2 KV) * hd
+  void init(const nova_model_config& mc);
+};
+
+// Offsets (in bf16 elements) of the tensors of one ViT layer inside its block.
+struct VitLayerLayout {
+  size_t n1g, n1b, n2g, n2b, qkv_w, qkv_b, proj_w, proj_b, fc1_w, fc1_b, fc2_w, fc2_b, elems;
+  void init(const Dims& d);
+};
+
+struct LlmLayerW {
+  bf16 *ln1, *qkv_w, *qkv_b, *o_w, *ln2, *gu_w, *down_w;
+};
+
+struct Weights {
+  bf16* patch_w = nullptr;
+  std::vector<bf16*> vit_dev;  // resident: L layer blocks; offload: K slot blocks
+  bf16 *mlnq_g, *mlnq_b, *m1_w, *m1_b, *m2_w, *m2_b;
+  bf16 *embed, *final_norm, *lm_head;
+  std::vector<LlmLayerW> llm;
+};
+
+// ------------------------------------------------------------------ requests
+struct Request {
+  uint64_t id = 0;
+  int slot = -1;
+  int gh = 0, gw = 0, n_prompt = 0, gen_len = 0;
+  int64_t arrival = 0;
+  int emitted = 0;
+  int64_t join_seq = -1;
+  float sim_vs = 1.f, sim_ps = 1.f;
+  std::vector<int> pages;
+  std::vector<int> forced;          // teacher forcing
+  std::vector<int> tokens;          // emitted tokens
+  std::vector<std::vector<float>> logits;  // debug
+  nova_req_stats st{};
+  int n_v() const { return (gh / 2) * (gw / 2); }
+  int S() const { return n_v() + n_prompt; }
+};
+
+// ------------------------------------------------------------------ Algorithm 1
+struct Decision {
+  int kind, ctx, s_dec;
+  std::vector<Request*> reqs;
+};
+struct Event {
+  int kind;      // NOVA_EV_*
+  uint64_t key;  // request id (min id of a decode batch)
+  std::vector<Request*> reqs;
+  int64_t t;
+  std::vector<int> tokens;  // tokens produced (prefill: 1, decode: one per request)
+};
+
+struct Alg1 {
+  nova_partition_policy pol{};
+  int total_sms = 148, granularity = 8, max_split = 112;
+  std::deque<Request*> q_v, prefill_wait;
+  Request* vision_running = nullptr;
+  Request* prefill_running = nullptr;
+  std::vector<Request*> decode_running;
+  bool decode_busy = false;
+  std::vector<Request*> q_d;
+  int64_t join_counter = 0;
+  int last_pass = -1;  // 0 front, 1 decode
+  int split(int ctx, int n_pend) const;
+  int n_pend() const;
+  bool front_running() const { return vision_running || prefill_running; }
+  // Process one tick's events (already including finished detection); returns decisions.
+  std::vector<Decision> tick(std::vector<Event>& evs);
+
+ private:
+  void emit(Request* r, std::vector<Decision>& out);
+  void decode_ready(Request* r);
+  void dispatch_front(std::vector<Decision>& out, bool corun, int npend, bool has_decode);
+  void dispatch_decode(std::vector<Decision>& out, int ctx, int s);
+};
+
+// ------------------------------------------------------------------ partition family
+struct Partition {
+  int n_groups = 0, granularity = 8, total = 148;
+  std::vector<cudaStream_t> dec_stream, front_stream;  // index k = decode groups (s = 8k)
+  std::vector<CUgreenCtx> gctx;
+  cudaStream_t solo_front = nullptr, solo_decode = nullptr;
+  bool green = false;
+  std::string init(int device, bool use_green);
+  void destroy();
+  int max_split() const { return (n_groups - 1) * granularity; }
+};
+
+// ------------------------------------------------------------------ GPU role worker
+struct PassCmd {
+  int kind;  // NOVA_DEC_VISION / PREFILL / DECODE
+  int ctx, s_dec;
+  std::vector<Request*> reqs;
+  std::vector<int> forced_tok;  // per row, -1 = none
+};
+
+class Engine;
+
+struct Worker {
+  Engine* eng = nullptr;
+  int role = 0;  // 0 front, 1 decode
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<PassCmd> q;
+  bool stop = false;
+  void start(Engine* e, int r);
+  void push(PassCmd&& c);
+  void run();
+};
+
+// ------------------------------------------------------------------ engine
+class Engine {
+ public:
+  Dims dims;
+  nova_engine_config cfg{};
+  std::string err;
+  bool failed = false;
+  bool finalized = false;
+  bool sim = false;
+
+  // memory
+  nova_buffers buf{};
+  Weights W;
+  VitLayerLayout vl;
+  int vit_K = 0;  // physical slots (0 = resident)
+  uint16_t* host_vit = nullptr;  // pinned arena of all ViT layers (offload)
+  cudaStream_t copy_stream = nullptr, upload_stream = nullptr;
+  std::vector<cudaEvent_t> ev_loaded, ev_free;
+  int n_slots_total = 0, max_pages_per_req = 0;
+  // device per-slot state
+  bf16* d_pix = nullptr;
+  int* d_prompt = nullptr;
+  int* d_bt = nullptr;
+  int* d_last = nullptr;
+  size_t pix_stride = 0;
+  std::vector<cudaEvent_t> ev_upload;
+  // workspaces
+  struct FrontWS {
+    bf16 *x0, *xb, *qkv, *attn, *act;
+    float *hid, *vhid, *xf, *logits;
+    int *pos3, *tok;
+    int* h_pos3;  // pinned
+    int* h_tok;   // pinned
+    float* h_logits;
+  } fw{};
+  struct DecWS {
+    float *hid, *xf, *logits, *attn_ws;
+    bf16 *xb, *qkv, *attn, *act;
+    DecodeRow* rows;
+    int* tok;
+    DecodeRow* h_rows;
+    int* h_tok;
+    int* h_forced;
+    float* h_logits;
+  } dw{};
+  Partition part;
+  Worker front_w, dec_w;
+
+  // controller
+  std::mutex ctl_mu;
+  Alg1 alg;
+  std::deque<Request*> inbox;
+  std::mutex inbox_mu;
+  std::condition_variable wake;
+  std::mutex wake_mu;
+  std::deque<Event> completions;  // from workers
+  std::map<uint64_t, std::unique_ptr<Request>> reqs;
+  uint64_t next_id = 1;
+  std::vector<int> free_slots, free_pages;
+  std::deque<nova_token> tok_q;
+  std::mutex tok_mu;
+  std::vector<nova_log_record> log;
+  int tick_no = 0;
+  int finished = 0;
+  nova_step_info last_info{};
+
+  // sim backend
+  nova_sim_curves sc{};
+  std::vector<int32_t> sc_s;
+  std::vector<int64_t> sc_tv, sc_tp, sc_tdv, sc_tdp;
+  int64_t sim_now = 0;
+  struct SimPending {
+    int64_t t;
+    Event ev;
+  };
+  std::vector<SimPending> sim_pending;
+
+  // lifecycle
+  nova_status create(const nova_model_config* m, const nova_engine_config* c, const nova_buffers* b);
+  nova_status load_tensor(const char* name, const void* src, uint64_t nbytes, int on_dev);
+  nova_status finalize();
+  void shutdown();
+  ~Engine() { shutdown(); }
+  nova_status fail(nova_status s, const std::string& m) {
+    err = m;
+    if (s == NOVA_E_CUDA) failed = true;
+    return s;
+  }
+
+  // memory plans
+  static size_t plan_weights(const Dims& d, const nova_engine_config& c, Weights* w, VitLayerLayout* vl, uint8_t* base);
+  static size_t plan_workspace(const Dims& d, const nova_engine_config& c, Engine* e, uint8_t* base);
+  static size_t plan_kv(const Dims& d, const nova_engine_config& c);
+
+  // requests / ticks
+  nova_status submit(const nova_request* r, uint64_t* id);
+  nova_status step(int64_t max_wait_us, nova_step_info* out);
+  void dispatch(const Decision& d);
+  void post_completion(Event&& e);
+  void finish_request(Request* r);
+  void log_event(const Event& e);
+  void log_decision(const Decision& d, int64_t t);
+
+  // stage programs (model.cpp); return cudaError
+  int front_sms(int s_dec) const { return s_dec <= 0 ? part.total : part.total - s_dec; }
+  cudaError_t run_encode(Request* r, cudaStream_t s, int sms);
+  cudaError_t run_prefill(Request* r, cudaStream_t s, int sms);
+  cudaError_t run_decode(const std::vector<Request*>& rows, const std::vector<int>& forced, cudaStream_t s);
+  cudaStream_t stream_for(int role, int ctx, int s_dec);
+  int s_max_of_public() const;
+  nova_status time_pass(int stage, int s, int gh, int gw, int n_prompt, int B, int ctx, int corun, int iters,
+                        double* out);
+};
+
+}  // namespace nova

@@ -1,0 +1,211 @@
+// L5: the C ABI of include/nova.h -- argument checking and marshalling only; no
+// exception or C++ type crosses the boundary.
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "engine.h"
+
+using namespace nova;
+
+struct nova_engine {
+  Engine e;
+};
+
+static thread_local std::string g_create_err;
+
+#define GUARD(body)                                     \
+  try {                                                 \
+    body                                                \
+  } catch (const std::bad_alloc&) {                     \
+    return NOVA_E_NOMEM;                                \
+  } catch (...) {                                       \
+    return NOVA_E_STATE;                                \
+  }
+
+extern "C" {
+
+nova_status nova_query_memory(const nova_model_config* m, const nova_engine_config* c, uint64_t* wb, uint64_t* kb,
+                              uint64_t* ws, uint64_t* ph) {
+  if (!m || !c) return NOVA_E_INVAL;
+  GUARD({
+    Dims d;
+    d.init(*m);
+    if (wb) *wb = Engine::plan_weights(d, *c, nullptr, nullptr, nullptr);
+    if (kb) *kb = Engine::plan_kv(d, *c);
+    if (ws) *ws = Engine::plan_workspace(d, *c, nullptr, nullptr);
+    if (ph) {
+      VitLayerLayout vl;
+      vl.init(d);
+      const bool off = c->vit_resident_layers > 0 && c->vit_resident_layers < m->vit_depth;
+      *ph = off ? (uint64_t)m->vit_depth * vl.elems * 2 : 0;
+    }
+    return NOVA_OK;
+  })
+}
+
+nova_status nova_create(const nova_model_config* m, const nova_engine_config* c, const nova_buffers* b,
+                        nova_engine** out) {
+  if (!m || !c || !out) return NOVA_E_INVAL;
+  GUARD({
+    nova_engine* e = new nova_engine();
+    nova_status s = e->e.create(m, c, b);
+    if (s != NOVA_OK) {
+      g_create_err = e->e.err;
+      delete e;
+      *out = nullptr;
+      return s;
+    }
+    *out = e;
+    return NOVA_OK;
+  })
+}
+
+nova_status nova_load_tensor(nova_engine* e, const char* name, const void* src, uint64_t nbytes, int32_t on_dev) {
+  if (!e || !name || !src) return NOVA_E_INVAL;
+  if (e->e.finalized) return e->e.fail(NOVA_E_STATE, "load_tensor after finalize");
+  GUARD({ return e->e.load_tensor(name, src, nbytes, on_dev); })
+}
+
+nova_status nova_finalize(nova_engine* e) {
+  if (!e) return NOVA_E_INVAL;
+  GUARD({ return e->e.finalize(); })
+}
+
+nova_status nova_destroy(nova_engine* e) {
+  if (!e) return NOVA_E_INVAL;
+  GUARD({
+    delete e;
+    return NOVA_OK;
+  })
+}
+
+const char* nova_last_error(nova_engine* e) { return e ? e->e.err.c_str() : g_create_err.c_str(); }
+
+nova_status nova_query_sms(nova_engine* e, int32_t* total, int32_t* gran, int32_t* n_splits) {
+  if (!e) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  const bool live = !E.sim && E.finalized;
+  if (total) *total = live ? E.part.total : E.alg.total_sms;
+  if (gran) *gran = live ? E.part.granularity : E.alg.granularity;
+  if (n_splits) *n_splits = live ? E.part.n_groups - 1 : E.alg.max_split / std::max(1, E.alg.granularity);
+  return NOVA_OK;
+}
+
+nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* id) {
+  if (!e || !r || !id) return NOVA_E_INVAL;
+  GUARD({ return e->e.submit(r, id); })
+}
+
+nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, nova_partition_policy* applied) {
+  if (!e || !p) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_ADAPTIVE) return E.fail(NOVA_E_INVAL, "mode");
+  const int g = E.alg.granularity, mx = E.alg.max_split;
+  nova_partition_policy q = *p;
+  auto rnd = [&](int v) { return v / g * g; };
+  q.sm_decode_dv = rnd(q.sm_decode_dv);
+  q.sm_decode_dp = rnd(q.sm_decode_dp);
+  q.sm_op_dv = rnd(q.sm_op_dv);
+  q.sm_op_dp = rnd(q.sm_op_dp);
+  q.sm_min = rnd(q.sm_min);
+  if (q.b_max <= 0 || q.b_max > E.cfg.max_decode_batch) q.b_max = E.cfg.max_decode_batch;
+  if (q.mode == NOVA_MODE_STATIC && (q.sm_decode_dv < g || q.sm_decode_dp < g || q.sm_decode_dv > mx ||
+                                     q.sm_decode_dp > mx))
+    return E.fail(NOVA_E_PARTITION, "static decode budget outside [granularity, max split]");
+  if (q.mode == NOVA_MODE_ADAPTIVE && (q.sm_min < g || q.sm_op_dv < q.sm_min || q.sm_op_dp < q.sm_min ||
+                                       q.sm_op_dv > mx || q.sm_op_dp > mx || q.alpha_dv < 0 || q.alpha_dp < 0))
+    return E.fail(NOVA_E_PARTITION, "adaptive budgets outside [granularity, max split]");
+  E.alg.pol = q;
+  if (applied) *applied = q;
+  return NOVA_OK;
+}
+
+nova_status nova_step(nova_engine* e, int64_t max_wait_us, nova_step_info* out) {
+  if (!e) return NOVA_E_INVAL;
+  GUARD({ return e->e.step(max_wait_us, out); })
+}
+
+nova_status nova_poll_tokens(nova_engine* e, nova_token* buf, int32_t cap, int32_t* n_out) {
+  if (!e || (!buf && cap > 0) || !n_out) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  std::lock_guard<std::mutex> g(E.tok_mu);
+  int n = 0;
+  while (n < cap && !E.tok_q.empty()) {
+    buf[n++] = E.tok_q.front();
+    E.tok_q.pop_front();
+  }
+  *n_out = n;
+  return NOVA_OK;
+}
+
+nova_status nova_request_stats(nova_engine* e, uint64_t id, nova_req_stats* out) {
+  if (!e || !out) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  std::lock_guard<std::mutex> g(E.ctl_mu);
+  auto it = E.reqs.find(id);
+  if (it == E.reqs.end()) return NOVA_E_NOTFOUND;
+  *out = it->second->st;
+  return NOVA_OK;
+}
+
+nova_status nova_decision_log(nova_engine* e, int64_t start, nova_log_record* buf, int32_t cap, int32_t* n_out,
+                              int64_t* total) {
+  if (!e || start < 0) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  const int64_t tot = (int64_t)E.log.size();
+  int n = 0;
+  for (int64_t i = start; i < tot && n < cap; ++i) buf[n++] = E.log[i];
+  if (n_out) *n_out = n;
+  if (total) *total = tot;
+  return NOVA_OK;
+}
+
+nova_status nova_debug_logits(nova_engine* e, uint64_t id, int32_t index, float* out, int32_t vocab) {
+  if (!e || !out) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  if (!E.cfg.debug_keep_logits) return E.fail(NOVA_E_STATE, "debug_keep_logits is off");
+  std::lock_guard<std::mutex> g(E.ctl_mu);
+  auto it = E.reqs.find(id);
+  if (it == E.reqs.end()) return NOVA_E_NOTFOUND;
+  const auto& L = it->second->logits;
+  if (index < 0 || index >= (int)L.size() || vocab != (int)L[index].size()) return NOVA_E_INVAL;
+  std::memcpy(out, L[index].data(), (size_t)vocab * 4);
+  return NOVA_OK;
+}
+
+nova_status nova_debug_force_tokens(nova_engine* e, uint64_t id, const int32_t* tokens, int32_t n) {
+  if (!e || (!tokens && n > 0) || n < 0) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  std::lock_guard<std::mutex> g(E.ctl_mu);
+  auto it = E.reqs.find(id);
+  if (it == E.reqs.end()) return NOVA_E_NOTFOUND;
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] < 0 || tokens[i] >= E.dims.m.vocab) return NOVA_E_INVAL;
+  it->second->forced.assign(tokens, tokens + n);
+  return NOVA_OK;
+}
+
+nova_status nova_time_pass(nova_engine* e, int32_t stage, int32_t s, int32_t gh, int32_t gw, int32_t n_prompt,
+                           int32_t B, int32_t ctx, int32_t corun, int32_t iters, double* out_ms) {
+  if (!e || !out_ms) return NOVA_E_INVAL;
+  GUARD({ return e->e.time_pass(stage, s, gh, gw, n_prompt, B, ctx, corun, iters, out_ms); })
+}
+
+nova_status nova_sim_set_curves(nova_engine* e, const nova_sim_curves* c) {
+  if (!e || !c || c->n <= 0 || !c->s || !c->t_v || !c->t_p || !c->t_d_dv || !c->t_d_dp) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  if (!E.sim) return E.fail(NOVA_E_STATE, "sim curves on a GPU engine");
+  E.sc = *c;
+  E.sc_s.assign(c->s, c->s + c->n);
+  E.sc_tv.assign(c->t_v, c->t_v + c->n);
+  E.sc_tp.assign(c->t_p, c->t_p + c->n);
+  E.sc_tdv.assign(c->t_d_dv, c->t_d_dv + c->n);
+  E.sc_tdp.assign(c->t_d_dp, c->t_d_dp + c->n);
+  E.alg.total_sms = c->total_sms > 0 ? c->total_sms : 148;
+  E.alg.granularity = c->granularity > 0 ? c->granularity : 8;
+  E.alg.max_split = E.alg.total_sms - E.alg.granularity;
+  return NOVA_OK;
+}
+
+}  // extern "C"
