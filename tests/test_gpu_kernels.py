@@ -214,7 +214,9 @@ def test_norms_patchify_vitrope_embed_argmax():
     rng = np.random.default_rng(5)
     M, d = 37, 1280
     x = rng.standard_normal((M, d)).astype(np.float32) * 3
-    g, b = rand_bf16(rng, (d,), 0.1) + 1, rand_bf16(rng, (d,), 0.05)
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    g = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (d,), 0.1) + 1))   # gamma exactly representable
+    b = rand_bf16(rng, (d,), 0.05)
     y = torch.empty(M, d, dtype=torch.bfloat16, device="cuda")
     O.nova_op_layernorm(torch.from_numpy(x).cuda(), bf16_dev(g), bf16_dev(b), y, M, d, 1e-6)
     torch.cuda.synchronize()
