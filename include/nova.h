@@ -103,7 +103,7 @@ nova_status nova_query_sms(nova_engine* e, int32_t* total_sms, int32_t* granular
 
 /* ------------------------------------------------------------------ requests */
 typedef struct {
-  const uint16_t* pixels_bf16; /* [3][height][width] bf16 bits, host memory                    */
+  const uint16_t* pixels_bf16; /* [3][height][width] bf16 bits, host or device memory (UVA)    */
   int32_t height, width;       /* multiples of patch * merge (28)                               */
   const int32_t* prompt_ids;   /* host [n_prompt], each < vocab                                 */
   int32_t n_prompt;
@@ -190,6 +190,31 @@ nova_status nova_debug_logits(nova_engine* e, uint64_t req_id, int32_t index, fl
 /* Teacher forcing: decode step k (k >= 1) consumes tokens[k-1] instead of the argmax
  * of step k-1.  Must be called right after nova_submit. */
 nova_status nova_debug_force_tokens(nova_engine* e, uint64_t req_id, const int32_t* tokens, int32_t n);
+
+/* ------------------------------------------------------------------ live kernel timing */
+/* Kernel classes with their ALGORITHMIC work unit (what the method must move or
+ * compute, no padding):                                        */
+enum {
+  NOVA_K_DEC_GEMV = 0,   /* decode linears: bytes = N*K*2 (weights) + B*K*sx + B*N*sy       */
+  NOVA_K_VIT_GEMM = 1,   /* ViT + merger linears: flops = 2*M*N*K                           */
+  NOVA_K_LLM_GEMM = 2,   /* prefill linears: flops = 2*M*N*K                                */
+  NOVA_K_VIT_ATTN = 3,   /* ViT attention: flops = 4*N^2*hd*heads                           */
+  NOVA_K_PRE_ATTN = 4,   /* prefill causal attention: flops = 2*S^2*hd*heads (causal half)  */
+  NOVA_K_DEC_ATTN = 5,   /* decode attention: bytes = sum_b (ctx_b+1)*2*KV*hd*2             */
+  NOVA_K_LM_HEAD = 6,    /* lm_head GEMV: bytes = V*D*2                                     */
+  NOVA_K_VIT_PASS = 7,   /* whole vision pass: flops (SURVEY §8(d) d2 a5 formula)           */
+  NOVA_K_PRE_PASS = 8,   /* whole prefill pass: flops (a6 formula)                          */
+  NOVA_K_DEC_PASS = 9,   /* whole decode iteration: bytes = weights + KV read (a7 formula)  */
+  NOVA_K_COUNT = 10
+};
+/* every_n = 0 disables; n >= 1 brackets the kernels of every n-th pass of each role
+ * with CUDA events on the stream they are launched on (whole passes: every pass). */
+nova_status nova_kernel_timing(nova_engine* e, int32_t every_n);
+/* out[0] = summed device ms, out[1] = summed algorithmic work, out[2] = launches. */
+nova_status nova_kernel_stats(nova_engine* e, int32_t cls, double* out3);
+nova_status nova_kernel_stats_reset(nova_engine* e);
+/* Total libnova kernel launches in this process so far (all engines and nova_op_*). */
+uint64_t nova_launch_count(void);
 
 /* ------------------------------------------------------------------ curves + planner */
 /* Time one forward pass with the SM split s (decode SMs; front gets the rest,

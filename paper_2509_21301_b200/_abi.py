@@ -96,6 +96,10 @@ ENGINE_SIGNATURES = {
     "nova_next_logical_layer": (I32, [I32, I32, I32]),
     "nova_required_bandwidth": (F64, [F64, F64, I32, I32]),
     "nova_sim_set_curves": (R, [E, C.POINTER(SimCurves)]),
+    "nova_kernel_timing": (R, [E, I32]),
+    "nova_kernel_stats": (R, [E, I32, C.POINTER(F64)]),
+    "nova_kernel_stats_reset": (R, [E]),
+    "nova_launch_count": (U64, []),
 }
 
 

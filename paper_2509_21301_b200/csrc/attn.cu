@@ -174,6 +174,7 @@ cudaError_t fa_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H,
   const float sl2 = LOG2E / sqrtf((float)HD);
   dim3 grid((S + 63) / 64, H), block(128);
   const int smem = FaCfg<HD>::SMEM;
+  count_launch();
   if (causal) {
     static bool set = false;
     if (!set) {
@@ -307,6 +308,7 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
   if (H / KV > MAXG) return cudaErrorInvalidValue;
   const int n_chunks = (max_ctx + 1 + DCHUNK - 1) / DCHUNK;
   const float sl2 = LOG2E / sqrtf((float)HD);
+  count_launch(2);
   decode_attn_partial<HD><<<dim3(B, KV, n_chunks), DCHUNK, 0, s>>>(qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages,
                                                                     rows, ws, n_chunks, sl2);
   decode_attn_combine<HD><<<dim3(B, H), HD, 0, s>>>(ws, rows, out, ldo, H, n_chunks);

@@ -116,6 +116,31 @@ struct Partition {
   int max_split() const { return (n_groups - 1) * granularity; }
 };
 
+// ------------------------------------------------------------------ live kernel timing
+// Sampled CUDA-event brackets around the stage kernels (for the roofline report):
+// per class the summed device time, the summed ALGORITHMIC work (bytes or FLOPs) and
+// the launch count.  Classes are NOVA_K_* in nova.h.
+struct KStat {
+  double ms = 0, work = 0;
+  int64_t launches = 0;
+};
+struct KTimer {
+  std::vector<cudaEvent_t> ev;
+  struct Rec {
+    int cls;
+    double work;
+    int i0;
+  };
+  std::vector<Rec> recs;
+  int n = 0;
+  bool on = false;
+  void init(int pairs);
+  void destroy();
+  int begin(cudaStream_t s);
+  void end(int i0, int cls, double work, cudaStream_t s);
+  void harvest(KStat* out, std::mutex& mu);  // after the pass completed
+};
+
 // ------------------------------------------------------------------ GPU role worker
 struct PassCmd {
   int kind;  // NOVA_DEC_VISION / PREFILL / DECODE
@@ -186,6 +211,12 @@ class Engine {
   } dw{};
   Partition part;
   Worker front_w, dec_w;
+  KTimer ktimer[2];                  // per role (0 front, 1 decode)
+  KStat kstats[NOVA_K_COUNT];
+  std::mutex kmu;
+  int64_t pass_count[2] = {0, 0};
+  int sample_every = 0;              // 0 = kernel timing off; n = time every n-th pass of a role
+  double pass_work[2] = {0, 0};      // algorithmic work of the last pass issued by each role
 
   // controller
   std::mutex ctl_mu;

@@ -149,8 +149,10 @@ static void spin_wait(cudaEvent_t ev) {
 
 void Worker::run() {
   cudaSetDevice(eng->cfg.device);
-  cudaEvent_t ev;
+  cudaEvent_t ev, p0, p1;
   cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventCreate(&p0);
+  cudaEventCreate(&p1);
   for (;;) {
     PassCmd c;
     {
@@ -162,6 +164,9 @@ void Worker::run() {
     }
     cudaStream_t s = eng->stream_for(role, c.ctx, c.s_dec);
     cudaError_t e = cudaSuccess;
+    const bool timing = eng->sample_every > 0;
+    eng->ktimer[role].on = timing && (eng->pass_count[role]++ % eng->sample_every == 0);
+    if (timing) cudaEventRecord(p0, s);
     Event done;
     done.reqs = c.reqs;
     done.key = c.reqs.empty() ? 0 : c.reqs[0]->id;
@@ -176,12 +181,26 @@ void Worker::run() {
       done.kind = NOVA_EV_DECODE_DONE;
       for (Request* r : c.reqs) done.key = std::min<uint64_t>(done.key, r->id);
     }
+    if (e == cudaSuccess && timing) e = cudaEventRecord(p1, s);
     if (e == cudaSuccess) e = cudaEventRecord(ev, s);
     if (e == cudaSuccess) {
       spin_wait(ev);
       e = cudaEventQuery(ev) == cudaSuccess ? cudaSuccess : cudaGetLastError();
     }
     done.t = mono_ns();
+    if (e == cudaSuccess && timing) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p0, p1);
+      const int cls = c.kind == NOVA_DEC_VISION ? NOVA_K_VIT_PASS
+                                                : (c.kind == NOVA_DEC_PREFILL ? NOVA_K_PRE_PASS : NOVA_K_DEC_PASS);
+      {
+        std::lock_guard<std::mutex> g(eng->kmu);
+        eng->kstats[cls].ms += ms;
+        eng->kstats[cls].work += eng->pass_work[role];
+        eng->kstats[cls].launches += 1;
+      }
+      eng->ktimer[role].harvest(eng->kstats, eng->kmu);
+    }
     if (e != cudaSuccess) {
       eng->err = std::string("CUDA error in stage pass: ") + cudaGetErrorString(e);
       eng->failed = true;
@@ -202,6 +221,8 @@ void Worker::run() {
     eng->post_completion(std::move(done));
   }
   cudaEventDestroy(ev);
+  cudaEventDestroy(p0);
+  cudaEventDestroy(p1);
 }
 
 void Engine::post_completion(Event&& e) {
@@ -294,6 +315,8 @@ nova_status Engine::finalize() {
   cudaMemset(d_prompt, 0, (size_t)n_slots_total * cfg.max_prompt * 4);
   cudaMemset(d_bt, 0, (size_t)n_slots_total * max_pages_per_req * 4);
   cudaMemset(d_last, 0, (size_t)n_slots_total * 4);
+  ktimer[0].init(512);
+  ktimer[1].init(512);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(NOVA_E_CUDA, "finalize sync");
   front_w.start(this, 0);
   dec_w.start(this, 1);
@@ -312,6 +335,8 @@ void Engine::shutdown() {
       if (w->th.joinable()) w->th.join();
     }
     cudaDeviceSynchronize();
+    ktimer[0].destroy();
+    ktimer[1].destroy();
     part.destroy();
     for (auto ev : ev_upload) cudaEventDestroy(ev);
     for (auto ev : ev_loaded) cudaEventDestroy(ev);
@@ -379,8 +404,9 @@ nova_status Engine::submit(const nova_request* q, uint64_t* id) {
   }
   if (!sim) {
     const size_t npix = (size_t)m.in_ch * q->height * q->width;
-    cudaError_t e = cudaMemcpyAsync(d_pix + (size_t)r->slot * pix_stride, q->pixels_bf16, npix * 2,
-                                    cudaMemcpyHostToDevice, upload_stream);
+    // pixels may be host or device memory (UVA): H2D for host buffers, D2D for HBM-resident inputs
+    cudaError_t e = cudaMemcpyAsync(d_pix + (size_t)r->slot * pix_stride, q->pixels_bf16, npix * 2, cudaMemcpyDefault,
+                                    upload_stream);
     if (e == cudaSuccess && q->n_prompt > 0)
       e = cudaMemcpyAsync(d_prompt + (size_t)r->slot * cfg.max_prompt, q->prompt_ids, q->n_prompt * 4,
                           cudaMemcpyHostToDevice, upload_stream);

@@ -268,6 +268,7 @@ cudaError_t launch_bn(const bf16* A, int lda, const bf16* W, int ldw, const Gemm
   const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
   int grid = tiles < max_ctas ? tiles : max_ctas;
   if (grid < 1) grid = 1;
+  count_launch();
   kern<<<grid, 256, GemmCfg<BN>::SMEM, s>>>(ma, mb, g);
   return cudaGetLastError();
 }

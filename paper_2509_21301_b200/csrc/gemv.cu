@@ -188,6 +188,7 @@ cudaError_t launch_nt(const void* X, int ldx, const bf16* W, int N, int K, void*
                       int epi, cudaStream_t s) {
   const int kslice = ((K + WARPS * 32 - 1) / (WARPS * 32)) * 32;
   dim3 grid(N / ROWS), block(WARPS * 32);
+  count_launch();
   switch (epi) {
     case EPI_BF16:
       gemv_kernel<NT, XF32, EPI_BF16><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);

@@ -8,9 +8,15 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace nova {
 
 typedef __nv_bfloat16 bf16;
+
+// Number of libnova kernels launched in this process (incremented by every launcher).
+extern std::atomic<unsigned long long> g_kernel_launches;
+inline void count_launch(int n = 1) { g_kernel_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 // GEMM / GEMV epilogues (C = A . W^T + bias, then):
 enum Epi {

@@ -223,10 +223,13 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int ldl, int V, 
 
 }  // namespace
 
+std::atomic<unsigned long long> g_kernel_launches{0};
+
 cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d, float eps,
                       cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
+  count_launch();
   layernorm_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, g, b, y, ldy, M, d, eps);
   return cudaGetLastError();
 }
@@ -234,17 +237,20 @@ cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, 
                     cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
+  count_launch();
   rmsnorm_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, g, y, y_f32, ldy, M, d, eps);
   return cudaGetLastError();
 }
 cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int merge, bf16* X0, cudaStream_t s) {
   const int N = (H / P) * (W / P);
   if (N <= 0) return cudaSuccess;
+  count_launch();
   patchify_kernel<<<N, 256, 0, s>>>(pix, C, H, W, P, T, merge, X0);
   return cudaGetLastError();
 }
 cudaError_t vit_rope(bf16* qkv, int N, int heads, int hd, int gw, int merge, float theta, cudaStream_t s) {
   if (N <= 0) return cudaSuccess;
+  count_launch();
   vit_rope_kernel<<<N, 256, 0, s>>>(qkv, heads, hd, gw, merge, log2f(theta));
   return cudaGetLastError();
 }
@@ -252,6 +258,7 @@ cudaError_t llm_rope_kv(bf16* qkv, int ld, int nrows, int H, int KV, int hd, flo
                         const int* pos3, int ld_pos, const DecodeRow* rows, int slot, int ctx0, bf16* pool, int layer,
                         int n_pages, const int* bt, int max_pages, cudaStream_t s) {
   if (nrows <= 0) return cudaSuccess;
+  count_launch();
   llm_rope_kv_kernel<<<nrows, 256, 0, s>>>(qkv, ld, H, KV, hd, log2f(theta), sec0, sec1, pos3, ld_pos, rows, slot,
                                            ctx0, pool, layer, n_pages, bt, max_pages);
   return cudaGetLastError();
@@ -259,12 +266,14 @@ cudaError_t llm_rope_kv(bf16* qkv, int ld, int nrows, int H, int KV, int hd, flo
 cudaError_t embed(const bf16* table, int d, const int* ids, const DecodeRow* rows, const int* last_tok, float* out,
                   int ldo, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  count_launch();
   embed_kernel<<<n, 256, 0, s>>>(table, d, ids, rows, last_tok, out, ldo);
   return cudaGetLastError();
 }
 cudaError_t argmax_rows(const float* logits, int ldl, int V, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
                         int single_slot, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  count_launch();
   argmax_kernel<<<n, 1024, 0, s>>>(logits, ldl, V, out_tok, rows, last_tok, single_slot);
   return cudaGetLastError();
 }

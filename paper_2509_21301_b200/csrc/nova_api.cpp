@@ -192,6 +192,30 @@ nova_status nova_time_pass(nova_engine* e, int32_t stage, int32_t s, int32_t gh,
   GUARD({ return e->e.time_pass(stage, s, gh, gw, n_prompt, B, ctx, corun, iters, out_ms); })
 }
 
+nova_status nova_kernel_timing(nova_engine* e, int32_t every_n) {
+  if (!e || every_n < 0) return NOVA_E_INVAL;
+  e->e.sample_every = every_n;
+  return NOVA_OK;
+}
+
+nova_status nova_kernel_stats(nova_engine* e, int32_t cls, double* out3) {
+  if (!e || !out3 || cls < 0 || cls >= NOVA_K_COUNT) return NOVA_E_INVAL;
+  std::lock_guard<std::mutex> g(e->e.kmu);
+  out3[0] = e->e.kstats[cls].ms;
+  out3[1] = e->e.kstats[cls].work;
+  out3[2] = (double)e->e.kstats[cls].launches;
+  return NOVA_OK;
+}
+
+uint64_t nova_launch_count(void) { return g_kernel_launches.load(); }
+
+nova_status nova_kernel_stats_reset(nova_engine* e) {
+  if (!e) return NOVA_E_INVAL;
+  std::lock_guard<std::mutex> g(e->e.kmu);
+  for (auto& k : e->e.kstats) k = KStat{};
+  return NOVA_OK;
+}
+
 nova_status nova_sim_set_curves(nova_engine* e, const nova_sim_curves* c) {
   if (!e || !c || c->n <= 0 || !c->s || !c->t_v || !c->t_p || !c->t_d_dv || !c->t_d_dp) return NOVA_E_INVAL;
   Engine& E = e->e;

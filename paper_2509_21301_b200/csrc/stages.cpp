@@ -1,0 +1,241 @@
+// L2 stage programs: the vision encode, LLM prefill and LLM decode forward passes
+// (§II-A, Table stage_duration; SURVEY.md §8(a) rows a5,
+// a6, a7) as launch sequences of the sm_100a kernels, with the layer-wise ViT
+// weight swap-in of PAPER.md §III-E (Eq. 7; row a9) inside encode.
+// Every launch goes through t_gemm / t_gemv / t_attn, which add the kernel's
+// ALGORITHMIC work to the pass total and, on sampled passes, bracket it with CUDA
+// events on its own stream (live roofline numbers, nova_kernel_stats).
+#include <algorithm>
+
+#include "engine.h"
+
+namespace nova {
+
+#define CUDA_TRY(x)                   \
+  do {                                \
+    cudaError_t _e = (x);             \
+    if (_e != cudaSuccess) return _e; \
+  } while (0)
+
+// ---------------------------------------------------------------- kernel timer
+void KTimer::init(int pairs) {
+  ev.assign(2 * pairs, nullptr);
+  for (auto& e : ev) cudaEventCreate(&e);
+}
+void KTimer::destroy() {
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  ev.clear();
+}
+int KTimer::begin(cudaStream_t s) {
+  if (!on || n + 2 > (int)ev.size()) return -1;
+  cudaEventRecord(ev[n], s);
+  return n;
+}
+void KTimer::end(int i0, int cls, double work, cudaStream_t s) {
+  if (i0 < 0) return;
+  cudaEventRecord(ev[i0 + 1], s);
+  recs.push_back(Rec{cls, work, i0});
+  n += 2;
+}
+void KTimer::harvest(KStat* out, std::mutex& mu) {
+  std::lock_guard<std::mutex> g(mu);
+  for (const Rec& r : recs) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ev[r.i0], ev[r.i0 + 1]) == cudaSuccess) {
+      out[r.cls].ms += ms;
+      out[r.cls].work += r.work;
+      out[r.cls].launches += 1;
+    }
+  }
+  recs.clear();
+  n = 0;
+}
+
+static cudaError_t t_gemm(Engine* E, int role, int cls, const bf16* A, int lda, const bf16* W, int ldw, void* C,
+                          int ldc, const bf16* bias, int M, int N, int K, int epi, int sms, cudaStream_t s) {
+  const double w = 2.0 * M * N * K;
+  E->pass_work[role] += w;
+  const int i = E->ktimer[role].begin(s);
+  CUDA_TRY(gemm_tc(A, lda, W, ldw, C, ldc, bias, M, N, K, epi, sms, s));
+  E->ktimer[role].end(i, cls, w, s);
+  return cudaSuccess;
+}
+
+static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xf32, int ldx, const bf16* W, int N, int K, void* Y,
+                          int ldy, const bf16* bias, int B, int epi, cudaStream_t s) {
+  const int nout = epi == EPI_BF16_SILUMUL ? N / 2 : N;
+  const int ysz = epi == EPI_F32_RESID ? 8 : (epi == EPI_F32_STORE ? 4 : 2);
+  const double bytes = (double)N * K * 2 + (double)B * K * (xf32 ? 4 : 2) + (double)B * nout * ysz;
+  E->pass_work[1] += bytes;
+  const int i = E->ktimer[1].begin(s);
+  CUDA_TRY(gemv(X, xf32, ldx, W, N, K, Y, ldy, bias, B, epi, s));
+  E->ktimer[1].end(i, cls, bytes, s);
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- vision encode (a5)
+cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
+  const auto& m = dims.m;
+  const int gh = r->gh, gw = r->gw, N = gh * gw, Dv = m.vit_dim, hd = dims.vit_hd;
+  const int H = gh * m.patch, Wd = gw * m.patch;
+  pass_work[0] = 0;
+  CUDA_TRY(cudaStreamWaitEvent(s, ev_upload[r->slot], 0));
+  CUDA_TRY(patchify(d_pix + (size_t)r->slot * pix_stride, m.in_ch, H, Wd, m.patch, m.temporal_patch, m.merge, fw.x0, s));
+  CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.x0, dims.patch_dim, W.patch_w, dims.patch_dim, fw.vhid, Dv, nullptr, N,
+                  Dv, dims.patch_dim, EPI_F32_STORE, sms, s));
+  const int L = m.vit_depth;
+  for (int l = 0; l < L; ++l) {
+    bf16* blk;
+    int k = 0;
+    if (vit_K > 0) {  // Eq. 7 ring: slot l mod K holds logical layer l
+      k = l % vit_K;
+      CUDA_TRY(cudaStreamWaitEvent(s, ev_loaded[k], 0));
+      blk = W.vit_dev[k];
+    } else {
+      blk = W.vit_dev[l];
+    }
+    CUDA_TRY(layernorm(fw.vhid, Dv, blk + vl.n1g, blk + vl.n1b, fw.xb, Dv, N, Dv, m.ln_eps, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.xb, Dv, blk + vl.qkv_w, Dv, fw.qkv, 3 * Dv, blk + vl.qkv_b, N, 3 * Dv,
+                    Dv, EPI_BF16, sms, s));
+    CUDA_TRY(vit_rope(fw.qkv, N, m.vit_heads, hd, gw, m.merge, m.vit_theta, s));
+    {
+      const double w = 4.0 * N * N * hd * m.vit_heads;
+      pass_work[0] += w;
+      const int i = ktimer[0].begin(s);
+      CUDA_TRY(flash_attn(fw.qkv, 3 * Dv, fw.attn, Dv, N, m.vit_heads, m.vit_heads, hd, 0, s));
+      ktimer[0].end(i, NOVA_K_VIT_ATTN, w, s);
+    }
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.attn, Dv, blk + vl.proj_w, Dv, fw.vhid, Dv, blk + vl.proj_b, N, Dv,
+                    Dv, EPI_F32_RESID, sms, s));
+    CUDA_TRY(layernorm(fw.vhid, Dv, blk + vl.n2g, blk + vl.n2b, fw.xb, Dv, N, Dv, m.ln_eps, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.xb, Dv, blk + vl.fc1_w, Dv, fw.act, m.vit_mlp, blk + vl.fc1_b, N,
+                    m.vit_mlp, Dv, EPI_BF16_QGELU, sms, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.act, m.vit_mlp, blk + vl.fc2_w, m.vit_mlp, fw.vhid, Dv,
+                    blk + vl.fc2_b, N, Dv, m.vit_mlp, EPI_F32_RESID, sms, s));
+    if (vit_K > 0) {  // swap in logical layer (l + K) mod L once slot k is free (Eq. 7)
+      CUDA_TRY(cudaEventRecord(ev_free[k], s));
+      CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_free[k], 0));
+      const int nxt = (l + vit_K) % L;
+      CUDA_TRY(cudaMemcpyAsync(W.vit_dev[k], host_vit + (size_t)nxt * vl.elems, vl.elems * 2, cudaMemcpyHostToDevice,
+                               copy_stream));
+      CUDA_TRY(cudaEventRecord(ev_loaded[k], copy_stream));
+    }
+  }
+  // merger: LN -> view [N/4][4 Dv] -> Linear + GELU -> Linear -> E_vis rows 0..n_v of the prefill hidden
+  const int nv = N / (m.merge * m.merge), md = dims.merge_dim;
+  CUDA_TRY(layernorm(fw.vhid, Dv, W.mlnq_g, W.mlnq_b, fw.xb, Dv, N, Dv, m.ln_eps, s));
+  CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.xb, md, W.m1_w, md, fw.act, md, W.m1_b, nv, md, md, EPI_BF16_GELU, sms,
+                  s));
+  CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.act, md, W.m2_w, md, fw.hid, m.llm_dim, W.m2_b, nv, m.llm_dim, md,
+                  EPI_F32_STORE, sms, s));
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- LLM prefill (a6)
+cudaError_t Engine::run_prefill(Request* r, cudaStream_t s, int sms) {
+  const auto& m = dims.m;
+  const int D = m.llm_dim, H = m.llm_heads, KV = m.llm_kv_heads, hd = m.head_dim, F = m.llm_ffn;
+  const int nv = r->n_v(), S = r->S(), ldq = dims.llm_qkv_n;
+  pass_work[0] = 0;
+  // M-RoPE positions (HF get_rope_index, image first): vision (0, r, c), text st + i
+  const int lw = r->gw / m.merge, st = std::max(r->gh / m.merge, lw);
+  for (int j = 0; j < S; ++j) {
+    if (j < nv) {
+      fw.h_pos3[j] = 0;
+      fw.h_pos3[S + j] = j / lw;
+      fw.h_pos3[2 * S + j] = j % lw;
+    } else {
+      fw.h_pos3[j] = fw.h_pos3[S + j] = fw.h_pos3[2 * S + j] = st + (j - nv);
+    }
+  }
+  CUDA_TRY(cudaMemcpyAsync(fw.pos3, fw.h_pos3, 3 * S * sizeof(int), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(embed(W.embed, D, d_prompt + (size_t)r->slot * cfg.max_prompt, nullptr, nullptr, fw.hid + (size_t)nv * D,
+                 D, r->n_prompt, s));
+  bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
+  for (int l = 0; l < m.llm_layers; ++l) {
+    const LlmLayerW& L = W.llm[l];
+    CUDA_TRY(rmsnorm(fw.hid, D, L.ln1, fw.xb, 0, D, S, D, m.rms_eps, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.xb, D, L.qkv_w, D, fw.qkv, ldq, L.qkv_b, S, ldq, D, EPI_BF16, sms, s));
+    CUDA_TRY(llm_rope_kv(fw.qkv, ldq, S, H, KV, hd, m.llm_theta, m.mrope_section[0], m.mrope_section[1], fw.pos3, S,
+                         nullptr, r->slot, 0, pool, l, cfg.kv_pages, d_bt, max_pages_per_req, s));
+    {
+      const double w = 2.0 * S * S * hd * H;
+      pass_work[0] += w;
+      const int i = ktimer[0].begin(s);
+      CUDA_TRY(flash_attn(fw.qkv, ldq, fw.attn, H * hd, S, H, KV, hd, 1, s));
+      ktimer[0].end(i, NOVA_K_PRE_ATTN, w, s);
+    }
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.attn, H * hd, L.o_w, H * hd, fw.hid, D, nullptr, S, D, H * hd,
+                    EPI_F32_RESID, sms, s));
+    CUDA_TRY(rmsnorm(fw.hid, D, L.ln2, fw.xb, 0, D, S, D, m.rms_eps, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.xb, D, L.gu_w, D, fw.act, F, nullptr, S, 2 * F, D, EPI_BF16_SILUMUL,
+                    sms, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.act, F, L.down_w, F, fw.hid, D, nullptr, S, D, F, EPI_F32_RESID, sms,
+                    s));
+  }
+  // token 0: final RMSNorm (f32 out) of the last row -> lm_head GEMV (f32 logits) -> argmax
+  CUDA_TRY(rmsnorm(fw.hid + (size_t)(S - 1) * D, D, W.final_norm, fw.xf, 1, D, 1, D, m.rms_eps, s));
+  pass_work[0] += 2.0 * D * m.vocab;
+  CUDA_TRY(gemv(fw.xf, 1, D, W.lm_head, m.vocab, D, fw.logits, m.vocab, nullptr, 1, EPI_F32_STORE, s));
+  CUDA_TRY(argmax_rows(fw.logits, m.vocab, m.vocab, 1, fw.tok, nullptr, d_last, r->slot, s));
+  CUDA_TRY(cudaMemcpyAsync(fw.h_tok, fw.tok, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (cfg.debug_keep_logits)
+    CUDA_TRY(cudaMemcpyAsync(fw.h_logits, fw.logits, (size_t)m.vocab * 4, cudaMemcpyDeviceToHost, s));
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- LLM decode iteration (a7)
+cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vector<int>& forced, cudaStream_t s) {
+  const auto& m = dims.m;
+  const int D = m.llm_dim, H = m.llm_heads, KV = m.llm_kv_heads, hd = m.head_dim, F = m.llm_ffn;
+  const int B = (int)rq.size(), ldq = dims.llm_qkv_n;
+  pass_work[1] = 0;
+  int max_ctx = 0;
+  double kv_bytes_layer = 0;
+  for (int b = 0; b < B; ++b) {
+    Request* r = rq[b];
+    const int e = r->emitted;  // tokens emitted so far; feed token e-1
+    const int st = std::max(r->gh / m.merge, r->gw / m.merge);
+    dw.h_rows[b] = DecodeRow{r->slot, r->S() + e - 1, st + r->n_prompt - 1 + e, 0};
+    max_ctx = std::max(max_ctx, dw.h_rows[b].ctx);
+    kv_bytes_layer += (double)(dw.h_rows[b].ctx + 1) * 2 * KV * hd * 2;
+  }
+  CUDA_TRY(cudaMemcpyAsync(dw.rows, dw.h_rows, B * sizeof(DecodeRow), cudaMemcpyHostToDevice, s));
+  for (int b = 0; b < B; ++b)
+    if (forced[b] >= 0) {
+      dw.h_forced[b] = forced[b];
+      CUDA_TRY(cudaMemcpyAsync(d_last + rq[b]->slot, dw.h_forced + b, 4, cudaMemcpyHostToDevice, s));
+    }
+  CUDA_TRY(embed(W.embed, D, nullptr, dw.rows, d_last, dw.hid, D, B, s));
+  bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
+  for (int l = 0; l < m.llm_layers; ++l) {
+    const LlmLayerW& L = W.llm[l];
+    CUDA_TRY(rmsnorm(dw.hid, D, L.ln1, dw.xb, 0, D, B, D, m.rms_eps, s));
+    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.xb, 0, D, L.qkv_w, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_BF16, s));
+    CUDA_TRY(llm_rope_kv(dw.qkv, ldq, B, H, KV, hd, m.llm_theta, m.mrope_section[0], m.mrope_section[1], nullptr, 0,
+                         dw.rows, 0, 0, pool, l, cfg.kv_pages, d_bt, max_pages_per_req, s));
+    {
+      pass_work[1] += kv_bytes_layer;
+      const int i = ktimer[1].begin(s);
+      CUDA_TRY(decode_attn(dw.qkv, ldq, dw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
+                           dw.rows, B, max_ctx, dw.attn_ws, s));
+      ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
+    }
+    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.attn, 0, H * hd, L.o_w, D, H * hd, dw.hid, D, nullptr, B, EPI_F32_RESID,
+                    s));
+    CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
+    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.xb, 0, D, L.gu_w, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL, s));
+    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.act, 0, F, L.down_w, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, s));
+  }
+  CUDA_TRY(rmsnorm(dw.hid, D, W.final_norm, dw.xf, 1, D, B, D, m.rms_eps, s));
+  CUDA_TRY(t_gemv(this, NOVA_K_LM_HEAD, dw.xf, 1, D, W.lm_head, m.vocab, D, dw.logits, m.vocab, nullptr, B,
+                  EPI_F32_STORE, s));
+  CUDA_TRY(argmax_rows(dw.logits, m.vocab, m.vocab, B, dw.tok, dw.rows, d_last, -1, s));
+  CUDA_TRY(cudaMemcpyAsync(dw.h_tok, dw.tok, B * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (cfg.debug_keep_logits)
+    CUDA_TRY(cudaMemcpyAsync(dw.h_logits, dw.logits, (size_t)B * m.vocab * 4, cudaMemcpyDeviceToHost, s));
+  return cudaSuccess;
+}
+
+}  // namespace nova

@@ -20,6 +20,12 @@ CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 DEC_VISION, DEC_PREFILL, DEC_DECODE, DEC_FINISH = 0, 1, 2, 3
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
 BACKEND_GPU, BACKEND_SIM = 0, 1
+# NOVA_K_* classes (nova.h) and the unit of their algorithmic work
+KERNEL_CLASSES = ["dec_gemv", "vit_gemm", "llm_gemm", "vit_attn", "pre_attn", "dec_attn", "lm_head", "vit_pass",
+                  "pre_pass", "dec_pass"]
+KERNEL_UNITS = {"dec_gemv": "bytes", "vit_gemm": "flops", "llm_gemm": "flops", "vit_attn": "flops",
+                "pre_attn": "flops", "dec_attn": "bytes", "lm_head": "bytes", "vit_pass": "flops",
+                "pre_pass": "flops", "dec_pass": "bytes"}
 
 
 class NovaError(RuntimeError):
@@ -213,6 +219,21 @@ class Engine:
         self._check(self.lib.nova_time_pass(self.h, stage, s, gh, gw, n_prompt, B, ctx, corun, iters, out),
                     "nova_time_pass")
         return out[0], out[1]
+
+    def kernel_timing(self, every_n: int) -> None:
+        self._check(self.lib.nova_kernel_timing(self.h, every_n), "nova_kernel_timing")
+
+    def kernel_stats(self) -> dict:
+        """{class: (device ms, algorithmic work, launches)} for the NOVA_K_* classes."""
+        out = {}
+        buf = (A.F64 * 3)()
+        for cls, name in enumerate(KERNEL_CLASSES):
+            self._check(self.lib.nova_kernel_stats(self.h, cls, buf), "nova_kernel_stats")
+            out[name] = (buf[0], buf[1], int(buf[2]))
+        return out
+
+    def kernel_stats_reset(self) -> None:
+        self._check(self.lib.nova_kernel_stats_reset(self.h), "nova_kernel_stats_reset")
 
     def sim_set_curves(self, splits, t_v, t_p, t_d_dv, t_d_dp, t_v_solo, t_p_solo, t_d_solo, beta=0.0,
                        total_sms=148, granularity=8):
