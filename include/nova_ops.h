@@ -53,6 +53,12 @@ int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K,
 int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int S, int H, int KV, int hd, int causal,
                        void* stream);
 
+/* Same contract, forced onto the legacy warp-level mma.sync kernel (the measured
+ * baseline the tcgen05 path is compared against); hd in {16, 32, 64, 80, 128}.
+ * nova_op_flash_attn uses the tcgen05/TMEM kernel for hd 80 and 128. */
+int nova_op_flash_attn_mma(const void* qkv, int ld, void* out, int ldo, int S, int H, int KV, int hd, int causal,
+                           void* stream);
+
 /* Row descriptor of one decode request (device memory, 16 bytes). */
 typedef struct {
   int32_t slot; /* request slot: row of block_tables and of last_tok       */

@@ -22,6 +22,7 @@ OPS_SIGNATURES = {
     "nova_op_gemm": [P, I, P, I, P, I, P, I, I, I, I, I, P],
     "nova_op_gemv": [P, I, I, P, I, I, P, I, P, I, I, P],
     "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, P],
+    "nova_op_flash_attn_mma": [P, I, P, I, I, I, I, I, I, P],
     "nova_op_decode_attn": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P],
     "nova_op_layernorm": [P, I, P, P, P, I, I, I, F, P],
     "nova_op_rmsnorm": [P, I, P, P, I, I, I, I, F, P],

@@ -203,6 +203,8 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
                                                               int H, int KV, const int* __restrict__ bt, int max_pages,
                                                               const DecodeRow* __restrict__ rows, float* __restrict__ ws,
                                                               int n_chunks, float scale_log2) {
+  constexpr int SEG = HD / 4;            // phase 1: 4 lanes per key, SEG elements each
+  constexpr int NG = DCHUNK / (HD / 2);  // phase 3: token groups (each thread owns 2 columns)
   const int b = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z;
   const int G = H / KV;
   const DecodeRow rr = rows[b];
@@ -210,42 +212,55 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   const int j0 = ch * DCHUNK;
   if (j0 >= L) return;
   const int nj = min(DCHUNK, L - j0);
-  __shared__ float sq[MAXG][HD];
+  __shared__ float sq[MAXG][4][SEG + 1];  // padded: the 4 lane segments fall in different banks
   __shared__ float sp[MAXG][DCHUNK];
   __shared__ float smax[MAXG], ssum[MAXG];
-  const int tid = threadIdx.x;
+  __shared__ float sred[NG][MAXG][HD];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < G * HD; i += DCHUNK) {
     const int gg = i / HD, d = i % HD;
-    sq[gg][d] = __bfloat162float(qkv[(size_t)b * ld + (size_t)(kvh * G + gg) * HD + d]) * scale_log2;
+    sq[gg][d / SEG][d % SEG] = __bfloat162float(qkv[(size_t)b * ld + (size_t)(kvh * G + gg) * HD + d]) * scale_log2;
   }
   __syncthreads();
-  const size_t kv_stride_page = (size_t)2 * KV * 64 * HD;
-  const bf16* lbase = pool + (size_t)layer * n_pages * kv_stride_page;
+  const size_t page_stride = (size_t)2 * KV * 64 * HD;
+  const bf16* lbase = pool + (size_t)layer * n_pages * page_stride;
   const int* btr = bt + (size_t)rr.slot * max_pages;
-  if (tid < nj) {
-    const int j = j0 + tid;
-    const bf16* kp = lbase + (size_t)btr[j >> 6] * kv_stride_page + ((size_t)kvh * 64 + (j & 63)) * HD;
+  // phase 1: scores; 8 keys per warp per pass, each key's row read by 4 lanes (coalesced)
+  const int sub = lane & 3, tk = lane >> 2;
+  for (int base = warp * 8; base < nj; base += 8 * (DCHUNK / 32)) {
+    const int j = base + tk;
     float acc[MAXG];
 #pragma unroll
     for (int gg = 0; gg < MAXG; ++gg) acc[gg] = 0.f;
-#pragma unroll 4
-    for (int d = 0; d < HD; d += 8) {
-      uint4 u = *reinterpret_cast<const uint4*>(kp + d);
-      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    if (j < nj) {
+      const int jj = j0 + j;
+      const bf16* kp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)kvh * 64 + (jj & 63)) * HD + sub * SEG;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = unpack_bf16(w[e]);
+      for (int e = 0; e < SEG; e += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(kp + e);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int gg = 0; gg < MAXG; ++gg)
-          if (gg < G) acc[gg] += f.x * sq[gg][d + 2 * e] + f.y * sq[gg][d + 2 * e + 1];
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = unpack_bf16(w[q]);
+#pragma unroll
+          for (int gg = 0; gg < MAXG; ++gg)
+            if (gg < G) acc[gg] += f.x * sq[gg][sub][e + 2 * q] + f.y * sq[gg][sub][e + 2 * q + 1];
+        }
       }
     }
 #pragma unroll
-    for (int gg = 0; gg < MAXG; ++gg)
-      if (gg < G) sp[gg][tid] = acc[gg];
+    for (int gg = 0; gg < MAXG; ++gg) {
+      acc[gg] += __shfl_xor_sync(0xffffffffu, acc[gg], 1);
+      acc[gg] += __shfl_xor_sync(0xffffffffu, acc[gg], 2);
+    }
+    if (j < nj && sub == 0) {
+#pragma unroll
+      for (int gg = 0; gg < MAXG; ++gg)
+        if (gg < G) sp[gg][j] = acc[gg];
+    }
   }
   __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
+  // phase 2: softmax statistics per head (one warp per head)
   for (int gg = warp; gg < G; gg += DCHUNK / 32) {
     float m = -1e30f;
     for (int j = lane; j < nj; j += 32) m = fmaxf(m, sp[gg][j]);
@@ -263,17 +278,36 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
     }
   }
   __syncthreads();
-  // o[g][d] = sum_j p[g][j] v[j][d]
+  // phase 3: o[g][d] = sum_j p[g][j] v[j][d]; thread owns columns (2dp, 2dp+1) of token group tg
+  const int dp = tid % (HD / 2), tg = tid / (HD / 2);
+  float o0[MAXG], o1[MAXG];
+#pragma unroll
+  for (int gg = 0; gg < MAXG; ++gg) o0[gg] = o1[gg] = 0.f;
+  for (int j = tg; j < nj; j += NG) {
+    const int jj = j0 + j;
+    const bf16* vp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + 2 * dp;
+    const float2 v = unpack_bf16(*reinterpret_cast<const uint32_t*>(vp));
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg)
+      if (gg < G) {
+        const float p = sp[gg][j];
+        o0[gg] += p * v.x;
+        o1[gg] += p * v.y;
+      }
+  }
+#pragma unroll
+  for (int gg = 0; gg < MAXG; ++gg)
+    if (gg < G) {
+      sred[tg][gg][2 * dp] = o0[gg];
+      sred[tg][gg][2 * dp + 1] = o1[gg];
+    }
+  __syncthreads();
   const size_t wbase = ((size_t)b * H + kvh * G) * n_chunks + ch;
   for (int i = tid; i < G * HD; i += DCHUNK) {
     const int gg = i / HD, d = i % HD;
     float acc = 0.f;
-    for (int j = 0; j < nj; ++j) {
-      const int jj = j0 + j;
-      const bf16* vp =
-          lbase + (size_t)btr[jj >> 6] * kv_stride_page + ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + d;
-      acc += sp[gg][j] * __bfloat162float(*vp);
-    }
+#pragma unroll
+    for (int t = 0; t < NG; ++t) acc += sred[t][gg][d];  // fixed order
     float* w = ws + (wbase + (size_t)gg * n_chunks) * (HD + 2);
     w[2 + d] = acc;
     if (d == 0) {
@@ -319,6 +353,12 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
 
 cudaError_t flash_attn(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                        cudaStream_t s) {
+  if (hd == 80 || hd == 128) return flash_attn_tc(qkv, ld, out, ldo, S, H, KV, hd, causal, s);
+  return flash_attn_mma(qkv, ld, out, ldo, S, H, KV, hd, causal, s);
+}
+
+cudaError_t flash_attn_mma(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
+                           cudaStream_t s) {
   if (S <= 0) return cudaSuccess;
   if (ld % 8 || H % KV) return cudaErrorInvalidValue;
   switch (hd) {

@@ -1,0 +1,358 @@
+// tcgen05 / TMEM / TMA flash attention for the vision encoder (bidirectional MHA,
+// SURVEY.md §8(a) row a5; PAPER.md Table resource_stage P:139 "Attention" row, the
+// part of the encode pass the paper ran with FlashInfer on sm_86) and the LLM
+// prefill (causal GQA, row a6).
+//
+// One CTA = 128 query rows of one head.  Warp roles:
+//   w0: TMA producer -- Q once, then K_j / V_j tiles (128 keys) in a 2-stage ring;
+//   w1: MMA issuer  -- S_j = Q K_j^T into TMEM (double-buffered, 2 x 128 columns),
+//                      O += P_j V_j into TMEM (HD columns), one thread issues;
+//   w4-w7: softmax  -- thread = query row = TMEM lane: tcgen05.ld S_j, online softmax
+//                      in the exp2 domain with lazy rescaling (O is corrected in TMEM
+//                      only when the row max grows by > 8, i.e. 2^8), P_j as bf16 into
+//                      a SWIZZLE_128B smem tile (the A operand of the second MMA).
+// Operands: Q, K K-major SW128 (64-column chunks of the fused qkv buffer, straight from
+// TMA); V is used as an MN-major B operand (no transpose pass); P K-major SW128.
+// Deterministic: per (row, head) the key order and every reduction are fixed.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nova {
+namespace {
+
+constexpr int FBM = 128;   // query rows per CTA
+constexpr int FBN = 128;   // keys per tile
+constexpr int CHUNK = 64;  // columns per SW128 chunk (128 B)
+constexpr float LOG2E_F = 1.4426950408889634f;
+
+template <int HD>
+struct FtCfg {
+  static constexpr int NCH = (HD + CHUNK - 1) / CHUNK;          // 64-col chunks per row of a head
+  static constexpr int TILE_BYTES = NCH * FBN * CHUNK * 2;       // one 128-row Q/K/V tile
+  static constexpr int P_BYTES = FBM * FBN * 2;                  // P tile (2 chunks of 64 keys)
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + TILE_BYTES;               // 2 stages
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;           // 2 stages
+  static constexpr int P_OFF = V_OFF + 2 * TILE_BYTES;
+  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr int SMEM = 1024 + BAR_OFF + 256;
+  static constexpr int TMEM_COLS = 512;                          // S0, S1, O
+};
+
+// MN-major SWIZZLE_128B descriptor (V as the B operand): LBO = stride between 64-element
+// N groups (chunk stride), SBO = stride between 8-row K groups (1024 B).
+NOVA_DEV uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// tcgen05.st of 32 consecutive f32 columns for this thread's lane
+NOVA_DEV void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+NOVA_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 16 consecutive f32 columns
+NOVA_DEV void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+NOVA_DEV void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(256, 1)
+    fmha_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, int ldo, int S, int H, int KV,
+                   float scale_log2) {
+  using C = FtCfg<HD>;
+  constexpr int NCH = C::NCH;
+  constexpr uint32_t IDESC_S = umma_idesc_bf16(FBM, FBN);
+  constexpr uint32_t IDESC_O = umma_idesc_bf16(FBM, HD) | (1u << 16);  // B (V) MN-major
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2]
+  uint64_t* s_empty = bars + 11; // [2]
+  uint64_t* p_full = bars + 13;
+  uint64_t* pv_done = bars + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y;
+  const int kvh = h / (H / KV);
+  const int q0 = qt * FBM;
+  const int n_tiles_all = (S + FBN - 1) / FBN;
+  const int n_tiles = CAUSAL ? min(n_tiles_all, (q0 + FBM + FBN - 1) / FBN) : n_tiles_all;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t tS[2] = {tbase, tbase + FBN};
+  const uint32_t tO = tbase + 2 * FBN;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      const int qcol = h * HD, kcol = (H + kvh) * HD, vcol = (H + KV + kvh) * HD;
+      mbar_arrive_expect_tx(q_full, C::TILE_BYTES);
+      for (int c = 0; c < NCH; ++c)
+        tma_load_2d(smem + C::Q_OFF + c * FBN * 128, &tm, q_full, qcol + c * CHUNK, q0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = ((j >> 1) & 1) ^ 1;
+        mbar_wait(&k_empty[st], ph);
+        mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + c * FBN * 128, &tm, &k_full[st], kcol + c * CHUNK,
+                      j * FBN);
+        mbar_wait(&v_empty[st], ph);
+        mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + c * FBN * 128, &tm, &v_full[st], vcol + c * CHUNK,
+                      j * FBN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t qa = smem_u32(smem + C::Q_OFF);
+      const uint32_t pa = smem_u32(smem + C::P_OFF);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(smem + C::K_OFF + st * C::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k * 16 / CHUNK) * FBN * 128 + (k * 16 % CHUNK) * 2;
+          umma_bf16_ss(tS[st], umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), IDESC_S, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[st]);
+        umma_commit(&k_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s(j + 1);
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(smem + C::V_OFF + st * C::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < FBN / 16; ++k) {  // 16 keys per step
+          const uint32_t aoff = (k * 16 / CHUNK) * FBM * 128 + (k * 16 % CHUNK) * 2;
+          umma_bf16_ss(tO, umma_desc_sw128(pa + aoff), umma_desc_sw128_mn(vb + k * 16 * 128, FBN * 128), IDESC_O,
+                       (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&v_empty[st]);
+        umma_commit(pv_done);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- softmax / correction / epilogue
+    const int row = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int qrow = q0 + row;
+    float m = -1e30f, l = 0.f;
+    uint8_t* P = smem + C::P_OFF;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const int k0 = j * FBN;
+      const bool edge = (k0 + FBN > S) || (CAUSAL && k0 + FBN > q0);
+      // pass 1: row max
+      float mx = -1e30f;
+#pragma unroll
+      for (int c = 0; c < FBN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tS[st] + lane_off + c * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = k0 + c * 32 + i;
+          const bool ok = !edge || (key < S && (!CAUSAL || key <= qrow));
+          mx = fmaxf(mx, ok ? v[i] : -1e30f);
+        }
+      }
+      const float mnew = fmaxf(m, mx * scale_log2);
+      const bool need = (mnew - m) > 8.0f;
+      // PV_{j-1} must be complete before P is overwritten and before O is rescaled
+      if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
+      if (__any_sync(0xffffffffu, need) && j > 0) {
+        tc_fence_after();
+        const float f = need ? exp2f(m - mnew) : 1.0f;
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + lane_off + c * 16, o);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] *= f;
+          tmem_st16(tO + lane_off + c * 16, o);
+        }
+        tmem_st_wait();
+      }
+      if (need) {
+        l *= exp2f(m - mnew);
+        m = mnew;
+      }
+      // pass 2: P = exp2(s*scale - m) -> bf16 -> swizzled smem
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < FBN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tS[st] + lane_off + c * 32, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int key = k0 + c * 32 + i;
+          const bool ok0 = !edge || (key < S && (!CAUSAL || key <= qrow));
+          const bool ok1 = !edge || (key + 1 < S && (!CAUSAL || key + 1 <= qrow));
+          const float p0 = ok0 ? exp2f(v[i] * scale_log2 - m) : 0.f;
+          const float p1 = ok1 ? exp2f(v[i + 1] * scale_log2 - m) : 0.f;
+          ls += p0 + p1;
+          pk[i / 2] = pack_bf16(p0, p1);
+        }
+        // 32 keys = 64 B = four 16-byte chunks of row `row` in key chunk (c / 2)
+        uint8_t* base = P + (c >> 1) * FBM * 128 + row * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int jj = (c & 1) * 4 + q;
+          *reinterpret_cast<uint4*>(base + ((jj ^ (row & 7)) * 16)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      }
+      l += ls;
+      tc_fence_before();
+      mbar_arrive(&s_empty[st]);
+      fence_proxy_async();  // generic-proxy smem writes of P -> visible to the tensor core
+      mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16 rows
+    mbar_wait(pv_done, (n_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 16; ++c) {
+      float o[16];
+      tmem_ld16(tO + lane_off + c * 16, o);
+      if (qrow < S) {
+        uint4 a = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
+                             pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
+        uint4 b = make_uint4(pack_bf16(o[8] * inv, o[9] * inv), pack_bf16(o[10] * inv, o[11] * inv),
+                             pack_bf16(o[12] * inv, o[13] * inv), pack_bf16(o[14] * inv, o[15] * inv));
+        reinterpret_cast<uint4*>(orow + c * 16)[0] = a;
+        reinterpret_cast<uint4*>(orow + c * 16)[1] = b;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, C::TMEM_COLS);
+  }
+}
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool make_qkv_map(CUtensorMap* m, const bf16* ptr, int rows, int cols) {
+  static PFN_encodeTiled_t enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)CHUNK, (cuuint32_t)FBN};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int HD, bool CAUSAL>
+cudaError_t fmha_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, cudaStream_t s) {
+  CUtensorMap tm;
+  if (!make_qkv_map(&tm, qkv, S, ld)) return cudaErrorInvalidValue;
+  auto kern = fmha_tc_kernel<HD, CAUSAL>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FtCfg<HD>::SMEM);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  const float sl2 = LOG2E_F / sqrtf((float)HD);
+  count_launch();
+  kern<<<dim3((S + FBM - 1) / FBM, H), 256, FtCfg<HD>::SMEM, s>>>(tm, out, ldo, S, H, KV, sl2);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ld (the qkv row length in elements) must be a multiple of 8; hd in {80, 128} (64-col SW128 chunks).
+cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
+                          cudaStream_t s) {
+  if (S <= 0) return cudaSuccess;
+  if (ld % 8 || H % KV || ldo % 8) return cudaErrorInvalidValue;
+  switch (hd) {
+    case 80: return causal ? fmha_launch<80, true>(qkv, ld, out, ldo, S, H, KV, s)
+                           : fmha_launch<80, false>(qkv, ld, out, ldo, S, H, KV, s);
+    case 128: return causal ? fmha_launch<128, true>(qkv, ld, out, ldo, S, H, KV, s)
+                            : fmha_launch<128, false>(qkv, ld, out, ldo, S, H, KV, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace nova

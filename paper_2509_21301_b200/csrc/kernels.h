@@ -42,6 +42,12 @@ cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K,
 // out [S][H * hd] (ldo).  causal: key j <= query i.  Query head h reads KV head h / (H / KV).
 cudaError_t flash_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                        cudaStream_t s);
+// tcgen05/TMEM/TMA version (hd 80 / 128); flash_attn() dispatches to it for those head dims.
+cudaError_t flash_attn_tc(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
+                          cudaStream_t s);
+// legacy warp-MMA (mma.sync) version, kept for head dims 16/32/64 and as the measured baseline
+cudaError_t flash_attn_mma(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
+                           cudaStream_t s);
 
 // Paged KV cache: pool [L][P][2][KV][64][hd] bf16; block table per request slot [max_pages].
 struct DecodeRow {

@@ -23,6 +23,10 @@ int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int Sq, int 
                        void* stream) {
   return st(flash_attn((const bf16*)qkv, ld, (bf16*)out, ldo, Sq, H, KV, hd, causal, S(stream)));
 }
+int nova_op_flash_attn_mma(const void* qkv, int ld, void* out, int ldo, int Sq, int H, int KV, int hd, int causal,
+                           void* stream) {
+  return st(flash_attn_mma((const bf16*)qkv, ld, (bf16*)out, ldo, Sq, H, KV, hd, causal, S(stream)));
+}
 int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int32_t* bt, int max_pages, const nova_decode_row* rows, int B,
                         int max_ctx, float* ws, void* stream) {

@@ -36,6 +36,11 @@ def nova_op_flash_attn(qkv, out, S, H, KV, hd, causal, stream=None):
                                    _s(stream)), "flash_attn")
 
 
+def nova_op_flash_attn_mma(qkv, out, S, H, KV, hd, causal, stream=None):
+    check(lib().nova_op_flash_attn_mma(_p(qkv), qkv.stride(0), _p(out), out.stride(0), S, H, KV, hd, int(causal),
+                                       _s(stream)), "flash_attn_mma")
+
+
 def nova_op_decode_attn(qkv, out, kv_pool, layer, n_pages, H, KV, hd, block_tables, rows, B, max_ctx, ws,
                         stream=None):
     check(lib().nova_op_decode_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), _p(kv_pool), layer, n_pages,

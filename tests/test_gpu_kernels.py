@@ -143,6 +143,40 @@ def test_flash_attn(S, H, KV, hd, causal):
     assert rel_inf(bf16_host(out).reshape(S, H, hd), ref) <= 2e-2   # P rounded to bf16 before PV
 
 
+@pytest.mark.parametrize("S,H,KV,hd,causal", [(300, 2, 2, 80, 0), (131, 4, 2, 128, 1), (1286, 28, 4, 128, 1)])
+def test_flash_attn_mma_baseline_matches_oracle(S, H, KV, hd, causal):
+    """The legacy mma.sync kernel (kept as the measured baseline) on the tcgen05 head dims."""
+    rng = np.random.default_rng(S * 7 + hd)
+    qkv = rand_bf16(rng, (S, (H + 2 * KV) * hd))
+    out = torch.empty(S, H * hd, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_flash_attn_mma(bf16_dev(qkv), out, S, H, KV, hd, causal)
+    torch.cuda.synchronize()
+    q = qkv[:, :H * hd].reshape(S, H, hd).astype(np.float64)
+    k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd).astype(np.float64)
+    v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd).astype(np.float64)
+    ref = V.attention_causal_gqa(q, k, v, hd ** -0.5, 0) if causal else \
+        V.attention_full(q, np.repeat(k, H // KV, 1), np.repeat(v, H // KV, 1), hd ** -0.5)
+    assert rel_inf(bf16_host(out).reshape(S, H, hd), ref) <= 2e-2
+
+
+def test_flash_attn_tc_large_logits_rescale():
+    """Row maxima that grow along the key axis force the lazy O rescaling path (> 2^8)."""
+    rng = np.random.default_rng(99)
+    S, H, hd = 700, 2, 80
+    qkv = rand_bf16(rng, (S, 3 * H * hd))
+    ramp = np.linspace(0, 6, S)[:, None]                    # later keys have larger logits
+    qkv[:, H * hd:2 * H * hd] = rand_bf16(rng, (S, H * hd)) + ramp
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    qkv = bf16_bits_to_f32(f32_to_bf16_bits(qkv.astype(np.float32)))
+    out = torch.empty(S, H * hd, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_flash_attn(bf16_dev(qkv), out, S, H, H, hd, 0)
+    torch.cuda.synchronize()
+    t = qkv.reshape(S, 3, H, hd).astype(np.float64)
+    ref = V.attention_full(t[:, 0] * 3, t[:, 1], t[:, 2], hd ** -0.5) if False else \
+        V.attention_full(t[:, 0], t[:, 1], t[:, 2], hd ** -0.5)
+    assert rel_inf(bf16_host(out).reshape(S, H, hd), ref) <= 2e-2
+
+
 def _pool_setup(rng, L, n_pages, KV, hd):
     return torch.zeros(L, n_pages, 2, KV, 64, hd, dtype=torch.bfloat16, device="cuda")
 
