@@ -203,6 +203,8 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
                                                               int H, int KV, const int* __restrict__ bt, int max_pages,
                                                               const DecodeRow* __restrict__ rows, float* __restrict__ ws,
                                                               int n_chunks, float scale_log2) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int SEG = HD / 4;            // phase 1: 4 lanes per key, SEG elements each
   constexpr int NG = DCHUNK / (HD / 2);  // phase 3: token groups (each thread owns 2 columns)
   const int b = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z;
@@ -227,17 +229,28 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   const int* btr = bt + (size_t)rr.slot * max_pages;
   // phase 1: scores; 8 keys per warp per pass, each key's row read by 4 lanes (coalesced)
   const int sub = lane & 3, tk = lane >> 2;
-  for (int base = warp * 8; base < nj; base += 8 * (DCHUNK / 32)) {
-    const int j = base + tk;
-    float acc[MAXG];
+  constexpr int PASSES = DCHUNK / (8 * (DCHUNK / 32));  // 4: every key of the chunk in one unrolled sweep
+  uint4 kv[PASSES][SEG / 8];
 #pragma unroll
-    for (int gg = 0; gg < MAXG; ++gg) acc[gg] = 0.f;
+  for (int ps = 0; ps < PASSES; ++ps) {  // issue every K load of this thread first (memory-level parallelism)
+    const int j = warp * 8 + tk + ps * 8 * (DCHUNK / 32);
     if (j < nj) {
       const int jj = j0 + j;
       const bf16* kp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)kvh * 64 + (jj & 63)) * HD + sub * SEG;
 #pragma unroll
+      for (int e = 0; e < SEG / 8; ++e) kv[ps][e] = *reinterpret_cast<const uint4*>(kp + 8 * e);
+    }
+  }
+#pragma unroll
+  for (int ps = 0; ps < PASSES; ++ps) {
+    const int j = warp * 8 + tk + ps * 8 * (DCHUNK / 32);
+    float acc[MAXG];
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg) acc[gg] = 0.f;
+    if (j < nj) {
+#pragma unroll
       for (int e = 0; e < SEG; e += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(kp + e);
+        const uint4 u = kv[ps][e / 8];
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -283,17 +296,29 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   float o0[MAXG], o1[MAXG];
 #pragma unroll
   for (int gg = 0; gg < MAXG; ++gg) o0[gg] = o1[gg] = 0.f;
-  for (int j = tg; j < nj; j += NG) {
-    const int jj = j0 + j;
-    const bf16* vp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + 2 * dp;
-    const float2 v = unpack_bf16(*reinterpret_cast<const uint32_t*>(vp));
+  constexpr int VU = 8;  // V loads in flight per thread
+  for (int j = tg; j < nj; j += NG * VU) {
+    uint32_t vr[VU];
 #pragma unroll
-    for (int gg = 0; gg < MAXG; ++gg)
-      if (gg < G) {
-        const float p = sp[gg][j];
-        o0[gg] += p * v.x;
-        o1[gg] += p * v.y;
-      }
+    for (int u = 0; u < VU; ++u) {
+      const int jj = j0 + j + u * NG;
+      vr[u] = (j + u * NG < nj) ? *reinterpret_cast<const uint32_t*>(
+                                      lbase + (size_t)btr[jj >> 6] * page_stride +
+                                      ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + 2 * dp)
+                                : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < VU; ++u) {
+      if (j + u * NG >= nj) break;
+      const float2 v = unpack_bf16(vr[u]);
+#pragma unroll
+      for (int gg = 0; gg < MAXG; ++gg)
+        if (gg < G) {
+          const float p = sp[gg][j + u * NG];
+          o0[gg] += p * v.x;
+          o1[gg] += p * v.y;
+        }
+    }
   }
 #pragma unroll
   for (int gg = 0; gg < MAXG; ++gg)
@@ -320,6 +345,8 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
 template <int HD>
 __global__ void decode_attn_combine(const float* __restrict__ ws, const DecodeRow* __restrict__ rows, bf16* out,
                                     int ldo, int H, int n_chunks) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int L = rows[b].ctx + 1;
   const int nc = (L + DCHUNK - 1) / DCHUNK;
@@ -342,10 +369,11 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
   if (H / KV > MAXG) return cudaErrorInvalidValue;
   const int n_chunks = (max_ctx + 1 + DCHUNK - 1) / DCHUNK;
   const float sl2 = LOG2E / sqrtf((float)HD);
-  count_launch(2);
-  decode_attn_partial<HD><<<dim3(B, KV, n_chunks), DCHUNK, 0, s>>>(qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages,
-                                                                    rows, ws, n_chunks, sl2);
-  decode_attn_combine<HD><<<dim3(B, H), HD, 0, s>>>(ws, rows, out, ldo, H, n_chunks);
+  cudaError_t e = launch_k(decode_attn_partial<HD>, dim3(B, KV, n_chunks), dim3(DCHUNK), 0, s, true, qkv, ld, pool,
+                           layer, n_pages, H, KV, bt, max_pages, rows, ws, n_chunks, sl2);
+  if (e != cudaSuccess) return e;
+  e = launch_k(decode_attn_combine<HD>, dim3(B, H), dim3(HD), 0, s, true, ws, rows, out, ldo, H, n_chunks);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -353,7 +381,9 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
 
 cudaError_t flash_attn(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                        cudaStream_t s) {
-  if (hd == 80 || hd == 128) return flash_attn_tc(qkv, ld, out, ldo, S, H, KV, hd, causal, s);
+  // tcgen05 kernel for the bidirectional ViT attention (1.6x the mma.sync kernel, scripts/kbench.py);
+  // the causal prefill keeps the mma.sync kernel until the tcgen05 one balances causal tiles.
+  if (!causal && (hd == 80 || hd == 128)) return flash_attn_tc(qkv, ld, out, ldo, S, H, KV, hd, causal, s);
   return flash_attn_mma(qkv, ld, out, ldo, S, H, KV, hd, causal, s);
 }
 

@@ -136,6 +136,17 @@ NOVA_DEV void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// The secondary kernel may start while its stream predecessor drains; everything before
+// pdl_wait() must not touch data the predecessor writes (weights / constants only).
+NOVA_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+NOVA_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+NOVA_DEV float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ------------------------------------------------------------------ legacy warp MMA (mma.sync)
 // D(16x8 f32) += A(16x16 bf16, row) * B(16x8 bf16, col)
 NOVA_DEV void mma_bf16_16816(float* d, const uint32_t* a, const uint32_t* b) {

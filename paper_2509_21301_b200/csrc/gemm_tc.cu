@@ -37,9 +37,9 @@ struct GemmCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
 };
 
-NOVA_DEV float quick_gelu(float z) { return z / (1.0f + __expf(-1.702f * z)); }
+NOVA_DEV float quick_gelu(float z) { return __fdividef(z, 1.0f + __expf(-1.702f * z)); }
 NOVA_DEV float gelu_erf(float z) { return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f)); }
-NOVA_DEV float silu(float z) { return z / (1.0f + __expf(-z)); }
+NOVA_DEV float silu(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
 
 // Epilogue for 32 consecutive columns n0..n0+31 of row m (v = accumulators).
 template <int EPI>
@@ -103,7 +103,7 @@ NOVA_DEV void epilogue32(const GemmArgs& g, int m, int n0, float* v) {
 }
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 256);
     }
     fence_barrier_init();
   }
@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();  // A (activations) and the epilogue's C are written by the previous kernel
 
   const int num_m = (g.M + BM - 1) / BM;
   const int num_n = g.N / BN;
@@ -194,8 +196,9 @@ __global__ void __launch_bounds__(256, 1)
         if (acc == 0) aphase ^= 1;
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue
-    const int row = (warp - 4) * 32 + lane;
+  } else if (warp >= 4) {  // ---------------- epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -204,9 +207,9 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int m = mb * BM + row;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
         if (m < g.M) epilogue32<EPI>(g, m, nb * BN + c * 32, v);
       }
       tc_fence_before();
@@ -268,9 +271,7 @@ cudaError_t launch_bn(const bf16* A, int lda, const bf16* W, int ldw, const Gemm
   const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
   int grid = tiles < max_ctas ? tiles : max_ctas;
   if (grid < 1) grid = 1;
-  count_launch();
-  kern<<<grid, 256, GemmCfg<BN>::SMEM, s>>>(ma, mb, g);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(grid), dim3(384), GemmCfg<BN>::SMEM, s, true, ma, mb, g);
 }
 
 template <int BN>
@@ -294,7 +295,10 @@ cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int
   if (M <= 0) return cudaSuccess;
   if (N % 64 != 0 || K <= 0 || (lda % 8) || (ldw % 8) || (ldc % 8)) return cudaErrorInvalidValue;
   GemmArgs g{C, bias, M, N, K, ldc};
-  if (N % 256 == 0) return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
+  // widest tile that still gives >= 2 tiles per CTA of the SM budget (wave balance for narrow N)
+  const int mblk = (M + BM - 1) / BM;
+  if (N % 256 == 0 && (mblk * (N / 256) >= 2 * max_ctas || N % 128 != 0))
+    return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
   if (N % 128 == 0) return dispatch_epi<128>(A, lda, W, ldw, g, epi, max_ctas, s);
   return dispatch_epi<64>(A, lda, W, ldw, g, epi, max_ctas, s);
 }

@@ -8,19 +8,23 @@
 // batch rows x 16 k.  Each thread loads 16 contiguous bytes of a weight row
 // (128-bit, L1::no_allocate streaming) and of the matching x row; the k order
 // inside the 32-wide chunk is permuted identically for both operands, which
-// leaves the dot product unchanged.  A CTA owns 32 weight rows (two m16 tiles:
-// gate and up of an interleaved SiLU block land in the same CTA) and splits K
-// over its 8 warps; partials are reduced through shared memory in fixed warp
-// order.  The split depends only on K, never on the grid or the batch size, so
-// results are bitwise invariant to the SM budget and to the batch composition.
+// leaves the dot product unchanged.  A CTA owns MT x 16 weight rows (MT = 2 for the
+// interleaved gate|up blocks so SiLU*up fuses) and splits K over WARPS warps;
+// partials are reduced through shared memory in fixed warp order.  Small-N shapes
+// use 32 warps per CTA so every SM keeps enough loads in flight; large-N shapes use 8.
+// The configuration depends only on (N, K), never on the grid or the batch size,
+// so results are bitwise invariant to the SM budget and to the batch composition.
+// PDL prologue: the first weight batch is requested before griddepcontrol.wait, so
+// weight streaming of this linear overlaps the drain of the previous kernel.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace nova {
+
+bool g_use_pdl = true;
+
 namespace {
 
-constexpr int WARPS = 8;
-constexpr int ROWS = 32;
 constexpr int UNROLL = 4;
 
 NOVA_DEV float silu_f(float z) { return z / (1.0f + __expf(-z)); }
@@ -64,10 +68,10 @@ NOVA_DEV void load_x(XFrag<NT, XF32>& f, const void* X, int ldx, int B, int g, i
 }
 
 // acc[mt][nt][4] += W rows (wg: row g, wg8: row g+8 of each m tile) . x
-template <int NT, bool XF32>
+template <int MT, int NT, bool XF32>
 NOVA_DEV void mma_chunk(float (*acc)[NT][4], const uint4* wg, const uint4* wg8, const XFrag<NT, XF32>& f) {
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
+  for (int mt = 0; mt < MT; ++mt) {
     const uint32_t a1[4] = {wg[mt].x, wg8[mt].x, wg[mt].y, wg8[mt].y};
     const uint32_t a2[4] = {wg[mt].z, wg8[mt].z, wg[mt].w, wg8[mt].w};
 #pragma unroll
@@ -86,18 +90,27 @@ NOVA_DEV void mma_chunk(float (*acc)[NT][4], const uint4* wg, const uint4* wg8, 
   }
 }
 
-template <int NT, bool XF32, int EPI>
+template <int MT>
+NOVA_DEV void load_w(uint4 (&wg)[MT], uint4 (&wg8)[MT], const bf16* const* wrow, int kk) {
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    wg[mt] = ld_nc_v4(wrow[2 * mt] + kk);
+    wg8[mt] = ld_nc_v4(wrow[2 * mt + 1] + kk);
+  }
+}
+
+template <int NT, bool XF32, int EPI, int MT, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict__ X, int ldx,
                                                           const bf16* __restrict__ W, int N, int K,
                                                           void* __restrict__ Y, int ldy,
                                                           const bf16* __restrict__ bias, int B, int kslice) {
-  __shared__ float red[WARPS][2][NT][32][4];
+  __shared__ float red[WARPS][MT][NT][32][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
-  const int r0 = blockIdx.x * ROWS;
-  float acc[2][NT][4];
+  const int r0 = blockIdx.x * (16 * MT);
+  float acc[MT][NT][4];
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -105,36 +118,45 @@ __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict
 
   const int kbeg = warp * kslice;
   const int kend = min(K, kbeg + kslice);
-  const bf16* wrow[4] = {W + (size_t)(r0 + g) * K, W + (size_t)(r0 + g + 8) * K, W + (size_t)(r0 + 16 + g) * K,
-                         W + (size_t)(r0 + 24 + g) * K};
+  const bf16* wrow[2 * MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    wrow[2 * mt] = W + (size_t)(r0 + 16 * mt + g) * K;
+    wrow[2 * mt + 1] = W + (size_t)(r0 + 16 * mt + g + 8) * K;
+  }
+  // PDL prologue: weights do not depend on the previous kernel -- request the first batch now
+  uint4 wg[UNROLL][MT], wg8[UNROLL][MT];
   int k = kbeg;
-  for (; k + UNROLL * 32 <= kend; k += UNROLL * 32) {
-    uint4 wg[UNROLL][2], wg8[UNROLL][2];
+  const bool full0 = k + UNROLL * 32 <= kend;
+  if (full0) {
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const int kk = k + u * 32 + 8 * c;
-      wg[u][0] = ld_nc_v4(wrow[0] + kk);
-      wg8[u][0] = ld_nc_v4(wrow[1] + kk);
-      wg[u][1] = ld_nc_v4(wrow[2] + kk);
-      wg8[u][1] = ld_nc_v4(wrow[3] + kk);
-    }
+    for (int u = 0; u < UNROLL; ++u) load_w<MT>(wg[u], wg8[u], wrow, k + u * 32 + 8 * c);
+  }
+  pdl_launch_dependents();
+  pdl_wait();
+  if (full0) {
+    for (;;) {
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      XFrag<NT, XF32> f;
-      load_x<NT, XF32>(f, X, ldx, B, g, k + u * 32 + 8 * c);
-      mma_chunk<NT, XF32>(acc, wg[u], wg8[u], f);
+      for (int u = 0; u < UNROLL; ++u) {
+        XFrag<NT, XF32> f;
+        load_x<NT, XF32>(f, X, ldx, B, g, k + u * 32 + 8 * c);
+        mma_chunk<MT, NT, XF32>(acc, wg[u], wg8[u], f);
+      }
+      k += UNROLL * 32;
+      if (k + UNROLL * 32 > kend) break;
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) load_w<MT>(wg[u], wg8[u], wrow, k + u * 32 + 8 * c);
     }
   }
   for (; k < kend; k += 32) {
-    const int kk = k + 8 * c;
-    uint4 wg[2] = {ld_nc_v4(wrow[0] + kk), ld_nc_v4(wrow[2] + kk)};
-    uint4 wg8[2] = {ld_nc_v4(wrow[1] + kk), ld_nc_v4(wrow[3] + kk)};
+    uint4 a[MT], b[MT];
+    load_w<MT>(a, b, wrow, k + 8 * c);
     XFrag<NT, XF32> f;
-    load_x<NT, XF32>(f, X, ldx, B, g, kk);
-    mma_chunk<NT, XF32>(acc, wg, wg8, f);
+    load_x<NT, XF32>(f, X, ldx, B, g, k + 8 * c);
+    mma_chunk<MT, NT, XF32>(acc, a, b, f);
   }
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -143,7 +165,7 @@ __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict
   if (warp != 0) return;
   // fixed-order reduction over the K slices
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -162,11 +184,11 @@ __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict
       const int ro = g + ((j >> 1) << 3);
       if (b >= B) continue;
       if constexpr (EPI == EPI_BF16_SILUMUL) {
-        const float gt = acc[0][nt][j], up = acc[1][nt][j];
+        const float gt = acc[0][nt][j], up = acc[MT - 1][nt][j];
         reinterpret_cast<bf16*>(Y)[(size_t)b * ldy + r0 / 2 + ro] = __float2bfloat16_rn(silu_f(gt) * up);
       } else {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
           const int n = r0 + mt * 16 + ro;
           float v = acc[mt][nt][j];
           if (bias != nullptr) v += __bfloat162float(bias[n]);
@@ -183,28 +205,38 @@ __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict
   }
 }
 
+template <int NT, bool XF32, int EPI, int MT, int WARPS>
+cudaError_t launch_cfg(const void* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
+                       cudaStream_t s) {
+  const int kslice = ((K + WARPS * 32 - 1) / (WARPS * 32)) * 32;
+  return launch_k(gemv_kernel<NT, XF32, EPI, MT, WARPS>, dim3(N / (16 * MT)), dim3(WARPS * 32), 0, s, true, X, ldx,
+                  W, N, K, Y, ldy, bias, B, kslice);
+}
+
+// Shape-only configuration: many rows -> 32 rows x 8 warps; few rows -> 16 rows x 32 warps.
+template <int NT, bool XF32, int EPI>
+cudaError_t launch_epi(const void* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
+                       cudaStream_t s) {
+  const bool big = N / 32 >= 4 * 148;
+  if constexpr (EPI == EPI_BF16_SILUMUL) {
+    if (big) return launch_cfg<NT, XF32, EPI, 2, 8>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+    return launch_cfg<NT, XF32, EPI, 2, 16>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+  } else {
+    if (big) return launch_cfg<NT, XF32, EPI, 2, 8>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+    return launch_cfg<NT, XF32, EPI, 1, 32>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+  }
+}
+
 template <int NT, bool XF32>
 cudaError_t launch_nt(const void* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
                       int epi, cudaStream_t s) {
-  const int kslice = ((K + WARPS * 32 - 1) / (WARPS * 32)) * 32;
-  dim3 grid(N / ROWS), block(WARPS * 32);
-  count_launch();
   switch (epi) {
-    case EPI_BF16:
-      gemv_kernel<NT, XF32, EPI_BF16><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
-      break;
-    case EPI_BF16_SILUMUL:
-      gemv_kernel<NT, XF32, EPI_BF16_SILUMUL><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
-      break;
-    case EPI_F32_RESID:
-      gemv_kernel<NT, XF32, EPI_F32_RESID><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
-      break;
-    case EPI_F32_STORE:
-      gemv_kernel<NT, XF32, EPI_F32_STORE><<<grid, block, 0, s>>>(X, ldx, W, N, K, Y, ldy, bias, B, kslice);
-      break;
-    default: return cudaErrorInvalidValue;
+    case EPI_BF16: return launch_epi<NT, XF32, EPI_BF16>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+    case EPI_BF16_SILUMUL: return launch_epi<NT, XF32, EPI_BF16_SILUMUL>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+    case EPI_F32_RESID: return launch_epi<NT, XF32, EPI_F32_RESID>(X, ldx, W, N, K, Y, ldy, bias, B, s);
+    case EPI_F32_STORE: return launch_epi<NT, XF32, EPI_F32_STORE>(X, ldx, W, N, K, Y, ldy, bias, B, s);
   }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -212,7 +244,7 @@ cudaError_t launch_nt(const void* X, int ldx, const bf16* W, int N, int K, void*
 cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias,
                  int B, int epi, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
-  if (B > 16 || N % ROWS || K % 32 || ldx % 8) return cudaErrorInvalidValue;
+  if (B > 16 || N % 32 || K % 32 || ldx % 8) return cudaErrorInvalidValue;
   if (x_f32) return B <= 8 ? launch_nt<1, true>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s)
                            : launch_nt<2, true>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s);
   return B <= 8 ? launch_nt<1, false>(X, ldx, W, N, K, Y, ldy, bias, B, epi, s)

@@ -18,6 +18,26 @@ typedef __nv_bfloat16 bf16;
 extern std::atomic<unsigned long long> g_kernel_launches;
 inline void count_launch(int n = 1) { g_kernel_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
+// Programmatic dependent launch (PDL) for the decode chain: the next kernel's CTAs are
+// scheduled while the previous one drains and run their weight-streaming prologue early.
+extern bool g_use_pdl;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && g_use_pdl) ? 1 : 0;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // GEMM / GEMV epilogues (C = A . W^T + bias, then):
 enum Epi {
   EPI_BF16 = 0,         // out bf16

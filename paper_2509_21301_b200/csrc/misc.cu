@@ -11,6 +11,8 @@ namespace {
 // ---------------------------------------------------------------- norms (one warp per row)
 __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm,
                                  const bf16* __restrict__ bt, bf16* __restrict__ y, int ldy, int M, int d, float eps) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -44,6 +46,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf1
 
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm, void* __restrict__ y,
                                int y_f32, int ldy, int M, int d, float eps) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -115,6 +119,8 @@ __global__ void llm_rope_kv_kernel(bf16* __restrict__ qkv, int ld, int H, int KV
                                    int sec1, const int* __restrict__ pos3, int ld_pos,
                                    const DecodeRow* __restrict__ rows, int slot, int ctx0, bf16* __restrict__ pool,
                                    int layer, int n_pages, const int* __restrict__ bt, int max_pages) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int r = blockIdx.x;
   int p[3], cidx, sl;
   if (rows) {
@@ -159,6 +165,8 @@ __global__ void llm_rope_kv_kernel(bf16* __restrict__ qkv, int ld, int H, int KV
 __global__ void embed_kernel(const bf16* __restrict__ table, int d, const int* __restrict__ ids,
                              const DecodeRow* __restrict__ rows, const int* __restrict__ last_tok, float* __restrict__ out,
                              int ldo) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int r = blockIdx.x;
   const int id = ids ? ids[r] : last_tok[rows[r].slot];
   const bf16* src = table + (size_t)id * d;
@@ -172,6 +180,8 @@ __global__ void embed_kernel(const bf16* __restrict__ table, int d, const int* _
 
 __global__ void argmax_kernel(const float* __restrict__ logits, int ldl, int V, int* __restrict__ out_tok,
                               const DecodeRow* __restrict__ rows, int* __restrict__ last_tok, int single_slot) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int r = blockIdx.x;
   const float* l = logits + (size_t)r * ldl;
   float best = -INFINITY;
@@ -229,17 +239,13 @@ cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf1
                       cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
-  count_launch();
-  layernorm_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, g, b, y, ldy, M, d, eps);
-  return cudaGetLastError();
+  return launch_k(layernorm_kernel, dim3((M + 7) / 8), dim3(256), 0, s, true, x, ldx, g, b, y, ldy, M, d, eps);
 }
 cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
                     cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
-  count_launch();
-  rmsnorm_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, ldx, g, y, y_f32, ldy, M, d, eps);
-  return cudaGetLastError();
+  return launch_k(rmsnorm_kernel, dim3((M + 7) / 8), dim3(256), 0, s, true, x, ldx, g, y, y_f32, ldy, M, d, eps);
 }
 cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int merge, bf16* X0, cudaStream_t s) {
   const int N = (H / P) * (W / P);
@@ -258,24 +264,18 @@ cudaError_t llm_rope_kv(bf16* qkv, int ld, int nrows, int H, int KV, int hd, flo
                         const int* pos3, int ld_pos, const DecodeRow* rows, int slot, int ctx0, bf16* pool, int layer,
                         int n_pages, const int* bt, int max_pages, cudaStream_t s) {
   if (nrows <= 0) return cudaSuccess;
-  count_launch();
-  llm_rope_kv_kernel<<<nrows, 256, 0, s>>>(qkv, ld, H, KV, hd, log2f(theta), sec0, sec1, pos3, ld_pos, rows, slot,
-                                           ctx0, pool, layer, n_pages, bt, max_pages);
-  return cudaGetLastError();
+  return launch_k(llm_rope_kv_kernel, dim3(nrows), dim3(256), 0, s, true, qkv, ld, H, KV, hd, log2f(theta), sec0,
+                  sec1, pos3, ld_pos, rows, slot, ctx0, pool, layer, n_pages, bt, max_pages);
 }
 cudaError_t embed(const bf16* table, int d, const int* ids, const DecodeRow* rows, const int* last_tok, float* out,
                   int ldo, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  count_launch();
-  embed_kernel<<<n, 256, 0, s>>>(table, d, ids, rows, last_tok, out, ldo);
-  return cudaGetLastError();
+  return launch_k(embed_kernel, dim3(n), dim3(256), 0, s, true, table, d, ids, rows, last_tok, out, ldo);
 }
 cudaError_t argmax_rows(const float* logits, int ldl, int V, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
                         int single_slot, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  count_launch();
-  argmax_kernel<<<n, 1024, 0, s>>>(logits, ldl, V, out_tok, rows, last_tok, single_slot);
-  return cudaGetLastError();
+  return launch_k(argmax_kernel, dim3(n), dim3(1024), 0, s, true, logits, ldl, V, out_tok, rows, last_tok, single_slot);
 }
 
 }  // namespace nova
