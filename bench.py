@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--requests", type=int, default=48, help="requests per step (per GPU)")
     p.add_argument("--no-compare", action="store_true", help="skip the serial / static-50/50 comparison replays")
     p.add_argument("--quick", action="store_true", help="smaller profile sweep (debug)")
+    p.add_argument("--dispatch", default="jsq", choices=["jsq", "rr"], help="replica dispatcher policy (N > 1)")
     p.add_argument("--out", default=None, help="also write the JSON line here")
     return p.parse_args()
 
@@ -171,18 +172,22 @@ def make_inputs(shape, rows, seed, device, resident):
     return out
 
 
-def replay(eng, inputs):
+def replay(eng, inputs, t0=None, rank=0, world=1, board=None, policy="jsq"):
     """Submit at the trace's arrival times (real time), step the scheduler until every request
-    finished.  Returns per-request latencies, the step wall time and host<->device bytes."""
-    from paper_2509_21301_b200 import engine as E
+    finished.  With world > 1 the trace is global: rank 0's dispatcher assigns each arrival to a
+    replica (JSQ on the published front backlog) and each rank submits only its own requests.
+    Returns per-request latencies, the step wall time and host<->device bytes."""
     import ctypes as C
     from paper_2509_21301_b200 import _abi as A
+    from paper_2509_21301_b200.dispatch import Dispatcher, wait_assignment
     n = len(inputs)
-    ids = [None] * n
-    t0 = time.monotonic_ns() + 2_000_000   # first arrival 2 ms from now
+    ids = {}
+    if t0 is None:
+        t0 = time.monotonic_ns() + 2_000_000   # first arrival 2 ms from now
     base_finished = eng.step(0).finished
     h2d = 0
     sub_err = []
+    state = {"submitted": 0, "done": False}
 
     def submitter():
         nonlocal h2d
@@ -194,6 +199,8 @@ def replay(eng, inputs):
                     if dt <= 0:
                         break
                     time.sleep(min(dt / 1e9, 0.002))
+                if world > 1 and wait_assignment(board, i) != rank:
+                    continue
                 r = A.Request()
                 r.pixels_bf16 = pix.data_ptr()
                 r.height, r.width = int(pix.shape[1]), int(pix.shape[2])
@@ -209,24 +216,42 @@ def replay(eng, inputs):
                     time.sleep(0.0005)
                 if rc != 0:
                     raise RuntimeError(f"submit failed {rc}")
-                ids[i] = rid.value
+                ids[rid.value] = i
+                state["submitted"] += 1
                 if not pix.is_cuda:
                     h2d += pix.numel() * 2
                 h2d += len(prm) * 4
         except Exception as ex:  # pragma: no cover
             sub_err.append(ex)
+        state["done"] = True
 
-    th = threading.Thread(target=submitter)
-    th.start()
+    def dispatcher():
+        d = Dispatcher(board, [x[3] for x in inputs], policy)
+        while not d.done():
+            d.assign_due((time.monotonic_ns() - t0) / 1e9)
+            time.sleep(0.0001)
+
+    threads = [threading.Thread(target=submitter)]
+    if world > 1 and rank == 0:
+        threads.append(threading.Thread(target=dispatcher))
+    for th in threads:
+        th.start()
+    toks, first = [], 0
     while True:
         info = eng.step(500)
         if sub_err:
             raise sub_err[0]
-        if info.finished - base_finished >= n and not th.is_alive():
+        new = eng.poll_tokens(1 << 16)
+        toks += new
+        first += sum(1 for t in new if t[1] == 0)
+        if board is not None:
+            board.publish(rank, state["submitted"] - first, state["submitted"])
+        if state["done"] and info.finished - base_finished >= state["submitted"]:
             break
-    th.join()
+    for th in threads:
+        th.join()
     t1 = time.monotonic_ns()
-    toks = eng.poll_tokens(1 << 20)
+    toks += eng.poll_tokens(1 << 20)
     lat, ttft = [], []
     for rid in ids:
         st = eng.stats(rid)
@@ -234,8 +259,8 @@ def replay(eng, inputs):
         ttft.append((st["first_tok"] - st["arrival"]) / 1e6)
     d2h = 4 * len(toks)
     first_arrival = t0 + int(inputs[0][3] * 1e9)
-    return {"lat_ms": lat, "ttft_ms": ttft, "wall_s": (t1 - first_arrival) / 1e9, "h2d": h2d, "d2h": d2h,
-            "tokens": len(toks)}
+    return {"lat_ms": lat or [0.0], "ttft_ms": ttft or [0.0], "wall_s": (t1 - first_arrival) / 1e9, "h2d": h2d,
+            "d2h": d2h, "tokens": len(toks), "n": len(ids)}
 
 
 def pct(xs, q):
@@ -356,14 +381,36 @@ def main():
     eng.set_partition(**policy)
     # T_front: request-mix mean of solo t_v + t_p (half 4888-patch, half 7920-patch screenshots)
     t_front = (0.5 * (curves["t_v_solo_ms"] + curves["t_v_solo_7920_ms"]) + curves["t_p_solo_ms"]) / 1000.0
-    traces = [make_trace(shape, args.requests, args.rho, t_front, 31 + 97 * rank + i)
+    # global trace (identical on every rank): world x requests at world x the per-GPU load (weak scaling)
+    traces = [make_trace(shape, args.requests * world, args.rho * world, t_front, 31 + i)
               for i in range(args.warmup + 2 * args.steps + 2)]
+    counter = [0]
+
+    def run_step(tr, seed, resident):
+        inputs = make_inputs(shape, tr, seed, local, resident)
+        if world == 1:
+            return replay(eng, inputs)
+        from paper_2509_21301_b200.dispatch import ReplicaBoard
+        counter[0] += 1
+        name = f"nova_{os.environ.get('MASTER_PORT', '0')}_{counter[0]}"
+        board = ReplicaBoard(name, world, len(inputs), create=True) if rank == 0 else None
+        dist.barrier()
+        if rank != 0:
+            board = ReplicaBoard(name, world, len(inputs), create=False)
+        t0 = torch.tensor([time.monotonic_ns() + 200_000_000], dtype=torch.int64, device="cuda")
+        dist.broadcast(t0, 0)
+        r = replay(eng, inputs, int(t0.item()), rank, world, board, args.dispatch)
+        dist.barrier()
+        board.close()
+        return r
+
     # warm-up steps (untimed)
     for i in range(args.warmup):
-        replay(eng, make_inputs(shape, traces[i], 100 + i, local, True))
+        run_step(traces[i], 100 + i, True)
     eng.kernel_stats_reset()
     eng.kernel_timing(4)
     launches0 = eng.lib.nova_launch_count()
+    log(f"[bench] libnova launches before the timed region: {launches0}")
     clocks = ClockSampler(local)
     clocks.start()
     torch.cuda.synchronize()
@@ -373,7 +420,7 @@ def main():
     ev0.record()
     res = []
     for i in range(args.steps):       # inputs resident in HBM
-        res.append(replay(eng, make_inputs(shape, traces[args.warmup + i], 200 + i, local, True)))
+        res.append(run_step(traces[args.warmup + i], 200 + i, True))
     torch.cuda.synchronize()
     ev1.record()
     torch.cuda.synchronize()
@@ -383,7 +430,7 @@ def main():
     # end-to-end: pinned host screenshots, H2D inside the timed region
     res_e2e = []
     for i in range(args.steps):
-        res_e2e.append(replay(eng, make_inputs(shape, traces[args.warmup + args.steps + i], 300 + i, local, False)))
+        res_e2e.append(run_step(traces[args.warmup + args.steps + i], 300 + i, False))
     clk = clocks.stop()
     dev_ms = ev0.elapsed_time(ev1)
 
@@ -391,7 +438,8 @@ def main():
         lat = [x for r in rs for x in r["lat_ms"]]
         wall = sum(r["wall_s"] for r in rs)
         return {"max_ms": max(lat), "p99_ms": pct(lat, 0.99), "mean_ms": statistics.mean(lat),
-                "ttft_p99_ms": pct([x for r in rs for x in r["ttft_ms"]], 0.99), "n": len(lat), "wall_s": wall,
+                "ttft_p99_ms": pct([x for r in rs for x in r["ttft_ms"]], 0.99), "n": sum(r["n"] for r in rs),
+                "wall_s": wall,
                 "h2d": sum(r["h2d"] for r in rs) / len(rs), "d2h": sum(r["d2h"] for r in rs) / len(rs)}
 
     A, Ae = agg(res), agg(res_e2e)
@@ -403,21 +451,25 @@ def main():
                           ("static_50_50", dict(mode=E.STATIC, sm_decode_dv=72, sm_decode_dp=72, b_max=16)),
                           ("serial", dict(mode=E.SERIAL, b_max=16))]:
             eng.set_partition(**pol)
-            r = agg([replay(eng, make_inputs(shape, tr, 400, local, True))])
+            r = agg([run_step(tr, 400, True)])
             compare[name] = {k: round(v, 2) if isinstance(v, float) else v for k, v in r.items()
                              if k in ("max_ms", "p99_ms", "mean_ms", "n", "wall_s")}
             compare[name]["req_per_s"] = round(r["n"] / r["wall_s"], 3)
         eng.set_partition(**policy)
 
-    # max over ranks (weak scaling replicas)
-    loc = torch.tensor([A["max_ms"], A["p99_ms"], A["wall_s"], Ae["max_ms"], Ae["p99_ms"], Ae["wall_s"], dev_ms],
-                       dtype=torch.float64, device="cuda")
-    nreq = torch.tensor([A["n"], Ae["n"]], dtype=torch.float64, device="cuda")
+    # replicas: latencies of every rank pooled (exact global max / p99), wall time = max over ranks
+    loc = torch.tensor([A["wall_s"], Ae["wall_s"], dev_ms], dtype=torch.float64, device="cuda")
+    lat_all = [x for r in res for x in r["lat_ms"]]
+    lat_all_e = [x for r in res_e2e for x in r["lat_ms"]]
     if dist:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
-        dist.all_reduce(nreq, op=dist.ReduceOp.SUM)
-    mx, p99, wall, mx_e, p99_e, wall_e, dev_ms = loc.tolist()
-    n_all, n_all_e = nreq.tolist()
+        g = [None] * world
+        dist.all_gather_object(g, (lat_all, lat_all_e))
+        lat_all = [x for a, _ in g for x in a]
+        lat_all_e = [x for _, b in g for x in b]
+    wall, wall_e, dev_ms = loc.tolist()
+    mx, p99, n_all = max(lat_all), pct(lat_all, 0.99), len(lat_all)
+    mx_e, p99_e, n_all_e = max(lat_all_e), pct(lat_all_e, 0.99), len(lat_all_e)
 
     # roofline of the dominant kernel (largest summed device time among kernel classes)
     hbm = pk["hbm_gbs"]
@@ -464,7 +516,7 @@ def main():
                        "t_front_ms": round(t_front * 1000, 2), "images": "50% 52x94 (4888 patches) / 50% 66x120 "
                        "(7920 patches)", "prompt": "U{32..128}", "gen_len": "U{32..64}",
                        "policy": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in policy.items()},
-                       "l2": "weights 16.5 GB >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world}"},
+                       "l2": "weights 16.5 GB >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world} ({args.dispatch} dispatcher)"},
             "e2e": {"value": round(mx_e, 2), "unit": "ms", "p99_ms": round(p99_e, 2),
                     "req_per_s": round(n_all_e / wall_e, 3), "h2d_bytes_per_step": int(Ae["h2d"]),
                     "d2h_bytes_per_step": int(Ae["d2h"])},

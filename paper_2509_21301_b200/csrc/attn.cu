@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   pdl_launch_dependents();
   pdl_wait();
   constexpr int SEG = HD / 4;            // phase 1: 4 lanes per key, SEG elements each
-  constexpr int NG = DCHUNK / (HD / 2);  // phase 3: token groups (each thread owns 2 columns)
   const int b = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z;
   const int G = H / KV;
   const DecodeRow rr = rows[b];
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   __shared__ float sq[MAXG][4][SEG + 1];  // padded: the 4 lane segments fall in different banks
   __shared__ float sp[MAXG][DCHUNK];
   __shared__ float smax[MAXG], ssum[MAXG];
-  __shared__ float sred[NG][MAXG][HD];
+  __shared__ float sred[DCHUNK / 32][MAXG][HD];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < G * HD; i += DCHUNK) {
     const int gg = i / HD, d = i % HD;
@@ -291,48 +290,70 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
     }
   }
   __syncthreads();
-  // phase 3: o[g][d] = sum_j p[g][j] v[j][d]; thread owns columns (2dp, 2dp+1) of token group tg
-  const int dp = tid % (HD / 2), tg = tid / (HD / 2);
-  float o0[MAXG], o1[MAXG];
+  // phase 3: o[g][d] = sum_j p[g][j] v[j][d].  Thread owns 8 columns (one 16-byte load per key)
+  // of token group tg; all V loads of the chunk are issued before any FMA.
+  constexpr int CG = HD / 8;           // column groups per row
+  constexpr int TG = DCHUNK / CG;      // token groups
+  constexpr int TPT = DCHUNK / TG;     // keys per thread (= CG)
+  const int cg = tid % CG, tg = tid / CG;
+  uint4 vr[TPT];
 #pragma unroll
-  for (int gg = 0; gg < MAXG; ++gg) o0[gg] = o1[gg] = 0.f;
-  constexpr int VU = 8;  // V loads in flight per thread
-  for (int j = tg; j < nj; j += NG * VU) {
-    uint32_t vr[VU];
-#pragma unroll
-    for (int u = 0; u < VU; ++u) {
-      const int jj = j0 + j + u * NG;
-      vr[u] = (j + u * NG < nj) ? *reinterpret_cast<const uint32_t*>(
-                                      lbase + (size_t)btr[jj >> 6] * page_stride +
-                                      ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + 2 * dp)
-                                : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < VU; ++u) {
-      if (j + u * NG >= nj) break;
-      const float2 v = unpack_bf16(vr[u]);
-#pragma unroll
-      for (int gg = 0; gg < MAXG; ++gg)
-        if (gg < G) {
-          const float p = sp[gg][j + u * NG];
-          o0[gg] += p * v.x;
-          o1[gg] += p * v.y;
-        }
+  for (int u = 0; u < TPT; ++u) {
+    const int j = tg + u * TG;
+    if (j < nj) {
+      const int jj = j0 + j;
+      vr[u] = *reinterpret_cast<const uint4*>(lbase + (size_t)btr[jj >> 6] * page_stride +
+                                              ((size_t)(KV + kvh) * 64 + (jj & 63)) * HD + 8 * cg);
+    } else {
+      vr[u] = make_uint4(0, 0, 0, 0);
     }
   }
+  float o[MAXG][8];
 #pragma unroll
   for (int gg = 0; gg < MAXG; ++gg)
-    if (gg < G) {
-      sred[tg][gg][2 * dp] = o0[gg];
-      sred[tg][gg][2 * dp + 1] = o1[gg];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[gg][e] = 0.f;
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int j = tg + u * TG;
+    if (j >= nj) break;
+    const uint32_t w4[4] = {vr[u].x, vr[u].y, vr[u].z, vr[u].w};
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = unpack_bf16(w4[q]);
+      v[2 * q] = f.x;
+      v[2 * q + 1] = f.y;
     }
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg)
+      if (gg < G) {
+        const float p = sp[gg][j];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[gg][e] += p * v[e];
+      }
+  }
+  // token groups inside a warp share cg when lane % CG matches: butterfly over those lanes (fixed order)
+#pragma unroll
+  for (int off = CG; off < 32; off <<= 1)
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[gg][e] += __shfl_xor_sync(0xffffffffu, o[gg][e], off);
+  if (lane < CG) {
+#pragma unroll
+    for (int gg = 0; gg < MAXG; ++gg)
+      if (gg < G)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sred[warp][gg][8 * cg + e] = o[gg][e];
+  }
   __syncthreads();
   const size_t wbase = ((size_t)b * H + kvh * G) * n_chunks + ch;
   for (int i = tid; i < G * HD; i += DCHUNK) {
     const int gg = i / HD, d = i % HD;
     float acc = 0.f;
 #pragma unroll
-    for (int t = 0; t < NG; ++t) acc += sred[t][gg][d];  // fixed order
+    for (int t = 0; t < DCHUNK / 32; ++t) acc += sred[t][gg][d];  // fixed order over warps
     float* w = ws + (wbase + (size_t)gg * n_chunks) * (HD + 2);
     w[2 + d] = acc;
     if (d == 0) {

@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_kernels.py -x -q 2>&1 | tail -3
+timeout 100 python scripts/kbench.py --only dattn
+timeout 600 python bench.py --quick --requests 6 --steps 1 --warmup 1 --no-compare --out gpurun_out/bench_small.json 2>gpurun_out/bench_small.err; grep "launches before" gpurun_out/bench_small.err
+N0=$(grep "launches before" gpurun_out/bench_small.err | grep -o "[0-9]*$")
+echo "skip $N0"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s $N0 -c 6000 --csv --log-file gpurun_out/launches.csv python bench.py --quick --requests 6 --steps 1 --warmup 1 --no-compare > gpurun_out/bench_ncu.log 2>&1
+tail -2 gpurun_out/bench_ncu.log; wc -l gpurun_out/launches.csv
