@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--requests", type=int, default=48, help="requests per step (per GPU)")
     p.add_argument("--no-compare", action="store_true", help="skip the serial / static-50/50 comparison replays")
     p.add_argument("--quick", action="store_true", help="smaller profile sweep (debug)")
+    p.add_argument("--skip-profile", action="store_true", help="no co-run curve sweep (ncu launch-list runs)")
     p.add_argument("--dispatch", default="jsq", choices=["jsq", "rr"], help="replica dispatcher policy (N > 1)")
     p.add_argument("--out", default=None, help="also write the JSON line here")
     return p.parse_args()
@@ -252,15 +253,18 @@ def replay(eng, inputs, t0=None, rank=0, world=1, board=None, policy="jsq"):
         th.join()
     t1 = time.monotonic_ns()
     toks += eng.poll_tokens(1 << 20)
-    lat, ttft = [], []
+    lat, ttft, qwait, front = [], [], [], []
     for rid in ids:
         st = eng.stats(rid)
         lat.append((st["last_tok"] - st["arrival"]) / 1e6)
         ttft.append((st["first_tok"] - st["arrival"]) / 1e6)
+        qwait.append(max(0, st["vis_start"] - st["arrival"]) / 1e9)
+        front.append((st["pre_end"] - st["vis_start"]) / 1e9)
     d2h = 4 * len(toks)
     first_arrival = t0 + int(inputs[0][3] * 1e9)
     return {"lat_ms": lat or [0.0], "ttft_ms": ttft or [0.0], "wall_s": (t1 - first_arrival) / 1e9, "h2d": h2d,
-            "d2h": d2h, "tokens": len(toks), "n": len(ids)}
+            "d2h": d2h, "tokens": len(toks), "n": len(ids), "qwait_s": qwait, "front_s": front,
+            "span_s": (inputs[-1][3] - inputs[0][3])}
 
 
 def pct(xs, q):
@@ -374,7 +378,13 @@ def main():
     t_setup = time.time()
     eng = build_engine(shape, local)
     log(f"[bench] engine ready in {time.time() - t_setup:.1f}s; memory {eng.memory}")
-    curves, plan = profile_and_plan(eng, args.quick, log)
+    if args.skip_profile:   # ncu launch-list runs: no co-run sweep, fixed plan, solo curve points only
+        tv = eng.time_pass(0, 0, 52, 94, iters=1)[0]
+        curves = {"t_v_solo_ms": tv, "t_v_solo_7920_ms": 1.6 * tv, "t_p_solo_ms": eng.time_pass(1, 0, 52, 94, 64,
+                                                                                               iters=1)[0]}
+        plan = {"best": (88, 88, 0.0, 0.0), "sm_min": 32, "alpha_dv": 18.667, "alpha_dp": 18.667}
+    else:
+        curves, plan = profile_and_plan(eng, args.quick, log)
     sv, sp = plan["best"][0], plan["best"][1]
     policy = dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=plan["sm_min"], alpha_dv=plan["alpha_dv"],
                   alpha_dp=plan["alpha_dp"], b_max=16)
@@ -443,6 +453,16 @@ def main():
                 "h2d": sum(r["h2d"] for r in rs) / len(rs), "d2h": sum(r["d2h"] for r in rs) / len(rs)}
 
     A, Ae = agg(res), agg(res_e2e)
+    # Eq. 6: M/G/1 prediction of the vision-queue wait from the measured front service
+    qw = [x for r in res for x in r["qwait_s"]]
+    fs = [x for r in res for x in r["front_s"]]
+    lam = sum(r["n"] for r in res) / max(1e-9, sum(r["span_s"] for r in res))
+    ET, ET2 = statistics.mean(fs), statistics.mean([x * x for x in fs])
+    rho_m = lam * ET
+    mg1 = {"lambda_rps": round(lam, 3), "E_T_ms": round(ET * 1e3, 2), "E_T2_ms2": round(ET2 * 1e6, 1),
+           "utilization": round(rho_m, 3), "measured_wait_ms": round(statistics.mean(qw) * 1e3, 2),
+           "predicted_wait_ms": round(lam * ET2 / (2 * (1 - rho_m)) * 1e3, 2) if rho_m < 1 else None,
+           "note": "bursty MMPP arrivals, so M/G/1 (Poisson) is expected to under-predict"}
     # comparison modes on the same trace (serial stage execution, static 50/50 split)
     compare = {}
     if not args.no_compare:
@@ -526,7 +546,7 @@ def main():
             "plan": {"best": plan["best"][:2], "e2e_ms": round(plan["best"][2], 2), "thr_rps": round(plan["best"][3], 2),
                      "sm_min": plan["sm_min"], "alpha_dv": round(plan["alpha_dv"], 3),
                      "alpha_dp": round(plan["alpha_dp"], 3)},
-            "compare": compare, "clocks": clk}
+            "compare": compare, "mg1": mg1, "clocks": clk}
     if rank == 0 and world == 1:
         try:
             v, med, cores = cpu_oracle_sample(shape)

@@ -47,6 +47,12 @@ int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ld
 int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias,
                  int B, int epi, void* stream);
 
+/* TMA-streamed decode linear (bf16 X only): same contract as nova_op_gemv (N % 64 == 0,
+ * K % 64 == 0).  ws: f32 workspace of 16*B*N floats for split-K partials; tickets: int32
+ * [N/64] zero-initialised once (the kernel leaves them zero).  Deterministic. */
+int nova_op_gemv_tma(const void* X, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias, int B,
+                     int epi, float* ws, int32_t* tickets, void* stream);
+
 /* Flash attention (a5 ViT: causal = 0, KV = H; a6 prefill: causal = 1, GQA).
  * qkv [S][(H + 2 KV) hd] bf16 (ld): q heads, then k heads, then v heads; out
  * [S][H hd] bf16 (ldo); scale hd^-1/2; hd in {16, 32, 64, 80, 128}. */

@@ -21,6 +21,7 @@ U64 = C.c_uint64
 OPS_SIGNATURES = {
     "nova_op_gemm": [P, I, P, I, P, I, P, I, I, I, I, I, P],
     "nova_op_gemv": [P, I, I, P, I, I, P, I, P, I, I, P],
+    "nova_op_gemv_tma": [P, I, P, I, I, P, I, P, I, I, P, P, P],
     "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, P],
     "nova_op_flash_attn_mma": [P, I, P, I, I, I, I, I, I, P],
     "nova_op_decode_attn": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P],

@@ -206,17 +206,20 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int k0 = j * FBN;
       const bool edge = (k0 + FBN > S) || (CAUSAL && k0 + FBN > q0);
+      // keys >= lim are masked (tail of the sequence; causal diagonal); interior tiles skip the test
+      const int lim = CAUSAL ? min(S, qrow + 1) : S;
       // pass 1: row max
       float mx = -1e30f;
 #pragma unroll
       for (int c = 0; c < FBN / 32; ++c) {
         float v[32];
         tmem_ld32(tS[st] + lane_off + c * 32, v);
+        if (edge) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = k0 + c * 32 + i;
-          const bool ok = !edge || (key < S && (!CAUSAL || key <= qrow));
-          mx = fmaxf(mx, ok ? v[i] : -1e30f);
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, (k0 + c * 32 + i < lim) ? v[i] : -1e30f);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
         }
       }
       const float mnew = fmaxf(m, mx * scale_log2);
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(256, 1)
       if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
       if (__any_sync(0xffffffffu, need) && j > 0) {
         tc_fence_after();
-        const float f = need ? exp2f(m - mnew) : 1.0f;
+        const float f = need ? fast_exp2(m - mnew) : 1.0f;
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
           float o[16];
@@ -237,11 +240,12 @@ __global__ void __launch_bounds__(256, 1)
         tmem_st_wait();
       }
       if (need) {
-        l *= exp2f(m - mnew);
+        l *= fast_exp2(m - mnew);
         m = mnew;
       }
       // pass 2: P = exp2(s*scale - m) -> bf16 -> swizzled smem
-      float ls = 0.f;
+      const float nm = -m;
+      float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
       for (int c = 0; c < FBN / 32; ++c) {
         float v[32];
@@ -249,12 +253,15 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const int key = k0 + c * 32 + i;
-          const bool ok0 = !edge || (key < S && (!CAUSAL || key <= qrow));
-          const bool ok1 = !edge || (key + 1 < S && (!CAUSAL || key + 1 <= qrow));
-          const float p0 = ok0 ? exp2f(v[i] * scale_log2 - m) : 0.f;
-          const float p1 = ok1 ? exp2f(v[i + 1] * scale_log2 - m) : 0.f;
-          ls += p0 + p1;
+          float p0 = fast_exp2(fmaf(v[i], scale_log2, nm));
+          float p1 = fast_exp2(fmaf(v[i + 1], scale_log2, nm));
+          if (edge) {
+            const int key = k0 + c * 32 + i;
+            p0 = key < lim ? p0 : 0.f;
+            p1 = key + 1 < lim ? p1 : 0.f;
+          }
+          ls0 += p0;
+          ls1 += p1;
           pk[i / 2] = pack_bf16(p0, p1);
         }
         // 32 keys = 64 B = four 16-byte chunks of row `row` in key chunk (c / 2)
@@ -266,6 +273,7 @@ __global__ void __launch_bounds__(256, 1)
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
       }
+      const float ls = ls0 + ls1;
       l += ls;
       tc_fence_before();
       mbar_arrive(&s_empty[st]);
@@ -274,6 +282,210 @@ __global__ void __launch_bounds__(256, 1)
     }
     // epilogue: O / l -> bf16 rows
     mbar_wait(pv_done, (n_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 16; ++c) {
+      float o[16];
+      tmem_ld16(tO + lane_off + c * 16, o);
+      if (qrow < S) {
+        uint4 a = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
+                             pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
+        uint4 b = make_uint4(pack_bf16(o[8] * inv, o[9] * inv), pack_bf16(o[10] * inv, o[11] * inv),
+                             pack_bf16(o[12] * inv, o[13] * inv), pack_bf16(o[14] * inv, o[15] * inv));
+        reinterpret_cast<uint4*>(orow + c * 16)[0] = a;
+        reinterpret_cast<uint4*>(orow + c * 16)[1] = b;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// v2: two CTAs per SM.  P stays in TMEM (bf16 pairs written over the S columns already read:
+// the FA4 aliasing) and the P.V product is a TS MMA (A from TMEM), so shared memory holds only
+// Q, K_j, V_j (single-buffered, 96 KB) and TMEM only S|P (128 cols) + O (<= 128 cols).  The two
+// CTAs on an SM interleave: one CTA's softmax runs while the other's MMAs use the tensor core.
+// In-CTA order per key tile: S_j (after PV_{j-1}, issue order) -> softmax_j -> PV_j.
+template <int HD>
+struct Ft2Cfg {
+  static constexpr int NCH = (HD + CHUNK - 1) / CHUNK;
+  static constexpr int TILE_BYTES = NCH * FBN * CHUNK * 2;
+  static constexpr int Q_OFF = 0, K_OFF = TILE_BYTES, V_OFF = 2 * TILE_BYTES, BAR_OFF = 3 * TILE_BYTES;
+  static constexpr int SMEM = 1024 + BAR_OFF + 128;
+  static constexpr int TMEM_COLS = 256;
+};
+
+NOVA_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+NOVA_DEV void tmem_st16u(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(256, 2)
+    fmha2_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, int ldo, int S, int H, int KV,
+                 float scale_log2) {
+  using C = Ft2Cfg<HD>;
+  constexpr int NCH = C::NCH;
+  constexpr uint32_t IDESC_S = umma_idesc_bf16(FBM, FBN);
+  constexpr uint32_t IDESC_O = umma_idesc_bf16(FBM, HD) | (1u << 16);  // B (V) MN-major
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t *q_full = bars + 0, *k_full = bars + 1, *k_empty = bars + 2, *v_full = bars + 3, *v_empty = bars + 4;
+  uint64_t *s_full = bars + 5, *p_full = bars + 6, *o_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y;
+  const int kvh = h / (H / KV);
+  const int q0 = qt * FBM;
+  const int n_tiles_all = (S + FBN - 1) / FBN;
+  const int n_tiles = CAUSAL ? min(n_tiles_all, (q0 + FBM + FBN - 1) / FBN) : n_tiles_all;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], i == 6 ? 128 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t tS = tbase, tO = tbase + FBN;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (single-buffered K and V)
+      const int qcol = h * HD, kcol = (H + kvh) * HD, vcol = (H + KV + kvh) * HD;
+      mbar_arrive_expect_tx(q_full, C::TILE_BYTES);
+      for (int c = 0; c < NCH; ++c) tma_load_2d(smem + C::Q_OFF + c * FBN * 128, &tm, q_full, qcol + c * CHUNK, q0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const uint32_t ph = (j & 1) ^ 1;
+        mbar_wait(k_empty, ph);
+        mbar_arrive_expect_tx(k_full, C::TILE_BYTES);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_2d(smem + C::K_OFF + c * FBN * 128, &tm, k_full, kcol + c * CHUNK, j * FBN);
+        mbar_wait(v_empty, ph);
+        mbar_arrive_expect_tx(v_full, C::TILE_BYTES);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_2d(smem + C::V_OFF + c * FBN * 128, &tm, v_full, vcol + c * CHUNK, j * FBN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t qa = smem_u32(smem + C::Q_OFF), kb = smem_u32(smem + C::K_OFF), vb = smem_u32(smem + C::V_OFF);
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(k_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k * 16 / CHUNK) * FBN * 128 + (k * 16 % CHUNK) * 2;
+          umma_bf16_ss(tS, umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), IDESC_S, k > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);   // also covers PV_{j-1}: O is stable once S_j is visible
+        umma_commit(k_empty);
+        mbar_wait(p_full, j & 1);
+        mbar_wait(v_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < FBN / 16; ++k)  // P: 16 keys = 8 packed TMEM columns per step
+          umma_bf16_ts(tO, tS + k * 8, umma_desc_sw128_mn(vb + k * 16 * 128, FBN * 128), IDESC_O,
+                       (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(v_empty);
+      }
+      umma_commit(o_done);
+    }
+  } else if (warp >= 4) {  // ---------------- softmax / correction / epilogue
+    const int row = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int qrow = q0 + row;
+    float m = -1e30f, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      const int k0 = j * FBN;
+      const bool edge = (k0 + FBN > S) || (CAUSAL && k0 + FBN > q0);
+      const int lim = CAUSAL ? min(S, qrow + 1) : S;
+      float mx = -1e30f;
+#pragma unroll
+      for (int c = 0; c < FBN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tS + lane_off + c * 32, v);
+        if (edge) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, (k0 + c * 32 + i < lim) ? v[i] : -1e30f);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
+        }
+      }
+      const float mnew = fmaxf(m, mx * scale_log2);
+      const bool need = (mnew - m) > 8.0f;
+      if (__any_sync(0xffffffffu, need) && j > 0) {  // lazy rescale of O in TMEM (PV_{j-1} done: see s_full)
+        const float f = need ? fast_exp2(m - mnew) : 1.0f;
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + lane_off + c * 16, o);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] *= f;
+          tmem_st16(tO + lane_off + c * 16, o);
+        }
+      }
+      if (need) {
+        l *= fast_exp2(m - mnew);
+        m = mnew;
+      }
+      const float nm = -m;
+      float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < FBN / 32; ++c) {
+        // S chunk c (cols 32c..32c+31) is re-read; P chunk c lands in cols 16c..16c+15, i.e. over
+        // S columns this thread has already read (chunks <= c), so the aliasing is safe
+        float sv[32];
+        tmem_ld32(tS + lane_off + c * 32, sv);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = fast_exp2(fmaf(sv[i], scale_log2, nm));
+          float p1 = fast_exp2(fmaf(sv[i + 1], scale_log2, nm));
+          if (edge) {
+            const int key = k0 + c * 32 + i;
+            p0 = key < lim ? p0 : 0.f;
+            p1 = key + 1 < lim ? p1 : 0.f;
+          }
+          ls0 += p0;
+          ls1 += p1;
+          pk[i / 2] = pack_bf16(p0, p1);
+        }
+        tmem_st16u(tS + lane_off + c * 16, pk);  // P keys 32c..32c+31 -> packed columns 16c..16c+15
+      }
+      l += ls0 + ls1;
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16 rows
+    mbar_wait(o_done, 0);
     tc_fence_after();
     const float inv = 1.0f / l;
     bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
@@ -339,6 +551,22 @@ cudaError_t fmha_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int 
   return cudaGetLastError();
 }
 
+template <int HD, bool CAUSAL>
+cudaError_t fmha2_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, cudaStream_t s) {
+  CUtensorMap tm;
+  if (!make_qkv_map(&tm, qkv, S, ld)) return cudaErrorInvalidValue;
+  auto kern = fmha2_kernel<HD, CAUSAL>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Ft2Cfg<HD>::SMEM);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  const float sl2 = LOG2E_F / sqrtf((float)HD);
+  return launch_k(kern, dim3((S + FBM - 1) / FBM, H), dim3(256), Ft2Cfg<HD>::SMEM, s, false, tm, out, ldo, S, H, KV,
+                  sl2);
+}
+
 }  // namespace
 
 // ld (the qkv row length in elements) must be a multiple of 8; hd in {80, 128} (64-col SW128 chunks).
@@ -346,6 +574,15 @@ cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, in
                           cudaStream_t s) {
   if (S <= 0) return cudaSuccess;
   if (ld % 8 || H % KV || ldo % 8) return cudaErrorInvalidValue;
+  if (g_fmha_version == 2) {
+    switch (hd) {
+      case 80: return causal ? fmha2_launch<80, true>(qkv, ld, out, ldo, S, H, KV, s)
+                             : fmha2_launch<80, false>(qkv, ld, out, ldo, S, H, KV, s);
+      case 128: return causal ? fmha2_launch<128, true>(qkv, ld, out, ldo, S, H, KV, s)
+                              : fmha2_launch<128, false>(qkv, ld, out, ldo, S, H, KV, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (hd) {
     case 80: return causal ? fmha_launch<80, true>(qkv, ld, out, ldo, S, H, KV, s)
                            : fmha_launch<80, false>(qkv, ld, out, ldo, S, H, KV, s);
@@ -354,5 +591,7 @@ cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, in
   }
   return cudaErrorInvalidValue;
 }
+
+int g_fmha_version = 2;
 
 }  // namespace nova

@@ -200,7 +200,8 @@ class Engine {
     float* h_logits;
   } fw{};
   struct DecWS {
-    float *hid, *xf, *logits, *attn_ws;
+    float *hid, *xf, *logits, *attn_ws, *gemv_ws;
+    int* tickets;
     bf16 *xb, *qkv, *attn, *act;
     DecodeRow* rows;
     int* tok;

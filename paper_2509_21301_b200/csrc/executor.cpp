@@ -315,6 +315,7 @@ nova_status Engine::finalize() {
   cudaMemset(d_prompt, 0, (size_t)n_slots_total * cfg.max_prompt * 4);
   cudaMemset(d_bt, 0, (size_t)n_slots_total * max_pages_per_req * 4);
   cudaMemset(d_last, 0, (size_t)n_slots_total * 4);
+  cudaMemset(dw.tickets, 0, 8192 * 4);
   ktimer[0].init(512);
   ktimer[1].init(512);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(NOVA_E_CUDA, "finalize sync");

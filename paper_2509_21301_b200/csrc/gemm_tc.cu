@@ -295,11 +295,28 @@ cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int
   if (M <= 0) return cudaSuccess;
   if (N % 64 != 0 || K <= 0 || (lda % 8) || (ldw % 8) || (ldc % 8)) return cudaErrorInvalidValue;
   GemmArgs g{C, bias, M, N, K, ldc};
-  // widest tile that still gives >= 2 tiles per CTA of the SM budget (wave balance for narrow N)
+  // Tile width by modelled time = waves x per-tile time: waves = ceil(tiles / CTAs) (wave
+  // quantisation on the partition's SM budget), per-tile time ~ BN / efficiency(BN) (narrow
+  // tiles re-read A more often: measured ~0.92 at 128, ~0.75 at 64 of the 256-wide rate).
+  // The reference budget is the whole GPU (148 SMs), NOT max_ctas: the tiling must not depend
+  // on the partition so that co-executed passes stay bitwise equal to serial ones.
   const int mblk = (M + BM - 1) / BM;
-  if (N % 256 == 0 && (mblk * (N / 256) >= 2 * max_ctas || N % 128 != 0))
-    return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
-  if (N % 128 == 0) return dispatch_epi<128>(A, lda, W, ldw, g, epi, max_ctas, s);
+  const int ctas = 148;
+  double best = 1e30;
+  int bn = 64;
+  const int cand[3] = {256, 128, 64};
+  const double eff[3] = {1.0, 0.92, 0.75};
+  for (int i = 0; i < 3; ++i) {
+    if (N % cand[i]) continue;
+    const long tiles = (long)mblk * (N / cand[i]);
+    const double t = (double)((tiles + ctas - 1) / ctas) * cand[i] / eff[i];
+    if (t < best - 1e-9) {
+      best = t;
+      bn = cand[i];
+    }
+  }
+  if (bn == 256) return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
+  if (bn == 128) return dispatch_epi<128>(A, lda, W, ldw, g, epi, max_ctas, s);
   return dispatch_epi<64>(A, lda, W, ldw, g, epi, max_ctas, s);
 }
 

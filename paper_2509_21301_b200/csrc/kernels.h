@@ -58,6 +58,14 @@ cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int
 cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K, void* Y, int ldy,
                  const bf16* bias, int B, int epi, cudaStream_t s);
 
+// TMA-streamed decode GEMV (bf16 X): 64-row CTAs, 8-stage smem ring, split-K over P CTAs
+// (P = gemv_tma_splits(N, K), shape-only) with a deterministic last-CTA reduction.
+// ws: P*B*N floats, tickets: N/64 ints (zero-initialised once; the kernel restores them).
+cudaError_t gemv_tma(const bf16* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
+                     int epi, float* ws, int* tickets, cudaStream_t s);
+int gemv_tma_splits(int N, int K);
+extern bool g_use_tma_gemv;
+
 // Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).
 // out [S][H * hd] (ldo).  causal: key j <= query i.  Query head h reads KV head h / (H / KV).
 cudaError_t flash_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
@@ -65,6 +73,7 @@ cudaError_t flash_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, in
 // tcgen05/TMEM/TMA version (hd 80 / 128); flash_attn() dispatches to it for those head dims.
 cudaError_t flash_attn_tc(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                           cudaStream_t s);
+extern int g_fmha_version;  // 2: 2 CTAs/SM, P in TMEM (default); 1: single CTA, P in smem
 // legacy warp-MMA (mma.sync) version, kept for head dims 16/32/64 and as the measured baseline
 cudaError_t flash_attn_mma(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                            cudaStream_t s);

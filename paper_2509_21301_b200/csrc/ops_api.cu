@@ -19,6 +19,11 @@ int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K,
                  int B, int epi, void* stream) {
   return st(gemv(X, x_f32, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, S(stream)));
 }
+int nova_op_gemv_tma(const void* X, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias, int B,
+                     int epi, float* ws, int32_t* tickets, void* stream) {
+  return st(gemv_tma((const bf16*)X, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, ws, tickets,
+                     S(stream)));
+}
 int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int Sq, int H, int KV, int hd, int causal,
                        void* stream) {
   return st(flash_attn((const bf16*)qkv, ld, (bf16*)out, ldo, Sq, H, KV, hd, causal, S(stream)));

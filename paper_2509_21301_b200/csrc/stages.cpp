@@ -69,7 +69,11 @@ static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xf32, int ldx, 
   const double bytes = (double)N * K * 2 + (double)B * K * (xf32 ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  CUDA_TRY(gemv(X, xf32, ldx, W, N, K, Y, ldy, bias, B, epi, s));
+  if (!xf32 && g_use_tma_gemv)
+    CUDA_TRY(gemv_tma(reinterpret_cast<const bf16*>(X), ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws,
+                      E->dw.tickets, s));
+  else
+    CUDA_TRY(gemv(X, xf32, ldx, W, N, K, Y, ldy, bias, B, epi, s));
   E->ktimer[1].end(i, cls, bytes, s);
   return cudaSuccess;
 }

@@ -31,6 +31,19 @@ def nova_op_gemv(X, W, Y, bias, N, K, B, epi, x_f32=None, ldx=None, ldy=None, st
                              epi, _s(stream)), "gemv")
 
 
+_ws_cache = {}
+
+
+def nova_op_gemv_tma(X, W, Y, bias, N, K, B, epi, ldx=None, ldy=None, stream=None):
+    dev = X.device
+    if dev not in _ws_cache:
+        _ws_cache[dev] = (torch.empty(16 * 16 * 160000, dtype=torch.float32, device=dev),
+                          torch.zeros(8192, dtype=torch.int32, device=dev))
+    ws, tk = _ws_cache[dev]
+    check(lib().nova_op_gemv_tma(_p(X), ldx or X.stride(0), _p(W), N, K, _p(Y), ldy or Y.stride(0), _p(bias), B,
+                                 epi, _p(ws), _p(tk), _s(stream)), "gemv_tma")
+
+
 def nova_op_flash_attn(qkv, out, S, H, KV, hd, causal, stream=None):
     check(lib().nova_op_flash_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), S, H, KV, hd, int(causal),
                                    _s(stream)), "flash_attn")

@@ -53,11 +53,16 @@ def bench_gemv(iters):
             nout = N // 2 if epi == O.EPI_BF16_SILUMUL else N
             Y = torch.zeros(B, nout, device="cuda", dtype=torch.bfloat16 if epi in (O.EPI_BF16, O.EPI_BF16_SILUMUL)
                             else torch.float32)
-            ms = timeit(lambda i: O.nova_op_gemv(X, Ws[i], Y, None, N, K, B, epi), iters, rot)
             byt = wbytes + B * K * (4 if xf else 2) + B * nout * (8 if epi == O.EPI_F32_RESID else 4)
-            gbs = byt / ms / 1e6
-            print(json.dumps({"kernel": "gemv", "shape": name, "N": N, "K": K, "B": B, "us": round(ms * 1e3, 2),
-                              "GB/s": round(gbs, 1), "frac_hbm": round(gbs / HBM, 3)}), flush=True)
+            variants = [("gemv", lambda i: O.nova_op_gemv(X, Ws[i], Y, None, N, K, B, epi))]
+            if not xf:
+                variants.append(("gemv_tma", lambda i: O.nova_op_gemv_tma(X, Ws[i], Y, None, N, K, B, epi)))
+            for kname, fn in variants:
+                ms = timeit(fn, iters, rot)
+                gbs = byt / ms / 1e6
+                print(json.dumps({"kernel": kname, "shape": name, "N": N, "K": K, "B": B,
+                                  "us": round(ms * 1e3, 2), "GB/s": round(gbs, 1),
+                                  "frac_hbm": round(gbs / HBM, 3)}), flush=True)
         del Ws
 
 

@@ -102,6 +102,46 @@ def test_gemv_and_batch_invariance(N, K):
     assert rel_inf(R.cpu().numpy(), R0.cpu().numpy() + ref[:5]) <= 1e-4
 
 
+@pytest.mark.parametrize("N,K", [(256, 128), (4608, 3584), (3584, 18944), (2048, 1536), (37888, 3584)])
+def test_gemv_tma_matches_oracle_and_is_invariant(N, K):
+    rng = np.random.default_rng(N * 3 + K)
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    b = rand_bf16(rng, (N,), 0.1)
+    X = rand_bf16(rng, (16, K))
+    dW, db, dX = bf16_dev(W), bf16_dev(b), bf16_dev(X)
+    ref = V.linear(X.astype(np.float64), W.astype(np.float64), b.astype(np.float64))
+    rows = {}
+    for B in (1, 5, 8, 9, 16):
+        Y = torch.empty(B, N, dtype=torch.float32, device="cuda")
+        O.nova_op_gemv_tma(dX[:B], dW, Y, db, N, K, B, O.EPI_F32_STORE)
+        torch.cuda.synchronize()
+        rows[B] = Y.cpu().numpy()
+        assert rel_inf(rows[B], ref[:B]) <= 1e-4
+    for B in (5, 8, 9, 16):
+        assert np.array_equal(rows[B][0], rows[1][0])      # bitwise batch invariance
+    Y2 = torch.empty(16, N, dtype=torch.float32, device="cuda")
+    O.nova_op_gemv_tma(dX, dW, Y2, db, N, K, 16, O.EPI_F32_STORE)   # deterministic re-run
+    torch.cuda.synchronize()
+    assert np.array_equal(Y2.cpu().numpy(), rows[16])
+    R0 = torch.randn(3, N, device="cuda")
+    R = R0.clone()
+    O.nova_op_gemv_tma(dX[:3], dW, R, db, N, K, 3, O.EPI_F32_RESID)
+    Yb = torch.empty(3, N, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_gemv_tma(dX[:3], dW, Yb, db, N, K, 3, O.EPI_BF16)
+    torch.cuda.synchronize()
+    assert rel_inf(R.cpu().numpy(), R0.cpu().numpy() + ref[:3]) <= 1e-4
+    assert rel_inf(bf16_host(Yb), ref[:3]) <= 8e-3
+    if N % 64 == 0 and N >= 256:
+        F = N // 2
+        Wg, Wu = W[:F], W[F:]
+        Yg = torch.empty(4, F, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_gemv_tma(dX[:4], bf16_dev(interleave_gate_up(Wg, Wu)), Yg, None, N, K, 4, O.EPI_BF16_SILUMUL)
+        torch.cuda.synchronize()
+        x64 = X[:4].astype(np.float64)
+        refg = V.silu(x64 @ Wg.T.astype(np.float64)) * (x64 @ Wu.T.astype(np.float64))
+        assert rel_inf(bf16_host(Yg), refg) <= 8e-3
+
+
 def test_gemv_f32_input_and_silu():
     rng = np.random.default_rng(3)
     N, K = 512, 256
