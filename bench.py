@@ -426,6 +426,9 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    prof_range = os.environ.get("NOVA_PROFILER_RANGE") == "1"   # ncu --profile-from-start off
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     res = []
@@ -435,6 +438,8 @@ def main():
     ev1.record()
     torch.cuda.synchronize()
     launches = eng.lib.nova_launch_count() - launches0
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     ks = eng.kernel_stats()
     eng.kernel_timing(0)
     # end-to-end: pinned host screenshots, H2D inside the timed region

@@ -16,6 +16,9 @@ namespace nova {
 namespace {
 
 constexpr float LOG2E = 1.4426950408889634f;
+}  // namespace
+bool g_decode_attn_tc = true;
+namespace {
 
 template <int HD>
 struct FaCfg {
@@ -363,14 +366,152 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   }
 }
 
+// Tensor-core decode attention: the G query heads that share one KV head are the M side of
+// mma.sync m16n8k16 (padded to 16 rows), keys the N side.  CTA = (request, KV head, 128-key
+// chunk); each of the 4 warps owns 32 keys: cp.async gathers its K/V rows from the pages into
+// smem, S = Q K^T (4 n-tiles x HD/16 k-steps), masked softmax in registers, O = P V, and one
+// partial (m, l, o) per query head goes to the workspace for the fixed-order merge.
+constexpr int TKW = 32;  // keys per warp
+template <int HD>
+struct DtcCfg {
+  static constexpr int HDP = HD + 8;  // padded row (conflict-free ldmatrix)
+  static constexpr int SMEM = (16 + 2 * 4 * TKW) * HDP * 2;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128) decode_attn_tc_partial(const bf16* __restrict__ qkv, int ld,
+                                                              const bf16* __restrict__ pool, int layer, int n_pages,
+                                                              int H, int KV, const int* __restrict__ bt, int max_pages,
+                                                              const DecodeRow* __restrict__ rows,
+                                                              float* __restrict__ ws, int n_part, float scale_log2) {
+  constexpr int HDP = DtcCfg<HD>::HDP, CH = HD / 8, KT = HD / 16, DT = HD / 8;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  bf16* sQ = reinterpret_cast<bf16*>(dsm);
+  bf16* sK = sQ + 16 * HDP;
+  bf16* sV = sK + 4 * TKW * HDP;
+  pdl_launch_dependents();
+  pdl_wait();
+  const int b = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z;
+  const int G = H / KV;
+  const DecodeRow rr = rows[b];
+  const int L = rr.ctx + 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j0 = ch * 4 * TKW;
+  if (j0 >= L) return;
+  // Q rows g < G (rows >= G zero)
+  for (int i = tid; i < 16 * CH; i += 128) {
+    const int r = i / CH, c = i % CH;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < G) v = *reinterpret_cast<const uint4*>(qkv + (size_t)b * ld + (size_t)(kvh * G + r) * HD + c * 8);
+    *reinterpret_cast<uint4*>(sQ + r * HDP + c * 8) = v;
+  }
+  const int w0 = j0 + warp * TKW;  // this warp's first key
+  const bool active = w0 < L;
+  const size_t page_stride = (size_t)2 * KV * 64 * HD;
+  const bf16* lbase = pool + (size_t)layer * n_pages * page_stride;
+  const int* btr = bt + (size_t)rr.slot * max_pages;
+  bf16* wK = sK + warp * TKW * HDP;
+  bf16* wV = sV + warp * TKW * HDP;
+  if (active) {
+    for (int i = lane; i < TKW * CH; i += 32) {
+      const int r = i / CH, c = i % CH;
+      const int j = w0 + r;
+      const bool ok = j < L;
+      const int jj = ok ? j : w0;
+      const bf16* kp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)kvh * 64 + (jj & 63)) * HD + c * 8;
+      cp_async16(wK + r * HDP + c * 8, kp, ok);
+      cp_async16(wV + r * HDP + c * 8, kp + (size_t)KV * 64 * HD, ok);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (!active) return;
+  const int g = lane >> 2, c = lane & 3;
+  uint32_t qa[KT][4];
+#pragma unroll
+  for (int kk = 0; kk < KT; ++kk) ldmatrix_x4(qa[kk], smem_u32(sQ + (lane & 15) * HDP + kk * 16 + (lane >> 4) * 8));
+  float s[4][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      uint32_t bb[2];
+      ldmatrix_x2(bb, smem_u32(wK + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
+      mma_bf16_16816(s[nt], qa[kk], bb);
+    }
+  }
+  // rows g (s[.][0..1]) and g+8 (s[.][2..3]); keys w0 + nt*8 + 2c + (j&1)
+  float mx[2] = {-1e30f, -1e30f};
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = w0 + nt * 8 + 2 * c + (j & 1) < L;
+      s[nt][j] = ok ? s[nt][j] * scale_log2 : -1e30f;
+      mx[j >> 1] = fmaxf(mx[j >> 1], s[nt][j]);
+    }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+  }
+  float ls[2] = {0.f, 0.f};
+  uint32_t pa[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const float p0 = exp2f(s[nt][0] - mx[0]), p1 = exp2f(s[nt][1] - mx[0]);
+    const float p2 = exp2f(s[nt][2] - mx[1]), p3 = exp2f(s[nt][3] - mx[1]);
+    ls[0] += p0 + p1;
+    ls[1] += p2 + p3;
+    pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+    pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    ls[r] += __shfl_xor_sync(0xffffffffu, ls[r], 1);
+    ls[r] += __shfl_xor_sync(0xffffffffu, ls[r], 2);
+  }
+  float o[DT][4];
+#pragma unroll
+  for (int dt = 0; dt < DT; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      uint32_t bb[2];
+      ldmatrix_x2_trans(bb, smem_u32(wV + (kk * 16 + (lane & 15)) * HDP + dt * 8));
+      mma_bf16_16816(o[dt], pa[kk], bb);
+    }
+  }
+  // partial p of head (kvh*G + row): [m, l, o[HD]]
+  const int p = ch * 4 + warp;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = g + 8 * r;
+    if (row >= G) continue;
+    float* w = ws + (((size_t)b * H + kvh * G + row) * n_part + p) * (HD + 2);
+    if (c == 0) {
+      w[0] = mx[r];
+      w[1] = ls[r];
+    }
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      w[2 + dt * 8 + 2 * c] = o[dt][2 * r];
+      w[2 + dt * 8 + 2 * c + 1] = o[dt][2 * r + 1];
+    }
+  }
+}
+
 template <int HD>
 __global__ void decode_attn_combine(const float* __restrict__ ws, const DecodeRow* __restrict__ rows, bf16* out,
-                                    int ldo, int H, int n_chunks) {
+                                    int ldo, int H, int n_chunks, int keys_per_part) {
   pdl_launch_dependents();
   pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int L = rows[b].ctx + 1;
-  const int nc = (L + DCHUNK - 1) / DCHUNK;
+  const int nc = (L + keys_per_part - 1) / keys_per_part;
   const float* w = ws + ((size_t)b * H + h) * n_chunks * (HD + 2);
   float M = -1e30f;
   for (int c = 0; c < nc; ++c) M = fmaxf(M, w[c * (HD + 2)]);
@@ -387,13 +528,31 @@ template <int HD>
 cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
                       int KV, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx, float* ws,
                       cudaStream_t s) {
+  if (H / KV > 16) return cudaErrorInvalidValue;
+  const float sl2 = LOG2E / sqrtf((float)HD);
+  cudaError_t e;
+  if (g_decode_attn_tc) {  // tensor-core version: 128-key chunks, one partial per 32-key warp slice
+    const int n_chunks = (max_ctx + 1 + 4 * TKW - 1) / (4 * TKW);
+    const int n_part = n_chunks * 4;
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(decode_attn_tc_partial<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           DtcCfg<HD>::SMEM);
+      set = true;
+    }
+    e = launch_k(decode_attn_tc_partial<HD>, dim3(B, KV, n_chunks), dim3(128), DtcCfg<HD>::SMEM, s, true, qkv, ld,
+                 pool, layer, n_pages, H, KV, bt, max_pages, rows, ws, n_part, sl2);
+    if (e != cudaSuccess) return e;
+    e = launch_k(decode_attn_combine<HD>, dim3(B, H), dim3(HD), 0, s, true, ws, rows, out, ldo, H, n_part, TKW);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   if (H / KV > MAXG) return cudaErrorInvalidValue;
   const int n_chunks = (max_ctx + 1 + DCHUNK - 1) / DCHUNK;
-  const float sl2 = LOG2E / sqrtf((float)HD);
-  cudaError_t e = launch_k(decode_attn_partial<HD>, dim3(B, KV, n_chunks), dim3(DCHUNK), 0, s, true, qkv, ld, pool,
-                           layer, n_pages, H, KV, bt, max_pages, rows, ws, n_chunks, sl2);
+  e = launch_k(decode_attn_partial<HD>, dim3(B, KV, n_chunks), dim3(DCHUNK), 0, s, true, qkv, ld, pool, layer,
+               n_pages, H, KV, bt, max_pages, rows, ws, n_chunks, sl2);
   if (e != cudaSuccess) return e;
-  e = launch_k(decode_attn_combine<HD>, dim3(B, H), dim3(HD), 0, s, true, ws, rows, out, ldo, H, n_chunks);
+  e = launch_k(decode_attn_combine<HD>, dim3(B, H), dim3(HD), 0, s, true, ws, rows, out, ldo, H, n_chunks, DCHUNK);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

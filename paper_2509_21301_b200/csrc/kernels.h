@@ -85,6 +85,8 @@ struct DecodeRow {
   int pos;    // M-RoPE position (t = h = w for generated text)
   int pad;
 };
+extern bool g_decode_attn_tc;  // tensor-core decode attention (default) vs the CUDA-core version
+// ws: B * H * (ceil((max_ctx+1)/128)*4) * (hd+2) floats
 cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf16* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int* block_tables, int max_pages, const DecodeRow* rows, int B,
                         int max_ctx, float* ws, cudaStream_t s);

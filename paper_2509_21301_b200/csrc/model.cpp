@@ -135,7 +135,8 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   w.act = (bf16*)take(B * F * 2);
   w.logits = (float*)take(B * V * 4);
   const size_t nch = (max_ctx + 255) / 256;
-  w.attn_ws = (float*)take(B * m.llm_heads * nch * (m.head_dim + 2) * 4);
+  const size_t nparts = std::max(nch, (size_t)(max_ctx + 127) / 128 * 4);  // decode attention partials per head
+  w.attn_ws = (float*)take(B * m.llm_heads * nparts * (m.head_dim + 2) * 4);
   w.gemv_ws = (float*)take((size_t)16 * B * std::max(std::max(D, F), (size_t)d.llm_qkv_n) * 4);
   w.tickets = (int*)take(8192 * 4);
   w.rows = (DecodeRow*)take(B * sizeof(DecodeRow));

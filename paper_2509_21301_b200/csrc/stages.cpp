@@ -69,7 +69,9 @@ static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xf32, int ldx, 
   const double bytes = (double)N * K * 2 + (double)B * K * (xf32 ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  if (!xf32 && g_use_tma_gemv)
+  // TMA-streamed GEMV where it measured faster (large N, no split-K: gate|up, 99.6% vs 93% of
+  // HBM in scripts/kbench.py); the register-streaming GEMV for the small-N shapes
+  if (!xf32 && g_use_tma_gemv && gemv_tma_splits(N, K) == 1)
     CUDA_TRY(gemv_tma(reinterpret_cast<const bf16*>(X), ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws,
                       E->dw.tickets, s));
   else

@@ -109,7 +109,7 @@ def bench_dattn(iters):
         rows = torch.tensor([[b, ctx, 0, 0] for b in range(B)], dtype=torch.int32, device="cuda")
         qkv = rnd((B, (H + 2 * KV) * hd))
         out = torch.empty(B, H * hd, device="cuda", dtype=torch.bfloat16)
-        ws = torch.empty(B * H * ((ctx + 256) // 256 + 1) * (hd + 2), device="cuda")
+        ws = torch.empty(B * H * ((ctx + 128) // 128 + 1) * 4 * (hd + 2), device="cuda")
         ms = timeit(lambda i: O.nova_op_decode_attn(qkv, out, pool, 0, n_pages, H, KV, hd, bt, rows, B, ctx, ws),
                     iters, 1)
         byt = B * (ctx + 1) * 2 * KV * hd * 2
