@@ -29,7 +29,10 @@ enum {
   NOVA_EPI_BF16_GELU = 2,     /* C bf16 = GELU_erf(R)              (patch merger)      */
   NOVA_EPI_BF16_SILUMUL = 3,  /* W rows interleaved [16 gate | 16 up]*; C[:, N/2] bf16 = silu(gate) * up */
   NOVA_EPI_F32_RESID = 4,     /* C f32 += R                        (residual add)     */
-  NOVA_EPI_F32_STORE = 5      /* C f32 = R                                            */
+  NOVA_EPI_F32_STORE = 5,     /* C f32 = R                                            */
+  NOVA_EPI_QKV_ROPE_KV = 6,   /* decode qkv (nova_op_gemv_fused only): R + bias, M-RoPE on q/k
+                                 heads at rows[b].pos; q -> C bf16, k/v -> paged KV cache   */
+  NOVA_EPI_F32_ARGMAX = 7     /* C f32 = R, and greedy argmax into keys[b] (nova_op_gemv_fused) */
 };
 
 /* Dense linear of the vision encoder / prefill: tcgen05 +
@@ -73,12 +76,39 @@ typedef struct {
   int32_t pad;
 } nova_decode_row;
 
-/* Paged decode attention (a7).  Keys 0..ctx (inclusive) of each row.  kv_pool
- * bf16 [layers][n_pages][2][KV][64][hd]; block_tables int32 [slots][max_pages];
- * ws f32 workspace of B*H*ceil((max_ctx+1)/256)*(hd+2) floats. */
+/* Paged decode attention (a7; PAPER.md P:141, P:283 -- memory-bound, PagedAttention
+ * KV layout P:48).  Keys 0..ctx (inclusive) of each row.  kv_pool bf16
+ * [layers][n_pages][2][KV][64][hd]; block_tables int32 [slots][max_pages];
+ * ws f32 workspace of B*H*ceil((max_ctx+1)/64)*(hd+2) floats; tickets int32 [B*KV],
+ * zero on entry and left zero (one launch: chunk partials + last-CTA fixed-order merge).
+ * ceil((max_ctx+1)/128) <= 64, H/KV <= 16.  Deterministic, batch- and grid-invariant. */
 int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int32_t* block_tables, int max_pages, const nova_decode_row* rows,
-                        int B, int max_ctx, float* ws, void* stream);
+                        int B, int max_ctx, float* ws, int32_t* tickets, void* stream);
+
+/* Fused decode linear (a7; "kernel fusion ... RoPE and RMSNorm"):
+ * Y = epilogue(Xin . W^T + bias) for B <= 16 rows, where Xin is, by x_mode:
+ *   0: X bf16;  1: X f32 (hi/lo bf16 split, exact to ~2^-16);
+ *   2: RMSNorm(X f32 residual rows; gamma bf16 [K], eps) rounded to bf16;
+ *   3: RMSNorm(X) in f32, hi/lo split (the lm_head input).
+ * Epilogues: the NOVA_EPI_* above, plus
+ *   NOVA_EPI_QKV_ROPE_KV: W = fused [(H + 2 KV) hd][K] q|k|v rows; bias added, q and k
+ *     rotated by RoPE at rows[b].pos (t = h = w for generated text; log2(theta) given as
+ *     theta), q -> Y[b] (bf16, ldy), k and v -> kv_pool at cache index rows[b].ctx of
+ *     request rows[b].slot (block_tables, max_pages);
+ *   NOVA_EPI_F32_ARGMAX: logits -> Y f32, and keys[b] (uint64, zero on entry) receives the
+ *     packed (order-preserving logit bits << 32 | ~index) maximum: argmax, ties -> lowest
+ *     index.  nova_op_argmax_finalize turns keys into tokens.
+ * Unused pointer arguments may be NULL.  N % 32 == 0, K % 32 == 0. */
+int nova_op_gemv_fused(const void* X, int x_mode, int ldx, const void* W, int N, int K, void* Y, int ldy,
+                       const void* bias, int B, int epi, const void* gamma, float eps, int H, int KV, int hd,
+                       float theta, const nova_decode_row* rows, void* kv_pool, int layer, int n_pages,
+                       const int32_t* block_tables, int max_pages, uint64_t* keys, void* stream);
+
+/* keys[r] (from NOVA_EPI_F32_ARGMAX) -> out_tok[r]; also last_tok[rows[r].slot] (rows != NULL)
+ * or last_tok[single_slot] (>= 0); resets keys[r] to 0.  n <= 1024. */
+int nova_op_argmax_finalize(uint64_t* keys, int n, int32_t* out_tok, const nova_decode_row* rows, int32_t* last_tok,
+                            int single_slot, void* stream);
 
 /* LayerNorm (ViT, mean/biased variance) and RMSNorm (LLM) of f32 rows [M][d]. */
 int nova_op_layernorm(const float* x, int ldx, const void* gamma, const void* beta, void* y, int ldy, int M, int d,

@@ -366,132 +366,183 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
   }
 }
 
-// Tensor-core decode attention: the G query heads that share one KV head are the M side of
-// mma.sync m16n8k16 (padded to 16 rows), keys the N side.  CTA = (request, KV head, 128-key
-// chunk); each of the 4 warps owns 32 keys: cp.async gathers its K/V rows from the pages into
-// smem, S = Q K^T (4 n-tiles x HD/16 k-steps), masked softmax in registers, O = P V, and one
-// partial (m, l, o) per query head goes to the workspace for the fixed-order merge.
-constexpr int TKW = 32;  // keys per warp
+// Tensor-core decode attention, one launch, merged through a thread-block cluster (DSMEM).
+// Cluster = DA_CL CTAs per (request, KV head); CTA = 4 warps; the context is cut into 32-key
+// blocks and warp w of cluster rank r owns blocks (r*4 + w), (r*4 + w) + 4*DA_CL, ...  A warp
+// streams its blocks through a 2-stage cp.async ring in its own smem slice (pages gathered
+// through the block table), and keeps an online softmax over them: S = Q K^T with the G query
+// heads sharing the KV head as the M side of mma.sync m16n8k16 (padded to 16 rows), keys the
+// N side; O += P V.  The 4 warp states are merged in smem in warp order, then rank 0 reads the
+// DA_CL CTA states from the peers' shared memory (mapa + ld.shared::cluster) and merges them in
+// rank order.  Every reduction order depends only on the context length -> deterministic,
+// batch- and SM-budget-invariant; no global workspace, no second kernel.
+constexpr int TKW = 32;   // keys per block
+constexpr int DA_CL = 4;  // CTAs per (request, KV head)
 template <int HD>
 struct DtcCfg {
-  static constexpr int HDP = HD + 8;  // padded row (conflict-free ldmatrix)
-  static constexpr int SMEM = (16 + 2 * 4 * TKW) * HDP * 2;
+  static constexpr int HDP = HD + 8;                       // padded row (conflict-free ldmatrix)
+  static constexpr int BLK = 2 * TKW * HDP * 2;            // one K+V block (bytes)
+  static constexpr int Q_BYTES = 16 * HDP * 2;
+  static constexpr int RING = 4 * 2 * BLK;                 // 4 warps x 2 stages
+  static constexpr int ST_OFF = Q_BYTES + RING;            // CTA state [16][HD + 2] f32
+  static constexpr int SMEM = ST_OFF + 16 * (HD + 2) * 4;
 };
 
+NOVA_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+NOVA_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+NOVA_DEV float ld_dsmem_f32(uint32_t local_saddr, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_saddr), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
 template <int HD>
-__global__ void __launch_bounds__(128) decode_attn_tc_partial(const bf16* __restrict__ qkv, int ld,
-                                                              const bf16* __restrict__ pool, int layer, int n_pages,
-                                                              int H, int KV, const int* __restrict__ bt, int max_pages,
-                                                              const DecodeRow* __restrict__ rows,
-                                                              float* __restrict__ ws, int n_part, float scale_log2) {
-  constexpr int HDP = DtcCfg<HD>::HDP, CH = HD / 8, KT = HD / 16, DT = HD / 8;
+__global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restrict__ qkv, int ld,
+                                                             const bf16* __restrict__ pool, int layer, int n_pages,
+                                                             int H, int KV, const int* __restrict__ bt, int max_pages,
+                                                             const DecodeRow* __restrict__ rows, bf16* __restrict__ out,
+                                                             int ldo, float scale_log2) {
+  using Cf = DtcCfg<HD>;
+  constexpr int HDP = Cf::HDP, CH = HD / 8, KT = HD / 16, DT = HD / 8, PW = HD + 2;
   extern __shared__ __align__(16) uint8_t dsm[];
   bf16* sQ = reinterpret_cast<bf16*>(dsm);
-  bf16* sK = sQ + 16 * HDP;
-  bf16* sV = sK + 4 * TKW * HDP;
+  float* sW = reinterpret_cast<float*>(dsm + Cf::Q_BYTES);  // warp states [4][16][PW] (after the ring drains)
+  float* sS = reinterpret_cast<float*>(dsm + Cf::ST_OFF);   // CTA state [16][PW]
   pdl_launch_dependents();
   pdl_wait();
-  const int b = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z;
+  const int rank = (int)cluster_rank();
+  const int kvh = blockIdx.y, b = blockIdx.z;
   const int G = H / KV;
   const DecodeRow rr = rows[b];
   const int L = rr.ctx + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int j0 = ch * 4 * TKW;
-  if (j0 >= L) return;
-  // Q rows g < G (rows >= G zero)
-  for (int i = tid; i < 16 * CH; i += 128) {
+  for (int i = tid; i < 16 * CH; i += 128) {  // Q rows g < G (rows >= G zero)
     const int r = i / CH, c = i % CH;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < G) v = *reinterpret_cast<const uint4*>(qkv + (size_t)b * ld + (size_t)(kvh * G + r) * HD + c * 8);
     *reinterpret_cast<uint4*>(sQ + r * HDP + c * 8) = v;
   }
-  const int w0 = j0 + warp * TKW;  // this warp's first key
-  const bool active = w0 < L;
   const size_t page_stride = (size_t)2 * KV * 64 * HD;
   const bf16* lbase = pool + (size_t)layer * n_pages * page_stride;
   const int* btr = bt + (size_t)rr.slot * max_pages;
-  bf16* wK = sK + warp * TKW * HDP;
-  bf16* wV = sV + warp * TKW * HDP;
-  if (active) {
+  const int nblk = (L + TKW - 1) / TKW;
+  const int wg = rank * 4 + warp, wstride = 4 * DA_CL;
+  bf16* ring = reinterpret_cast<bf16*>(dsm + Cf::Q_BYTES) + (size_t)warp * 2 * (Cf::BLK / 2);
+  auto issue = [&](int blk, int stage) {  // gather K and V rows of block blk into stage
+    bf16* wK = ring + (size_t)stage * (Cf::BLK / 2);
+    bf16* wV = wK + TKW * HDP;
+    const int k0 = blk * TKW;
     for (int i = lane; i < TKW * CH; i += 32) {
       const int r = i / CH, c = i % CH;
-      const int j = w0 + r;
+      const int j = k0 + r;
       const bool ok = j < L;
-      const int jj = ok ? j : w0;
+      const int jj = ok ? j : k0;
       const bf16* kp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)kvh * 64 + (jj & 63)) * HD + c * 8;
       cp_async16(wK + r * HDP + c * 8, kp, ok);
       cp_async16(wV + r * HDP + c * 8, kp + (size_t)KV * 64 * HD, ok);
     }
-  }
+  };
+  if (wg < nblk) issue(wg, 0);
   cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  if (!active) return;
+  __syncthreads();  // Q in smem
   const int g = lane >> 2, c = lane & 3;
   uint32_t qa[KT][4];
 #pragma unroll
   for (int kk = 0; kk < KT; ++kk) ldmatrix_x4(qa[kk], smem_u32(sQ + (lane & 15) * HDP + kk * 16 + (lane >> 4) * 8));
-  float s[4][4];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-      uint32_t bb[2];
-      ldmatrix_x2(bb, smem_u32(wK + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
-      mma_bf16_16816(s[nt], qa[kk], bb);
-    }
-  }
-  // rows g (s[.][0..1]) and g+8 (s[.][2..3]); keys w0 + nt*8 + 2c + (j&1)
-  float mx[2] = {-1e30f, -1e30f};
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool ok = w0 + nt * 8 + 2 * c + (j & 1) < L;
-      s[nt][j] = ok ? s[nt][j] * scale_log2 : -1e30f;
-      mx[j >> 1] = fmaxf(mx[j >> 1], s[nt][j]);
-    }
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-  }
-  float ls[2] = {0.f, 0.f};
-  uint32_t pa[2][4];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    const float p0 = exp2f(s[nt][0] - mx[0]), p1 = exp2f(s[nt][1] - mx[0]);
-    const float p2 = exp2f(s[nt][2] - mx[1]), p3 = exp2f(s[nt][3] - mx[1]);
-    ls[0] += p0 + p1;
-    ls[1] += p2 + p3;
-    pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
-    pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
-  }
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    ls[r] += __shfl_xor_sync(0xffffffffu, ls[r], 1);
-    ls[r] += __shfl_xor_sync(0xffffffffu, ls[r], 2);
-  }
+  float mx[2] = {-1e30f, -1e30f}, ls[2] = {0.f, 0.f};
   float o[DT][4];
 #pragma unroll
   for (int dt = 0; dt < DT; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+  int it = 0;
+  for (int blk = wg; blk < nblk; blk += wstride, ++it) {
+    const int nxt = blk + wstride;
+    if (nxt < nblk) issue(nxt, (it + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const bf16* wK = ring + (size_t)(it & 1) * (Cf::BLK / 2);
+    const bf16* wV = wK + TKW * HDP;
+    const int k0 = blk * TKW;
+    float sc[4][4];
 #pragma unroll
-  for (int kk = 0; kk < 2; ++kk) {
+    for (int nt = 0; nt < 4; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk) {
+        uint32_t bb[2];
+        ldmatrix_x2(bb, smem_u32(wK + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
+        mma_bf16_16816(sc[nt], qa[kk], bb);
+      }
+    }
+    // rows g (sc[.][0..1]) and g+8 (sc[.][2..3]); keys k0 + nt*8 + 2c + (j&1)
+    float bm[2] = {-1e30f, -1e30f};
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool ok = k0 + nt * 8 + 2 * c + (j & 1) < L;
+        sc[nt][j] = ok ? sc[nt][j] * scale_log2 : -1e30f;
+        bm[j >> 1] = fmaxf(bm[j >> 1], sc[nt][j]);
+      }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 1));
+      bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 2));
+      const float mn = fmaxf(mx[r], bm[r]);
+      corr[r] = exp2f(mx[r] - mn);
+      mx[r] = mn;
+    }
+    float ps[2] = {0.f, 0.f};
+    uint32_t pa[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const float p0 = exp2f(sc[nt][0] - mx[0]), p1 = exp2f(sc[nt][1] - mx[0]);
+      const float p2 = exp2f(sc[nt][2] - mx[1]), p3 = exp2f(sc[nt][3] - mx[1]);
+      ps[0] += p0 + p1;
+      ps[1] += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 1);
+      ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 2);
+      ls[r] = ls[r] * corr[r] + ps[r];
+    }
 #pragma unroll
     for (int dt = 0; dt < DT; ++dt) {
-      uint32_t bb[2];
-      ldmatrix_x2_trans(bb, smem_u32(wV + (kk * 16 + (lane & 15)) * HDP + dt * 8));
-      mma_bf16_16816(o[dt], pa[kk], bb);
+      o[dt][0] *= corr[0];
+      o[dt][1] *= corr[0];
+      o[dt][2] *= corr[1];
+      o[dt][3] *= corr[1];
     }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        uint32_t bb[2];
+        ldmatrix_x2_trans(bb, smem_u32(wV + (kk * 16 + (lane & 15)) * HDP + dt * 8));
+        mma_bf16_16816(o[dt], pa[kk], bb);
+      }
+    }
+    __syncwarp();  // this stage is refilled two blocks later
   }
-  // partial p of head (kvh*G + row): [m, l, o[HD]]
-  const int p = ch * 4 + warp;
+  cp_async_wait<0>();
+  __syncthreads();  // every warp is done with the ring: reuse it for the warp states
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int row = g + 8 * r;
     if (row >= G) continue;
-    float* w = ws + (((size_t)b * H + kvh * G + row) * n_part + p) * (HD + 2);
+    float* w = sW + (warp * 16 + row) * PW;
     if (c == 0) {
       w[0] = mx[r];
       w[1] = ls[r];
@@ -502,6 +553,52 @@ __global__ void __launch_bounds__(128) decode_attn_tc_partial(const bf16* __rest
       w[2 + dt * 8 + 2 * c + 1] = o[dt][2 * r + 1];
     }
   }
+  __syncthreads();
+  // CTA state = merge of the 4 warp states in warp order (warps without blocks: m = -1e30, l = 0)
+  for (int i = tid; i < G * (HD + 2); i += 128) {
+    const int row = i / PW, d = i % PW;
+    float M = -1e30f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sW[(w * 16 + row) * PW]);
+    float acc = 0.f;
+    if (d == 0) {
+      acc = M;
+    } else {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float* pw = sW + (w * 16 + row) * PW;
+        acc += exp2f(pw[0] - M) * pw[d];
+      }
+    }
+    sS[row * PW + d] = acc;
+  }
+  cluster_sync_all();  // CTA states visible cluster-wide
+  if (rank == 0) {
+    const uint32_t base = smem_u32(sS);
+    for (int i = tid; i < G * HD; i += 128) {
+      const int row = i / HD, d = i % HD;
+      float m[DA_CL], l[DA_CL], v[DA_CL];
+#pragma unroll
+      for (int q = 0; q < DA_CL; ++q) {
+        const uint32_t a = base + (uint32_t)(row * PW) * 4u;
+        m[q] = ld_dsmem_f32(a, q);
+        l[q] = ld_dsmem_f32(a + 4u, q);
+        v[q] = ld_dsmem_f32(a + (uint32_t)(2 + d) * 4u, q);
+      }
+      float M = m[0];
+#pragma unroll
+      for (int q = 1; q < DA_CL; ++q) M = fmaxf(M, m[q]);
+      float num = 0.f, den = 0.f;
+#pragma unroll
+      for (int q = 0; q < DA_CL; ++q) {
+        const float f = exp2f(m[q] - M);
+        den += f * l[q];
+        num += f * v[q];
+      }
+      out[(size_t)b * ldo + (size_t)(kvh * G + row) * HD + d] = __float2bfloat16_rn(num / den);
+    }
+  }
+  cluster_sync_all();  // peers keep their shared memory alive until rank 0 has read it
 }
 
 template <int HD>
@@ -527,23 +624,34 @@ __global__ void decode_attn_combine(const float* __restrict__ ws, const DecodeRo
 template <int HD>
 cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
                       int KV, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx, float* ws,
-                      cudaStream_t s) {
+                      int* tickets, cudaStream_t s) {
   if (H / KV > 16) return cudaErrorInvalidValue;
   const float sl2 = LOG2E / sqrtf((float)HD);
   cudaError_t e;
-  if (g_decode_attn_tc) {  // tensor-core version: 128-key chunks, one partial per 32-key warp slice
-    const int n_chunks = (max_ctx + 1 + 4 * TKW - 1) / (4 * TKW);
-    const int n_part = n_chunks * 4;
+  if (g_decode_attn_tc) {  // tensor-core version: one cluster of DA_CL CTAs per (request, KV head)
+    if (H / KV > 16) return cudaErrorInvalidValue;
     static bool set = false;
     if (!set) {
-      cudaFuncSetAttribute(decode_attn_tc_partial<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           DtcCfg<HD>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD>::SMEM);
       set = true;
     }
-    e = launch_k(decode_attn_tc_partial<HD>, dim3(B, KV, n_chunks), dim3(128), DtcCfg<HD>::SMEM, s, true, qkv, ld,
-                 pool, layer, n_pages, H, KV, bt, max_pages, rows, ws, n_part, sl2);
-    if (e != cudaSuccess) return e;
-    e = launch_k(decode_attn_combine<HD>, dim3(B, H), dim3(HD), 0, s, true, ws, rows, out, ldo, H, n_part, TKW);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(DA_CL, KV, B);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = DtcCfg<HD>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = DA_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_use_pdl ? 2 : 1;
+    count_launch();
+    e = cudaLaunchKernelEx(&cfg, decode_attn_tc_kernel<HD>, qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages, rows,
+                           out, ldo, sl2);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
@@ -583,13 +691,13 @@ cudaError_t flash_attn_mma(const bf16* qkv, int ld, bf16* out, int ldo, int S, i
 
 cudaError_t decode_attn(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
                         int KV, int hd, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx,
-                        float* ws, cudaStream_t s) {
+                        float* ws, int* tickets, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   switch (hd) {
-    case 32: return da_launch<32>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, s);
-    case 64: return da_launch<64>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, s);
+    case 32: return da_launch<32>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
+    case 64: return da_launch<64>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
     case 128:
-      return da_launch<128>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, s);
+      return da_launch<128>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -32,6 +32,40 @@ NOVA_DEV float warp_max(float v) {
   return v;
 }
 
+// ------------------------------------------------------------------ canonical RMSNorm statistics
+// Sum of squares of one f32 row of length d (d % 4 == 0), in ONE fixed order shared by every
+// kernel that normalizes LLM rows (rmsnorm_kernel, the norm-on-load GEMV prologue): 128
+// virtual lanes; lane v accumulates float4 chunks v, v+128, v+256, ... in order (chunk value
+// (x0^2 + x1^2) + (x2^2 + x3^2)); the 4 groups of 32 lanes are reduced by the xor butterfly,
+// then combined ((g0 + g1) + g2) + g3.  The caller runs it with 128 consecutive threads
+// (`v` = thread index within them, 4 whole warps) and passes a 4-float smem scratch `red4`
+// private to this row; all loads of a lane are issued before the first FMA (one L2 round
+// trip for d <= 4096).  Returns the full sum to every one of the 128 threads.
+constexpr int NORM_LANES = 128;
+NOVA_DEV float row_sumsq_canonical(const float* __restrict__ xr, int d, int v, float* red4, int bar_id) {
+  const int nch = d >> 2;
+  float s = 0.f;
+  for (int base = 0; base < nch; base += 8 * NORM_LANES) {
+    float4 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = base + v + i * NORM_LANES;
+      x[i] = f < nch ? reinterpret_cast<const float4*>(xr)[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = base + v + i * NORM_LANES;
+      if (f < nch) s += (x[i].x * x[i].x + x[i].y * x[i].y) + (x[i].z * x[i].z + x[i].w * x[i].w);
+    }
+  }
+  s = warp_sum(s);
+  if ((v & 31) == 0) red4[v >> 5] = s;
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+  const float t = ((red4[0] + red4[1]) + red4[2]) + red4[3];
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");  // red4 may be reused afterwards
+  return t;
+}
+
 // ------------------------------------------------------------------ smem / mbarrier
 NOVA_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

@@ -195,13 +195,15 @@ class Engine {
     bf16 *x0, *xb, *qkv, *attn, *act;
     float *hid, *vhid, *xf, *logits;
     int *pos3, *tok;
+    unsigned long long* keys;  // greedy argmax (EPI_F32_ARGMAX), zero between passes
     int* h_pos3;  // pinned
     int* h_tok;   // pinned
     float* h_logits;
   } fw{};
   struct DecWS {
     float *hid, *xf, *logits, *attn_ws, *gemv_ws;
-    int* tickets;
+    int* tickets;               // [0, 4096): gemv_tma row blocks; [4096, 8192): decode attention
+    unsigned long long* keys;  // greedy argmax, zero between passes
     bf16 *xb, *qkv, *attn, *act;
     DecodeRow* rows;
     int* tok;

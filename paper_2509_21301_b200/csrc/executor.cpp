@@ -316,6 +316,8 @@ nova_status Engine::finalize() {
   cudaMemset(d_bt, 0, (size_t)n_slots_total * max_pages_per_req * 4);
   cudaMemset(d_last, 0, (size_t)n_slots_total * 4);
   cudaMemset(dw.tickets, 0, 8192 * 4);
+  cudaMemset(dw.keys, 0, (size_t)cfg.max_decode_batch * 8);
+  cudaMemset(fw.keys, 0, 16 * 8);
   ktimer[0].init(512);
   ktimer[1].init(512);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(NOVA_E_CUDA, "finalize sync");

@@ -46,6 +46,8 @@ enum Epi {
   EPI_BF16_SILUMUL = 3, // W rows interleaved gate/up in blocks of 16; out[:, N/2] = silu(g) * u
   EPI_F32_RESID = 4,    // out f32 += result (residual add)
   EPI_F32_STORE = 5,    // out f32 = result
+  EPI_QKV_ROPE_KV = 6,  // decode qkv: bias + M-RoPE on q/k; q -> out bf16, k/v -> paged KV cache (GemvAux)
+  EPI_F32_ARGMAX = 7,   // logits f32 = result, and greedy argmax into GemvAux::keys (64-bit atomicMax)
 };
 
 // tcgen05/TMEM/TMA persistent GEMM. A [M][K] (lda), W [N][K] (ldw), C [M][N] (ldc elems).
@@ -85,11 +87,33 @@ struct DecodeRow {
   int pos;    // M-RoPE position (t = h = w for generated text)
   int pad;
 };
+// Extra operands of the fused decode GEMV modes (gemv_ex).
+struct GemvAux {
+  const bf16* gamma = nullptr;  // x modes 2/3: RMSNorm gain, x = f32 residual rows
+  float eps = 0.f;
+  int H = 0, KV = 0, hd = 0;    // EPI_QKV_ROPE_KV
+  float log2_theta = 0.f;
+  const DecodeRow* rows = nullptr;
+  bf16* pool = nullptr;
+  int layer = 0, n_pages = 0;
+  const int* bt = nullptr;
+  int max_pages = 0;
+  unsigned long long* keys = nullptr;  // EPI_F32_ARGMAX: [B] packed (ordered logit, ~index), zero on entry
+};
+// x modes: 0 bf16, 1 f32 (hi/lo split), 2 f32 residual + RMSNorm on load -> bf16, 3 same -> hi/lo
+cudaError_t gemv_ex(const void* X, int xmode, int ldx, const bf16* W, int N, int K, void* Y, int ldy,
+                    const bf16* bias, int B, int epi, const GemvAux& aux, cudaStream_t s);
+// keys[r] -> out_tok[r], last_tok[rows[r].slot] (or last_tok[single_slot]); keys reset to 0
+cudaError_t argmax_finalize(unsigned long long* keys, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
+                            int single_slot, cudaStream_t s);
+
 extern bool g_decode_attn_tc;  // tensor-core decode attention (default) vs the CUDA-core version
-// ws: B * H * (ceil((max_ctx+1)/128)*4) * (hd+2) floats
+// ws: B * H * (ceil((max_ctx+1)/128)*4) * (hd+2) floats; tickets: B * KV ints, zero on entry
+// (restored to zero by the kernel).  Tensor-core path: one launch (chunk partials + last-CTA
+// fixed-order merge); CUDA-core path: partial + combine kernels.
 cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf16* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int* block_tables, int max_pages, const DecodeRow* rows, int B,
-                        int max_ctx, float* ws, cudaStream_t s);
+                        int max_ctx, float* ws, int* tickets, cudaStream_t s);
 
 cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d,
                       float eps, cudaStream_t s);

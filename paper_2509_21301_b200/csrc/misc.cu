@@ -44,25 +44,24 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf1
   }
 }
 
-__global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm, void* __restrict__ y,
-                               int y_f32, int ldy, int M, int d, float eps) {
+// RMSNorm: one 128-thread group per row (4 rows per 512-thread CTA), canonical statistics
+// order (common.cuh row_sumsq_canonical); y = (x * rstd) * gamma.
+__global__ void __launch_bounds__(512) rmsnorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm,
+                                                      void* __restrict__ y, int y_f32, int ldy, int M, int d, float eps) {
+  __shared__ float red[4][4];
   pdl_launch_dependents();
   pdl_wait();
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= M) return;
+  const int grp = threadIdx.x >> 7, v = threadIdx.x & 127;
+  const int row = blockIdx.x * 4 + grp;
+  if (row >= M) return;  // whole 128-thread group: named barrier grp + 1 stays consistent
   const float* xr = x + (size_t)row * ldx;
-  float q = 0.f;
-  for (int i = lane * 4; i < d; i += 128) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    q += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
-  }
-  const float rs = rsqrtf(warp_sum(q) / d + eps);
-  for (int i = lane * 4; i < d; i += 128) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
+  const float rs = rsqrtf(row_sumsq_canonical(xr, d, v, red[grp], grp + 1) / d + eps);
+  for (int f = v; f < (d >> 2); f += NORM_LANES) {
+    const int i = f * 4;
+    float4 xv = *reinterpret_cast<const float4*>(xr + i);
     const float2 g01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i));
     const float2 g23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i + 2));
-    const float o0 = v.x * rs * g01.x, o1 = v.y * rs * g01.y, o2 = v.z * rs * g23.x, o3 = v.w * rs * g23.y;
+    const float o0 = xv.x * rs * g01.x, o1 = xv.y * rs * g01.y, o2 = xv.z * rs * g23.x, o3 = xv.w * rs * g23.y;
     if (y_f32) {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + (size_t)row * ldy + i) = make_float4(o0, o1, o2, o3);
     } else {
@@ -231,9 +230,31 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int ldl, int V, 
   }
 }
 
+__global__ void argmax_finalize_kernel(unsigned long long* __restrict__ keys, int n, int* __restrict__ out_tok,
+                                       const DecodeRow* __restrict__ rows, int* __restrict__ last_tok,
+                                       int single_slot) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int r = threadIdx.x;
+  if (r >= n) return;
+  const int tok = (int)(0xFFFFFFFFu - (uint32_t)(keys[r] & 0xFFFFFFFFull));
+  keys[r] = 0ull;
+  out_tok[r] = tok;
+  if (rows) last_tok[rows[r].slot] = tok;
+  else if (single_slot >= 0 && last_tok) last_tok[single_slot] = tok;
+}
+
 }  // namespace
 
 std::atomic<unsigned long long> g_kernel_launches{0};
+
+cudaError_t argmax_finalize(unsigned long long* keys, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
+                            int single_slot, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 1024) return cudaErrorInvalidValue;
+  return launch_k(argmax_finalize_kernel, dim3(1), dim3(32 * ((n + 31) / 32)), 0, s, true, keys, n, out_tok, rows,
+                  last_tok, single_slot);
+}
 
 cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d, float eps,
                       cudaStream_t s) {
@@ -245,7 +266,7 @@ cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, 
                     cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
-  return launch_k(rmsnorm_kernel, dim3((M + 7) / 8), dim3(256), 0, s, true, x, ldx, g, y, y_f32, ldy, M, d, eps);
+  return launch_k(rmsnorm_kernel, dim3((M + 3) / 4), dim3(512), 0, s, true, x, ldx, g, y, y_f32, ldy, M, d, eps);
 }
 cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int merge, bf16* X0, cudaStream_t s) {
   const int N = (H / P) * (W / P);

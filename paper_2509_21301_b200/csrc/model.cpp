@@ -127,6 +127,7 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   f.logits = (float*)take(V * 4);
   f.pos3 = (int*)take(3 * S * 4);
   f.tok = (int*)take(16 * 4);
+  f.keys = (unsigned long long*)take(16 * 8);
   w.hid = (float*)take(B * D * 4);
   w.xf = (float*)take(B * D * 4);
   w.xb = (bf16*)take(B * std::max(std::max(D, F), Hhd) * 2);
@@ -135,12 +136,13 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   w.act = (bf16*)take(B * F * 2);
   w.logits = (float*)take(B * V * 4);
   const size_t nch = (max_ctx + 255) / 256;
-  const size_t nparts = std::max(nch, (size_t)(max_ctx + 127) / 128 * 4);  // decode attention partials per head
+  const size_t nparts = std::max(nch, (size_t)(max_ctx + 127) / 128 * 4);  // >= 128-key chunks of the fused kernel  // decode attention partials per head
   w.attn_ws = (float*)take(B * m.llm_heads * nparts * (m.head_dim + 2) * 4);
   w.gemv_ws = (float*)take((size_t)16 * B * std::max(std::max(D, F), (size_t)d.llm_qkv_n) * 4);
   w.tickets = (int*)take(8192 * 4);
   w.rows = (DecodeRow*)take(B * sizeof(DecodeRow));
   w.tok = (int*)take(B * 4);
+  w.keys = (unsigned long long*)take(B * 8);
   const size_t pix = (size_t)m.in_ch * N * m.patch * m.patch;
   bf16* d_pix = (bf16*)take(n_slots * pix * 2);
   int* d_prompt = (int*)take((size_t)n_slots * c.max_prompt * 4);

@@ -34,9 +34,34 @@ int nova_op_flash_attn_mma(const void* qkv, int ld, void* out, int ldo, int Sq, 
 }
 int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int32_t* bt, int max_pages, const nova_decode_row* rows, int B,
-                        int max_ctx, float* ws, void* stream) {
+                        int max_ctx, float* ws, int32_t* tickets, void* stream) {
   return st(decode_attn((const bf16*)qkv, ld, (bf16*)out, ldo, (const bf16*)kv_pool, layer, n_pages, H, KV, hd, bt,
-                        max_pages, (const DecodeRow*)rows, B, max_ctx, ws, S(stream)));
+                        max_pages, (const DecodeRow*)rows, B, max_ctx, ws, tickets, S(stream)));
+}
+int nova_op_gemv_fused(const void* X, int x_mode, int ldx, const void* W, int N, int K, void* Y, int ldy,
+                       const void* bias, int B, int epi, const void* gamma, float eps, int H, int KV, int hd,
+                       float theta, const nova_decode_row* rows, void* kv_pool, int layer, int n_pages,
+                       const int32_t* bt, int max_pages, uint64_t* keys, void* stream) {
+  GemvAux a;
+  a.gamma = (const bf16*)gamma;
+  a.eps = eps;
+  a.H = H;
+  a.KV = KV;
+  a.hd = hd;
+  a.log2_theta = theta > 0.f ? log2f(theta) : 0.f;
+  a.rows = (const DecodeRow*)rows;
+  a.pool = (bf16*)kv_pool;
+  a.layer = layer;
+  a.n_pages = n_pages;
+  a.bt = bt;
+  a.max_pages = max_pages;
+  a.keys = (unsigned long long*)keys;
+  return st(gemv_ex(X, x_mode, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, a, S(stream)));
+}
+int nova_op_argmax_finalize(uint64_t* keys, int n, int32_t* out_tok, const nova_decode_row* rows, int32_t* last_tok,
+                            int single_slot, void* stream) {
+  return st(argmax_finalize((unsigned long long*)keys, n, out_tok, (const DecodeRow*)rows, last_tok, single_slot,
+                            S(stream)));
 }
 int nova_op_layernorm(const float* x, int ldx, const void* g, const void* b, void* y, int ldy, int M, int d, float eps,
                       void* stream) {

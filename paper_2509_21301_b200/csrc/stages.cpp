@@ -62,21 +62,29 @@ static cudaError_t t_gemm(Engine* E, int role, int cls, const bf16* A, int lda, 
   return cudaSuccess;
 }
 
-static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xf32, int ldx, const bf16* W, int N, int K, void* Y,
-                          int ldy, const bf16* bias, int B, int epi, cudaStream_t s) {
+// Decode linear: x_mode 0 = bf16 x, 2 = f32 residual rows with the RMSNorm applied on load
+// (gamma in aux), 3 = same in f32 (lm_head).  Algorithmic bytes = weights + x + y (+ KV append).
+static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xmode, int ldx, const bf16* W, int N, int K, void* Y,
+                          int ldy, const bf16* bias, int B, int epi, const GemvAux& aux, cudaStream_t s) {
   const int nout = epi == EPI_BF16_SILUMUL ? N / 2 : N;
-  const int ysz = epi == EPI_F32_RESID ? 8 : (epi == EPI_F32_STORE ? 4 : 2);
-  const double bytes = (double)N * K * 2 + (double)B * K * (xf32 ? 4 : 2) + (double)B * nout * ysz;
+  const int ysz = epi == EPI_F32_RESID ? 8 : ((epi == EPI_F32_STORE || epi == EPI_F32_ARGMAX) ? 4 : 2);
+  const double bytes = (double)N * K * 2 + (double)B * K * (xmode ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  // TMA-streamed GEMV where it measured faster (large N, no split-K: gate|up, 99.6% vs 93% of
-  // HBM in scripts/kbench.py); the register-streaming GEMV for the small-N shapes
-  if (!xf32 && g_use_tma_gemv && gemv_tma_splits(N, K) == 1)
-    CUDA_TRY(gemv_tma(reinterpret_cast<const bf16*>(X), ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws,
-                      E->dw.tickets, s));
-  else
-    CUDA_TRY(gemv(X, xf32, ldx, W, N, K, Y, ldy, bias, B, epi, s));
+  CUDA_TRY(gemv_ex(X, xmode, ldx, W, N, K, Y, ldy, bias, B, epi, aux, s));
   E->ktimer[1].end(i, cls, bytes, s);
+  return cudaSuccess;
+}
+
+// TMA-streamed decode linear (bf16 x): gate|up, where it streams at ~99% of HBM (scripts/kbench.py)
+static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, int B,
+                              int epi, cudaStream_t s) {
+  const int nout = epi == EPI_BF16_SILUMUL ? N / 2 : N;
+  const double bytes = (double)N * K * 2 + (double)B * K * 2 + (double)B * nout * 2;
+  E->pass_work[1] += bytes;
+  const int i = E->ktimer[1].begin(s);
+  CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, nullptr, B, epi, E->dw.gemv_ws, E->dw.tickets, s));
+  E->ktimer[1].end(i, NOVA_K_DEC_GEMV, bytes, s);
   return cudaSuccess;
 }
 
@@ -180,11 +188,17 @@ cudaError_t Engine::run_prefill(Request* r, cudaStream_t s, int sms) {
     CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.act, F, L.down_w, F, fw.hid, D, nullptr, S, D, F, EPI_F32_RESID, sms,
                     s));
   }
-  // token 0: final RMSNorm (f32 out) of the last row -> lm_head GEMV (f32 logits) -> argmax
-  CUDA_TRY(rmsnorm(fw.hid + (size_t)(S - 1) * D, D, W.final_norm, fw.xf, 1, D, 1, D, m.rms_eps, s));
+  // token 0: final RMSNorm of the last row (applied on load, f32) -> lm_head -> fused greedy argmax
   pass_work[0] += 2.0 * D * m.vocab;
-  CUDA_TRY(gemv(fw.xf, 1, D, W.lm_head, m.vocab, D, fw.logits, m.vocab, nullptr, 1, EPI_F32_STORE, s));
-  CUDA_TRY(argmax_rows(fw.logits, m.vocab, m.vocab, 1, fw.tok, nullptr, d_last, r->slot, s));
+  {
+    GemvAux ax;
+    ax.gamma = W.final_norm;
+    ax.eps = m.rms_eps;
+    ax.keys = fw.keys;
+    CUDA_TRY(gemv_ex(fw.hid + (size_t)(S - 1) * D, 3, D, W.lm_head, m.vocab, D, fw.logits, m.vocab, nullptr, 1,
+                     EPI_F32_ARGMAX, ax, s));
+  }
+  CUDA_TRY(argmax_finalize(fw.keys, 1, fw.tok, nullptr, d_last, r->slot, s));
   CUDA_TRY(cudaMemcpyAsync(fw.h_tok, fw.tok, sizeof(int), cudaMemcpyDeviceToHost, s));
   if (cfg.debug_keep_logits)
     CUDA_TRY(cudaMemcpyAsync(fw.h_logits, fw.logits, (size_t)m.vocab * 4, cudaMemcpyDeviceToHost, s));
@@ -215,29 +229,45 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
     }
   CUDA_TRY(embed(W.embed, D, nullptr, dw.rows, d_last, dw.hid, D, B, s));
   bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
+  GemvAux plain;
+  GemvAux qa;  // RMSNorm(ln1) on load; bias + RoPE + KV append epilogue
+  qa.eps = m.rms_eps;
+  qa.H = H;
+  qa.KV = KV;
+  qa.hd = hd;
+  qa.log2_theta = log2f(m.llm_theta);
+  qa.rows = dw.rows;
+  qa.pool = pool;
+  qa.n_pages = cfg.kv_pages;
+  qa.bt = d_bt;
+  qa.max_pages = max_pages_per_req;
   for (int l = 0; l < m.llm_layers; ++l) {
     const LlmLayerW& L = W.llm[l];
-    CUDA_TRY(rmsnorm(dw.hid, D, L.ln1, dw.xb, 0, D, B, D, m.rms_eps, s));
-    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.xb, 0, D, L.qkv_w, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_BF16, s));
-    CUDA_TRY(llm_rope_kv(dw.qkv, ldq, B, H, KV, hd, m.llm_theta, m.mrope_section[0], m.mrope_section[1], nullptr, 0,
-                         dw.rows, 0, 0, pool, l, cfg.kv_pages, d_bt, max_pages_per_req, s));
+    qa.gamma = L.ln1;
+    qa.layer = l;
+    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.hid, 2, D, L.qkv_w, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV, qa,
+                    s));
     {
       pass_work[1] += kv_bytes_layer;
       const int i = ktimer[1].begin(s);
       CUDA_TRY(decode_attn(dw.qkv, ldq, dw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
-                           dw.rows, B, max_ctx, dw.attn_ws, s));
+                           dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
       ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
     }
     CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.attn, 0, H * hd, L.o_w, D, H * hd, dw.hid, D, nullptr, B, EPI_F32_RESID,
-                    s));
+                    plain, s));
+    // ln2 -> bf16 rows (one small kernel) -> TMA-streamed gate|up GEMV with the SiLU*up epilogue
     CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
-    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.xb, 0, D, L.gu_w, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL, s));
-    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.act, 0, F, L.down_w, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, s));
+    CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.gu_w, 2 * F, D, dw.act, F, B, EPI_BF16_SILUMUL, s));
+    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.act, 0, F, L.down_w, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, plain,
+                    s));
   }
+  GemvAux la;  // final RMSNorm (f32 rows) -> lm_head (hi/lo f32 input) -> fused greedy argmax
+  la.keys = dw.keys;
   CUDA_TRY(rmsnorm(dw.hid, D, W.final_norm, dw.xf, 1, D, B, D, m.rms_eps, s));
   CUDA_TRY(t_gemv(this, NOVA_K_LM_HEAD, dw.xf, 1, D, W.lm_head, m.vocab, D, dw.logits, m.vocab, nullptr, B,
-                  EPI_F32_STORE, s));
-  CUDA_TRY(argmax_rows(dw.logits, m.vocab, m.vocab, B, dw.tok, dw.rows, d_last, -1, s));
+                  EPI_F32_ARGMAX, la, s));
+  CUDA_TRY(argmax_finalize(dw.keys, B, dw.tok, dw.rows, d_last, -1, s));
   CUDA_TRY(cudaMemcpyAsync(dw.h_tok, dw.tok, B * sizeof(int), cudaMemcpyDeviceToHost, s));
   if (cfg.debug_keep_logits)
     CUDA_TRY(cudaMemcpyAsync(dw.h_logits, dw.logits, (size_t)B * m.vocab * 4, cudaMemcpyDeviceToHost, s));

@@ -9,7 +9,9 @@ import torch
 
 from ._lib import lib, check
 
-EPI_BF16, EPI_BF16_QGELU, EPI_BF16_GELU, EPI_BF16_SILUMUL, EPI_F32_RESID, EPI_F32_STORE = range(6)
+(EPI_BF16, EPI_BF16_QGELU, EPI_BF16_GELU, EPI_BF16_SILUMUL, EPI_F32_RESID, EPI_F32_STORE, EPI_QKV_ROPE_KV,
+ EPI_F32_ARGMAX) = range(8)
+XM_BF16, XM_F32, XM_NORM_BF16, XM_NORM_F32 = range(4)
 
 
 def _p(t):
@@ -55,10 +57,28 @@ def nova_op_flash_attn_mma(qkv, out, S, H, KV, hd, causal, stream=None):
 
 
 def nova_op_decode_attn(qkv, out, kv_pool, layer, n_pages, H, KV, hd, block_tables, rows, B, max_ctx, ws,
-                        stream=None):
+                        tickets=None, stream=None):
+    if tickets is None:
+        tickets = torch.zeros(B * KV, dtype=torch.int32, device=qkv.device)
     check(lib().nova_op_decode_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), _p(kv_pool), layer, n_pages,
                                     H, KV, hd, _p(block_tables), block_tables.shape[1], _p(rows), B, max_ctx, _p(ws),
-                                    _s(stream)), "decode_attn")
+                                    _p(tickets), _s(stream)), "decode_attn")
+
+
+def nova_op_gemv_fused(X, x_mode, W, Y, bias, N, K, B, epi, gamma=None, eps=0.0, H=0, KV=0, hd=0, theta=0.0,
+                       rows=None, kv_pool=None, layer=0, n_pages=0, block_tables=None, keys=None, ldx=None, ldy=None,
+                       stream=None):
+    import ctypes as C
+    check(lib().nova_op_gemv_fused(_p(X), x_mode, ldx or X.stride(0), _p(W), N, K, _p(Y), ldy or Y.stride(0),
+                                   _p(bias), B, epi, _p(gamma), C.c_float(eps), H, KV, hd, C.c_float(theta), _p(rows),
+                                   _p(kv_pool), layer, n_pages, _p(block_tables),
+                                   0 if block_tables is None else block_tables.shape[1], _p(keys), _s(stream)),
+          "gemv_fused")
+
+
+def nova_op_argmax_finalize(keys, n, out_tok, rows=None, last_tok=None, single_slot=-1, stream=None):
+    check(lib().nova_op_argmax_finalize(_p(keys), n, _p(out_tok), _p(rows), _p(last_tok), single_slot, _s(stream)),
+          "argmax_finalize")
 
 
 def nova_op_layernorm(x, gamma, beta, y, M, d, eps, stream=None):

@@ -23,16 +23,24 @@ HBM, TFL = PK["hbm_gbs"], PK["bf16_tflops"]
 
 
 def timeit(fn, iters, rot):
+    """ms per call: `iters` back-to-back calls captured in one CUDA graph (no Python/launch
+    overhead between kernels, PDL edges kept), replayed after a warm-up, CUDA events."""
     for i in range(3):
         fn(i % rot)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(iters):
+            fn(i % rot)
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(iters):
-        fn(i % rot)
+    for _ in range(3):
+        g.replay()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters
+    return e0.elapsed_time(e1) / (3 * iters)
 
 
 def rnd(shape, dtype=torch.bfloat16, scale=1.0):
@@ -57,6 +65,12 @@ def bench_gemv(iters):
             variants = [("gemv", lambda i: O.nova_op_gemv(X, Ws[i], Y, None, N, K, B, epi))]
             if not xf:
                 variants.append(("gemv_tma", lambda i: O.nova_op_gemv_tma(X, Ws[i], Y, None, N, K, B, epi)))
+            if name in ("qkv", "gate_up", "lm_head"):   # RMSNorm applied on load from the f32 residual rows
+                Xf = torch.randn(B, K, device="cuda")
+                gam = torch.ones(K, device="cuda", dtype=torch.bfloat16)
+                xm = O.XM_NORM_F32 if xf else O.XM_NORM_BF16
+                variants.append(("gemv_norm", lambda i: O.nova_op_gemv_fused(Xf, xm, Ws[i], Y, None, N, K, B, epi,
+                                                                             gamma=gam, eps=1e-6)))
             for kname, fn in variants:
                 ms = timeit(fn, iters, rot)
                 gbs = byt / ms / 1e6
@@ -101,7 +115,7 @@ def bench_attn(iters):
 
 def bench_dattn(iters):
     H, KV, hd, L = 28, 4, 128, 1
-    for B, ctx in [(1, 1334), (4, 1334), (8, 1334), (16, 2047)]:
+    for B, ctx in [(1, 1334), (2, 1334), (4, 1334), (8, 1334), (16, 1334), (16, 2047)]:
         pages = (ctx + 64) // 64
         n_pages = B * pages
         pool = rnd((L, n_pages, 2, KV, 64, hd))
@@ -110,7 +124,8 @@ def bench_dattn(iters):
         qkv = rnd((B, (H + 2 * KV) * hd))
         out = torch.empty(B, H * hd, device="cuda", dtype=torch.bfloat16)
         ws = torch.empty(B * H * ((ctx + 128) // 128 + 1) * 4 * (hd + 2), device="cuda")
-        ms = timeit(lambda i: O.nova_op_decode_attn(qkv, out, pool, 0, n_pages, H, KV, hd, bt, rows, B, ctx, ws),
+        tk = torch.zeros(B * KV, dtype=torch.int32, device="cuda")
+        ms = timeit(lambda i: O.nova_op_decode_attn(qkv, out, pool, 0, n_pages, H, KV, hd, bt, rows, B, ctx, ws, tk),
                     iters, 1)
         byt = B * (ctx + 1) * 2 * KV * hd * 2
         print(json.dumps({"kernel": "decode_attn", "B": B, "ctx": ctx, "us": round(ms * 1e3, 2),
