@@ -56,11 +56,13 @@ int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K,
 int nova_op_gemv_tma(const void* X, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias, int B,
                      int epi, float* ws, int32_t* tickets, void* stream);
 
-/* Flash attention (a5 ViT: causal = 0, KV = H; a6 prefill: causal = 1, GQA).
- * qkv [S][(H + 2 KV) hd] bf16 (ld): q heads, then k heads, then v heads; out
- * [S][H hd] bf16 (ldo); scale hd^-1/2; hd in {16, 32, 64, 80, 128}. */
+/* Flash attention (a5 ViT: causal = 0, KV = H; a6 prefill: causal = 1, GQA; PAPER.md
+ * Table resource_stage P:139-140 "Attention").  qkv [S][(H + 2 KV) hd] bf16 (ld): q heads,
+ * then k heads, then v heads; out [S][H hd] bf16 (ldo); scale hd^-1/2; hd in {16, 32, 64,
+ * 80, 128}.  max_ctas = SM budget of the caller's partition (0 = whole GPU); the output is
+ * bitwise independent of it. */
 int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int S, int H, int KV, int hd, int causal,
-                       void* stream);
+                       int max_ctas, void* stream);
 
 /* Same contract, forced onto the legacy warp-level mma.sync kernel (the measured
  * baseline the tcgen05 path is compared against); hd in {16, 32, 64, 80, 128}.

@@ -22,7 +22,7 @@ OPS_SIGNATURES = {
     "nova_op_gemm": [P, I, P, I, P, I, P, I, I, I, I, I, P],
     "nova_op_gemv": [P, I, I, P, I, I, P, I, P, I, I, P],
     "nova_op_gemv_tma": [P, I, P, I, I, P, I, P, I, I, P, P, P],
-    "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, P],
+    "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, I, P],
     "nova_op_flash_attn_mma": [P, I, P, I, I, I, I, I, I, P],
     "nova_op_decode_attn": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P, P],
     "nova_op_gemv_fused": [P, I, I, P, I, I, P, I, P, I, I, P, F, I, I, I, F, P, P, I, I, P, I, P, P],

@@ -14,6 +14,8 @@
 // Operands: Q, K K-major SW128 (64-column chunks of the fused qkv buffer, straight from
 // TMA); V is used as an MN-major B operand (no transpose pass); P K-major SW128.
 // Deterministic: per (row, head) the key order and every reduction are fixed.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -511,6 +513,384 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// v3: one CTA per SM, TWO 128-row Q tiles (A, B) of the same head sharing every K/V tile, the
+// FA4 ping-pong: while softmax warpgroup A turns S_A(j) into P_A(j), the tensor core runs
+// PV_B(j-1) / S_B(j), and vice versa, so the MUFU (exp) and the tensor pipe stay busy together.
+//   w0: TMA (Q_A, Q_B once; K_j, V_j through a 2-stage ring)     w1: MMA issuer (one thread)
+//   w2: TMEM alloc                                                w4-7 / w8-11: softmax A / B
+// TMEM (512 cols): S_A | S_B | O_A | O_B.  P_X is written as packed bf16 over S_X (TS MMA).
+// The softmax warpgroups take 224 registers (setmaxnreg; the producer group gives its share
+// back) so the whole 128-column S row sits in registers: ONE TMEM read per tile and no
+// second pass.  Per tile: 4 tcgen05.ld issued back to back, one wait.
+// MMA issue order (in-order tensor pipe):  S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) ...
+template <int HD>
+struct Ft3Cfg {
+  static constexpr int NCH = (HD + CHUNK - 1) / CHUNK;
+  static constexpr int TILE_BYTES = NCH * FBN * CHUNK * 2;
+  static constexpr int QA_OFF = 0, QB_OFF = TILE_BYTES;
+  static constexpr int K_OFF = 2 * TILE_BYTES;   // 2 stages
+  static constexpr int V_OFF = 4 * TILE_BYTES;   // 2 stages
+  static constexpr int BAR_OFF = 6 * TILE_BYTES;
+  static constexpr int SMEM = 1024 + BAR_OFF + 256;
+};
+
+template <int N>
+NOVA_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {  // no wait: pair with tmem_ld_wait32
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// tcgen05.wait::ld that the compiler must order before any use of r[0..31]
+NOVA_DEV void tmem_ld_wait32(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+// Work decomposition of the persistent v3 kernel, from the SHAPE only (never the grid): units
+// are (head, Q-tile pair) in head-major order; the first `full` = floor(units / 148) * 148
+// take every key tile; the remaining `rem` units are each cut into KC key-range chunks
+// (KC = 148 / rem, >= 2 tiles per chunk) whose (m, l, O) partials are merged in chunk order by
+// the last chunk to finish.  So the numerics are identical for any SM budget, and on the full
+// GPU the tail wave is ~148 short chunks instead of `rem` full-length units.
+struct Fmha3Plan {
+  int n_q2, n_tiles, units, full, rem, KC, total;
+  __host__ __device__ Fmha3Plan(int S, int H, int split = 1) {
+    n_q2 = (S + 2 * FBM - 1) / (2 * FBM);
+    n_tiles = (S + FBN - 1) / FBN;
+    units = n_q2 * H;
+    full = (units / 148) * 148;
+    rem = units - full;
+    KC = 1;
+    if (rem > 0) {
+      KC = 148 / rem;
+      if (KC > n_tiles / 2) KC = n_tiles / 2;
+      if (KC > 16) KC = 16;
+      if (KC < 1) KC = 1;
+    }
+    if (KC == 1 || !split) {
+      KC = 1;
+      full = units;
+      rem = 0;
+    }
+    total = full + rem * KC;
+  }
+  // unit -> (head, q pair, key tiles [t0, t1), split slot or -1, chunk index)
+  __host__ __device__ void decode(int u, int& h, int& pr, int& t0, int& t1, int& slot, int& ch) const {
+    int base = u;
+    ch = 0;
+    slot = -1;
+    if (u >= full) {
+      base = full + (u - full) / KC;
+      ch = (u - full) % KC;
+      slot = u - full;
+    }
+    h = base / n_q2;
+    pr = base % n_q2;
+    t0 = slot < 0 ? 0 : (ch * n_tiles) / KC;
+    t1 = slot < 0 ? n_tiles : ((ch + 1) * n_tiles) / KC;
+  }
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    fmha3_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, int ldo, int S, int H, int KV,
+                 float scale_log2, float* __restrict__ ws, int* __restrict__ tickets, int split) {
+  using C = Ft3Cfg<HD>;
+  constexpr int NCH = C::NCH;
+  constexpr int PW = HD + 4;  // split partial row: m, l, -, -, O[HD] (16-byte aligned rows)
+  constexpr uint32_t IDESC_S = umma_idesc_bf16(FBM, FBN);
+  constexpr uint32_t IDESC_O = umma_idesc_bf16(FBM, HD) | (1u << 16);  // B (V) MN-major
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2] (A, B)
+  uint64_t* p_full = bars + 11;  // [2] (A, B), 128 arrivals
+  uint64_t* o_done = bars + 13;
+  uint64_t* turn = bars + 14;    // [2] MUFU ping-pong token: A's exps, then B's, ... (128 arrivals)
+  uint64_t* q_empty = bars + 16; // Q tiles and O of the unit consumed (256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  int* s_last = reinterpret_cast<int*>(bars + 18);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Fmha3Plan plan(S, H, split);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm);
+    for (int i = 0; i < 17; ++i) mbar_init(&bars[i], (i == 11 || i == 12 || i == 14 || i == 15) ? 128 : (i == 16 ? 256 : 1));
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {  // ---------------- TMA producer
+      int it = 0, nu = 0;
+      for (int u = blockIdx.x; u < plan.total; u += gridDim.x, ++nu) {
+        int h, pr, t0, t1, slot, ch;
+        plan.decode(u, h, pr, t0, t1, slot, ch);
+        const int kvh = h / (H / KV), q0 = pr * 2 * FBM;
+        const int qcol = h * HD, kcol = (H + kvh) * HD, vcol = (H + KV + kvh) * HD;
+        mbar_wait(q_empty, (nu & 1) ^ 1);  // previous unit's MMAs and epilogue are done with Q / O
+        mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load_2d(smem + C::QA_OFF + c * FBN * 128, &tm, q_full, qcol + c * CHUNK, q0);
+          tma_load_2d(smem + C::QB_OFF + c * FBN * 128, &tm, q_full, qcol + c * CHUNK, q0 + FBM);
+        }
+        for (int j = t0; j < t1; ++j, ++it) {
+          const int st = it & 1;
+          const uint32_t ph = ((it >> 1) & 1) ^ 1;
+          mbar_wait(&k_empty[st], ph);
+          mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + c * FBN * 128, &tm, &k_full[st], kcol + c * CHUNK,
+                        j * FBN);
+          mbar_wait(&v_empty[st], ph);
+          mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + c * FBN * 128, &tm, &v_full[st], vcol + c * CHUNK,
+                        j * FBN);
+        }
+      }
+    } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer
+      const uint32_t tS[2] = {tbase, tbase + FBN};
+      const uint32_t tO[2] = {tbase + 2 * FBN, tbase + 3 * FBN};
+      const uint32_t qa[2] = {smem_u32(smem + C::QA_OFF), smem_u32(smem + C::QB_OFF)};
+      auto issue_s = [&](int x, int itx) {
+        const uint32_t kb = smem_u32(smem + C::K_OFF + (itx & 1) * C::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k * 16 / CHUNK) * FBN * 128 + (k * 16 % CHUNK) * 2;
+          umma_bf16_ss(tS[x], umma_desc_sw128(qa[x] + off), umma_desc_sw128(kb + off), IDESC_S, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int itx, bool first) {
+        const uint32_t vb = smem_u32(smem + C::V_OFF + (itx & 1) * C::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < FBN / 16; ++k)  // P: 16 keys = 8 packed TMEM columns per step
+          umma_bf16_ts(tO[x], tS[x] + k * 8, umma_desc_sw128_mn(vb + k * 16 * 128, FBN * 128), IDESC_O,
+                       (!first || k > 0) ? 1u : 0u);
+      };
+      int it = 0, nu = 0;
+      for (int u = blockIdx.x; u < plan.total; u += gridDim.x, ++nu) {
+        int h, pr, t0, t1, slot, ch;
+        plan.decode(u, h, pr, t0, t1, slot, ch);
+        const int n = t1 - t0;
+        mbar_wait(q_full, nu & 1);
+        mbar_wait(&k_full[it & 1], (it >> 1) & 1);
+        tc_fence_after();
+        issue_s(0, it);
+        issue_s(1, it);
+        umma_commit(&k_empty[it & 1]);
+        for (int j = 0; j < n; ++j, ++it) {
+          const int st = it & 1;
+          const uint32_t ph = (it >> 1) & 1;
+          const bool more = j + 1 < n;
+          mbar_wait(&v_full[st], ph);
+          mbar_wait(&p_full[0], it & 1);
+          tc_fence_after();
+          issue_pv(0, it, j == 0);
+          if (more) {
+            mbar_wait(&k_full[st ^ 1], ((it + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_s(0, it + 1);
+          }
+          mbar_wait(&p_full[1], it & 1);
+          tc_fence_after();
+          issue_pv(1, it, j == 0);
+          umma_commit(&v_empty[st]);
+          if (more) {
+            issue_s(1, it + 1);
+            umma_commit(&k_empty[st ^ 1]);
+          }
+        }
+        umma_commit(o_done);
+      }
+    }
+  } else {  // ---------------- softmax warpgroups: x = 0 (warps 4-7, tile A), 1 (warps 8-11, tile B)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    const int x = (warp - 4) >> 2;
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tbase + x * FBN + lane_off, tO = tbase + (2 + x) * FBN + lane_off;
+    int it = 0, nu = 0;
+    for (int u = blockIdx.x; u < plan.total; u += gridDim.x, ++nu) {
+      int h, pr, t0, t1, slot, ch;
+      plan.decode(u, h, pr, t0, t1, slot, ch);
+      const int qrow = pr * 2 * FBM + x * FBM + row;
+      float m = -1e30f, l = 0.f;
+      for (int j = t0; j < t1; ++j, ++it) {
+        mbar_wait(&s_full[x], it & 1);
+        tc_fence_after();
+        uint32_t sv[FBN];
+#pragma unroll
+        for (int c = 0; c < FBN / 32; ++c) tmem_ld32_nw<32>(tS + c * 32, sv + c * 32);
+#pragma unroll
+        for (int c = 0; c < FBN / 32; ++c) tmem_ld_wait32(sv + c * 32);
+        const int k0 = j * FBN;
+        if (k0 + FBN > S) {  // keys beyond S (TMA zero-filled rows) must not contribute
+#pragma unroll
+          for (int i = 0; i < FBN; ++i)
+            if (k0 + i >= S) sv[i] = __float_as_uint(-1e30f);
+        }
+        // row max with 8 independent accumulators (short dependency chains)
+        float mxa[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mxa[a] = __uint_as_float(sv[a]);
+#pragma unroll
+        for (int i = 8; i < FBN; i += 8)
+#pragma unroll
+          for (int a = 0; a < 8; ++a) mxa[a] = fmaxf(mxa[a], __uint_as_float(sv[i + a]));
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        const float mnew = fmaxf(m, mx * scale_log2);
+        const bool need = (mnew - m) > 8.0f;
+        if (__any_sync(0xffffffffu, need) && j > t0) {  // lazy rescale of O (PV_x(j-1) done: s_full order)
+          const float f = need ? fast_exp2(m - mnew) : 1.0f;
+#pragma unroll
+          for (int c = 0; c < HD / 16; ++c) {
+            float o[16];
+            tmem_ld16(tO + c * 16, o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= f;
+            tmem_st16(tO + c * 16, o);
+          }
+        }
+        if (need) {
+          l *= fast_exp2(m - mnew);
+          m = mnew;
+        }
+        // MUFU ping-pong: the two warpgroups take turns for the exponentials (A first)
+        if (x == 1) mbar_wait(&turn[1], it & 1);
+        else if (it > 0) mbar_wait(&turn[0], (it - 1) & 1);
+        const float nm = -m;
+        float lsa[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) lsa[a] = 0.f;
+#pragma unroll
+        for (int c = 0; c < FBN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = fast_exp2(fmaf(__uint_as_float(sv[c * 32 + i]), scale_log2, nm));
+            const float p1 = fast_exp2(fmaf(__uint_as_float(sv[c * 32 + i + 1]), scale_log2, nm));
+            lsa[(i >> 1) & 7] += p0 + p1;
+            pk[i / 2] = pack_bf16(p0, p1);
+          }
+          tmem_st16u(tS + c * 16, pk);  // packed P keys 32c..32c+31 -> columns 16c..16c+15
+        }
+        l += ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
+        mbar_arrive(&turn[x ^ 1]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[x]);
+      }
+      mbar_wait(o_done, nu & 1);
+      tc_fence_after();
+      if (slot < 0) {  // whole key range: normalize and store
+        const float inv = 1.0f / l;
+        bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+          if (qrow < S) {
+            uint4 a = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
+                                 pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
+            uint4 b = make_uint4(pack_bf16(o[8] * inv, o[9] * inv), pack_bf16(o[10] * inv, o[11] * inv),
+                                 pack_bf16(o[12] * inv, o[13] * inv), pack_bf16(o[14] * inv, o[15] * inv));
+            reinterpret_cast<uint4*>(orow + c * 16)[0] = a;
+            reinterpret_cast<uint4*>(orow + c * 16)[1] = b;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(q_empty);
+      } else {  // key chunk: (m, l, O) partial; the last chunk of the unit merges in chunk order
+        float* wr = ws + ((size_t)slot * 2 * FBM + x * FBM + row) * PW;
+        *reinterpret_cast<float4*>(wr) = make_float4(m, l, 0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(wr + 4 + c * 16 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(q_empty);
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int grp = (u - plan.full) / plan.KC;
+        if (threadIdx.x == 128) *s_last = atomicAdd(&tickets[grp], 1) == plan.KC - 1;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (*s_last) {
+          __threadfence();
+          const float* base = ws + ((size_t)grp * plan.KC * 2 * FBM + x * FBM + row) * PW;
+          const size_t cstride = (size_t)2 * FBM * PW;
+          float M = -1e30f;
+          for (int c2 = 0; c2 < plan.KC; ++c2) M = fmaxf(M, __ldcg(base + c2 * cstride));
+          float den = 0.f, acc[HD];
+#pragma unroll
+          for (int d = 0; d < HD; ++d) acc[d] = 0.f;
+          for (int c2 = 0; c2 < plan.KC; ++c2) {  // chunk order; one row = HD/4 independent 16-byte loads
+            const float* pr2 = base + c2 * cstride;
+            const float4 ml = __ldcg(reinterpret_cast<const float4*>(pr2));
+            float4 ov[HD / 4];
+#pragma unroll
+            for (int q = 0; q < HD / 4; ++q) ov[q] = __ldcg(reinterpret_cast<const float4*>(pr2 + 4) + q);
+            const float f = exp2f(ml.x - M);
+            den += f * ml.y;
+#pragma unroll
+            for (int q = 0; q < HD / 4; ++q) {
+              acc[4 * q] += f * ov[q].x;
+              acc[4 * q + 1] += f * ov[q].y;
+              acc[4 * q + 2] += f * ov[q].z;
+              acc[4 * q + 3] += f * ov[q].w;
+            }
+          }
+          const float inv = 1.0f / den;
+          bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
+          if (qrow < S) {
+#pragma unroll
+            for (int d0 = 0; d0 < HD; d0 += 8)
+              *reinterpret_cast<uint4*>(orow + d0) =
+                  make_uint4(pack_bf16(acc[d0] * inv, acc[d0 + 1] * inv), pack_bf16(acc[d0 + 2] * inv, acc[d0 + 3] * inv),
+                             pack_bf16(acc[d0 + 4] * inv, acc[d0 + 5] * inv), pack_bf16(acc[d0 + 6] * inv, acc[d0 + 7] * inv));
+          }
+          if (threadIdx.x == 128) tickets[grp] = 0;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -569,12 +949,49 @@ cudaError_t fmha2_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int
 
 }  // namespace
 
+float* g_fmha_ws = nullptr;  // split-chunk partials: <= 148 chunks x 256 rows x (hd + 2) f32
+int* g_fmha_tickets = nullptr;
+
+template <int HD>
+cudaError_t fmha3_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int max_ctas,
+                         cudaStream_t s) {
+  CUtensorMap tm;
+  if (!make_qkv_map(&tm, qkv, S, ld)) return cudaErrorInvalidValue;
+  auto kern = fmha3_kernel<HD>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Ft3Cfg<HD>::SMEM);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  if (!g_fmha_ws) {  // once per process (one device per engine process)
+    if (cudaMalloc(&g_fmha_ws, (size_t)148 * 2 * FBM * (128 + 4) * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&g_fmha_tickets, 256 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(g_fmha_tickets, 0, 256 * sizeof(int)) != cudaSuccess)
+      return cudaErrorMemoryAllocation;
+  }
+  static const int split = getenv("NOVA_FMHA_SPLIT") ? atoi(getenv("NOVA_FMHA_SPLIT")) : 1;  // experiments only
+  const Fmha3Plan plan(S, H, split);
+  int grid = max_ctas > 0 ? max_ctas : 148;
+  if (grid > plan.total) grid = plan.total;
+  const float sl2 = LOG2E_F / sqrtf((float)HD);
+  return launch_k(kern, dim3(grid), dim3(384), Ft3Cfg<HD>::SMEM, s, false, tm, out, ldo, S, H, KV, sl2, g_fmha_ws,
+                  g_fmha_tickets, split);
+}
+
 // ld (the qkv row length in elements) must be a multiple of 8; hd in {80, 128} (64-col SW128 chunks).
 cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
-                          cudaStream_t s) {
+                          int max_ctas, cudaStream_t s) {
   if (S <= 0) return cudaSuccess;
   if (ld % 8 || H % KV || ldo % 8) return cudaErrorInvalidValue;
-  if (g_fmha_version == 2) {
+  if (g_fmha_version == 3 && !causal) {
+    switch (hd) {
+      case 80: return fmha3_launch<80>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
+      case 128: return fmha3_launch<128>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (g_fmha_version >= 2) {
     switch (hd) {
       case 80: return causal ? fmha2_launch<80, true>(qkv, ld, out, ldo, S, H, KV, s)
                              : fmha2_launch<80, false>(qkv, ld, out, ldo, S, H, KV, s);
@@ -592,6 +1009,6 @@ cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, in
   return cudaErrorInvalidValue;
 }
 
-int g_fmha_version = 2;
+int g_fmha_version = 3;
 
 }  // namespace nova

@@ -70,12 +70,13 @@ extern bool g_use_tma_gemv;
 
 // Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).
 // out [S][H * hd] (ldo).  causal: key j <= query i.  Query head h reads KV head h / (H / KV).
+// max_ctas: SM budget of the partition (0 = whole GPU); results do not depend on it.
 cudaError_t flash_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
-                       cudaStream_t s);
+                       int max_ctas, cudaStream_t s);
 // tcgen05/TMEM/TMA version (hd 80 / 128); flash_attn() dispatches to it for those head dims.
 cudaError_t flash_attn_tc(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
-                          cudaStream_t s);
-extern int g_fmha_version;  // 2: 2 CTAs/SM, P in TMEM (default); 1: single CTA, P in smem
+                          int max_ctas, cudaStream_t s);
+extern int g_fmha_version;  // 3: persistent 2-Q-tile ping-pong (default, non-causal); 2: 2 CTAs/SM; 1: P in smem
 // legacy warp-MMA (mma.sync) version, kept for head dims 16/32/64 and as the measured baseline
 cudaError_t flash_attn_mma(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                            cudaStream_t s);

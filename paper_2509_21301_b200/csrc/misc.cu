@@ -9,6 +9,10 @@ namespace nova {
 namespace {
 
 // ---------------------------------------------------------------- norms (one warp per row)
+// LayerNorm (ViT): the row is loaded once into registers (all loads in flight together), then
+// mean, biased variance and the output are computed from registers; the summation order
+// (lane-strided float4 chunks, then the xor butterfly) is fixed by d.
+constexpr int LN_MAXCH = 12;  // d <= 1536 register-resident; longer rows take the streaming loop
 __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ gm,
                                  const bf16* __restrict__ bt, bf16* __restrict__ y, int ldy, int M, int d, float eps) {
   pdl_launch_dependents();
@@ -17,6 +21,44 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf1
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const float* xr = x + (size_t)row * ldx;
+  bf16* yr = y + (size_t)row * ldy;
+  const int nch = d >> 2;
+  if (nch <= 32 * LN_MAXCH) {
+    float4 v[LN_MAXCH];
+#pragma unroll
+    for (int t = 0; t < LN_MAXCH; ++t) {
+      const int f = lane + 32 * t;
+      v[t] = f < nch ? reinterpret_cast<const float4*>(xr)[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < LN_MAXCH; ++t)
+      if (lane + 32 * t < nch) s += (v[t].x + v[t].y) + (v[t].z + v[t].w);
+    const float mu = warp_sum(s) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int t = 0; t < LN_MAXCH; ++t)
+      if (lane + 32 * t < nch) {
+        const float a = v[t].x - mu, b = v[t].y - mu, c = v[t].z - mu, e = v[t].w - mu;
+        q += (a * a + b * b) + (c * c + e * e);
+      }
+    const float rs = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+    for (int t = 0; t < LN_MAXCH; ++t) {
+      const int f = lane + 32 * t;
+      if (f >= nch) continue;
+      const int i = f * 4;
+      const float2 g01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i));
+      const float2 g23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i + 2));
+      const float2 b01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(bt + i));
+      const float2 b23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(bt + i + 2));
+      uint2 o;
+      o.x = pack_bf16((v[t].x - mu) * rs * g01.x + b01.x, (v[t].y - mu) * rs * g01.y + b01.y);
+      o.y = pack_bf16((v[t].z - mu) * rs * g23.x + b23.x, (v[t].w - mu) * rs * g23.y + b23.y);
+      *reinterpret_cast<uint2*>(yr + i) = o;
+    }
+    return;
+  }
   float s = 0.f;
   for (int i = lane * 4; i < d; i += 128) {
     float4 v = *reinterpret_cast<const float4*>(xr + i);
@@ -30,7 +72,6 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int ldx, const bf1
     q += (a * a + b * b) + (c * c + e * e);
   }
   const float rs = rsqrtf(warp_sum(q) / d + eps);
-  bf16* yr = y + (size_t)row * ldy;
   for (int i = lane * 4; i < d; i += 128) {
     float4 v = *reinterpret_cast<const float4*>(xr + i);
     const float2 g01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i));
@@ -92,24 +133,52 @@ __global__ void patchify_kernel(const bf16* __restrict__ pix, int C, int H, int 
 
 // ---------------------------------------------------------------- RoPE
 // ViT: angle for pair i (< hd/2): i < hd/4 -> h * inv[i], else w * inv[i - hd/4]; inv[j] = theta^(-4j/hd).
-__global__ void vit_rope_kernel(bf16* __restrict__ qkv, int heads, int hd, int gw, int m, float log2_theta) {
-  const int r = blockIdx.x;
-  const int grp = r / (m * m), in = r % (m * m);
-  const int gi = grp / (gw / m), gj = grp % (gw / m);
-  const float ph = (float)(gi * m + in / m), pw = (float)(gj * m + in % m);
-  const int half = hd / 2, quarter = hd / 4;
-  bf16* row = qkv + (size_t)r * 3 * heads * hd;
-  for (int idx = threadIdx.x; idx < 2 * heads * half; idx += blockDim.x) {
-    const int hh = idx / half, i = idx % half;  // hh < heads: q, else k
+// CTA = VR rows: the hd/2 (cos, sin) pairs of each row are computed once into smem, then every
+// (row, q|k head, 8-pair group) is one thread: two 16-byte loads (x[i..i+7], x[i+half..]) and
+// two 16-byte stores, in place.  Same per-element arithmetic as the scalar form.
+constexpr int VR = 8;
+__global__ void __launch_bounds__(256) vit_rope_kernel(bf16* __restrict__ qkv, int N, int heads, int hd, int gw, int m,
+                                                       float log2_theta) {
+  extern __shared__ float cs_tab[];  // [VR][half] cos, then [VR][half] sin
+  const int half = hd / 2, quarter = hd / 4, r0 = blockIdx.x * VR;
+  float* ctab = cs_tab;
+  float* stab = cs_tab + VR * half;
+  for (int idx = threadIdx.x; idx < VR * half; idx += blockDim.x) {
+    const int rr = idx / half, i = idx % half, r = r0 + rr;
+    if (r >= N) continue;
+    const int grp = r / (m * m), in = r % (m * m);
+    const int gi = grp / (gw / m), gj = grp % (gw / m);
+    const float ph = (float)(gi * m + in / m), pw = (float)(gj * m + in % m);
     const int j = i < quarter ? i : i - quarter;
     const float inv = exp2f(-(4.0f * j / hd) * log2_theta);
     const float ang = (i < quarter ? ph : pw) * inv;
     float sn, cs;
     sincosf(ang, &sn, &cs);
-    bf16* v = row + (size_t)hh * hd;  // q heads then k heads are contiguous
-    const float x1 = __bfloat162float(v[i]), x2 = __bfloat162float(v[i + half]);
-    v[i] = __float2bfloat16_rn(x1 * cs - x2 * sn);
-    v[i + half] = __float2bfloat16_rn(x2 * cs + x1 * sn);
+    ctab[idx] = cs;
+    stab[idx] = sn;
+  }
+  __syncthreads();
+  const int groups = half / 8, per_row = 2 * heads * groups;
+  for (int u = threadIdx.x; u < VR * per_row; u += blockDim.x) {
+    const int rr = u / per_row, rem = u % per_row, r = r0 + rr;
+    if (r >= N) continue;
+    const int hh = rem / groups, i0 = (rem % groups) * 8;  // hh < heads: q, else k (contiguous)
+    bf16* v = qkv + (size_t)r * 3 * heads * hd + (size_t)hh * hd;
+    const uint4 a = *reinterpret_cast<const uint4*>(v + i0);
+    const uint4 b = *reinterpret_cast<const uint4*>(v + i0 + half);
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+    uint32_t oa[4], ob[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 x1 = unpack_bf16(aw[q]), x2 = unpack_bf16(bw[q]);
+      const int i = i0 + 2 * q;
+      const float c0 = ctab[rr * half + i], s0 = stab[rr * half + i];
+      const float c1 = ctab[rr * half + i + 1], s1 = stab[rr * half + i + 1];
+      oa[q] = pack_bf16(x1.x * c0 - x2.x * s0, x1.y * c1 - x2.y * s1);
+      ob[q] = pack_bf16(x2.x * c0 + x1.x * s0, x2.y * c1 + x1.y * s1);
+    }
+    *reinterpret_cast<uint4*>(v + i0) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+    *reinterpret_cast<uint4*>(v + i0 + half) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
   }
 }
 
@@ -277,9 +346,9 @@ cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int mer
 }
 cudaError_t vit_rope(bf16* qkv, int N, int heads, int hd, int gw, int merge, float theta, cudaStream_t s) {
   if (N <= 0) return cudaSuccess;
-  count_launch();
-  vit_rope_kernel<<<N, 256, 0, s>>>(qkv, heads, hd, gw, merge, log2f(theta));
-  return cudaGetLastError();
+  if (hd % 16) return cudaErrorInvalidValue;
+  return launch_k(vit_rope_kernel, dim3((N + VR - 1) / VR), dim3(256), (size_t)2 * VR * (hd / 2) * sizeof(float), s,
+                  false, qkv, N, heads, hd, gw, merge, log2f(theta));
 }
 cudaError_t llm_rope_kv(bf16* qkv, int ld, int nrows, int H, int KV, int hd, float theta, int sec0, int sec1,
                         const int* pos3, int ld_pos, const DecodeRow* rows, int slot, int ctx0, bf16* pool, int layer,

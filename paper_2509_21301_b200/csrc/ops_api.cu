@@ -25,8 +25,8 @@ int nova_op_gemv_tma(const void* X, int ldx, const void* W, int N, int K, void* 
                      S(stream)));
 }
 int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int Sq, int H, int KV, int hd, int causal,
-                       void* stream) {
-  return st(flash_attn((const bf16*)qkv, ld, (bf16*)out, ldo, Sq, H, KV, hd, causal, S(stream)));
+                       int max_ctas, void* stream) {
+  return st(flash_attn((const bf16*)qkv, ld, (bf16*)out, ldo, Sq, H, KV, hd, causal, max_ctas, S(stream)));
 }
 int nova_op_flash_attn_mma(const void* qkv, int ld, void* out, int ldo, int Sq, int H, int KV, int hd, int causal,
                            void* stream) {

@@ -117,7 +117,7 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
       const double w = 4.0 * N * N * hd * m.vit_heads;
       pass_work[0] += w;
       const int i = ktimer[0].begin(s);
-      CUDA_TRY(flash_attn(fw.qkv, 3 * Dv, fw.attn, Dv, N, m.vit_heads, m.vit_heads, hd, 0, s));
+      CUDA_TRY(flash_attn(fw.qkv, 3 * Dv, fw.attn, Dv, N, m.vit_heads, m.vit_heads, hd, 0, sms, s));
       ktimer[0].end(i, NOVA_K_VIT_ATTN, w, s);
     }
     CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.attn, Dv, blk + vl.proj_w, Dv, fw.vhid, Dv, blk + vl.proj_b, N, Dv,
@@ -177,7 +177,7 @@ cudaError_t Engine::run_prefill(Request* r, cudaStream_t s, int sms) {
       const double w = 2.0 * S * S * hd * H;
       pass_work[0] += w;
       const int i = ktimer[0].begin(s);
-      CUDA_TRY(flash_attn(fw.qkv, ldq, fw.attn, H * hd, S, H, KV, hd, 1, s));
+      CUDA_TRY(flash_attn(fw.qkv, ldq, fw.attn, H * hd, S, H, KV, hd, 1, sms, s));
       ktimer[0].end(i, NOVA_K_PRE_ATTN, w, s);
     }
     CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.attn, H * hd, L.o_w, H * hd, fw.hid, D, nullptr, S, D, H * hd,

@@ -46,9 +46,9 @@ def nova_op_gemv_tma(X, W, Y, bias, N, K, B, epi, ldx=None, ldy=None, stream=Non
                                  epi, _p(ws), _p(tk), _s(stream)), "gemv_tma")
 
 
-def nova_op_flash_attn(qkv, out, S, H, KV, hd, causal, stream=None):
+def nova_op_flash_attn(qkv, out, S, H, KV, hd, causal, max_ctas=0, stream=None):
     check(lib().nova_op_flash_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), S, H, KV, hd, int(causal),
-                                   _s(stream)), "flash_attn")
+                                   max_ctas, _s(stream)), "flash_attn")
 
 
 def nova_op_flash_attn_mma(qkv, out, S, H, KV, hd, causal, stream=None):

@@ -165,7 +165,7 @@ def test_gemv_f32_input_and_silu():
 
 @pytest.mark.parametrize("S,H,KV,hd,causal", [(16, 4, 4, 16, 0), (300, 4, 4, 16, 0), (12, 4, 2, 32, 1),
                                                (1286, 12, 2, 128, 1), (777, 16, 16, 80, 0), (130, 28, 4, 128, 1),
-                                               (4888, 2, 2, 80, 0)])
+                                               (4888, 2, 2, 80, 0), (500, 4, 4, 128, 0), (100, 3, 3, 80, 0)])
 def test_flash_attn(S, H, KV, hd, causal):
     rng = np.random.default_rng(S + hd)
     qkv = rand_bf16(rng, (S, (H + 2 * KV) * hd))
@@ -332,3 +332,27 @@ def test_norms_patchify_vitrope_embed_argmax():
     torch.cuda.synchronize()
     assert tok.cpu().tolist() == [V.argmax_lowest(r) for r in lg]
     assert tok.cpu().tolist()[1] == 7
+
+
+def test_flash_attn_vit_shape_grid_invariant():
+    """ViT shape (N = 4888, 16 heads, hd 80): the persistent kernel's tail units are split along
+    keys and merged; output must not depend on the SM budget, and matches the oracle on the
+    heads that take the split path (head 15) and the whole-range path (head 0)."""
+    rng = np.random.default_rng(4888)
+    S, H, hd = 4888, 16, 80
+    qkv = rand_bf16(rng, (S, 3 * H * hd))
+    d = bf16_dev(qkv)
+    outs = []
+    for ctas in (148, 100, 37):
+        out = torch.empty(S, H * hd, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_flash_attn(d, out, S, H, H, hd, 0, max_ctas=ctas)
+        torch.cuda.synchronize()
+        outs.append(out)
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16))
+    t = qkv.reshape(S, 3, H, hd)
+    got = bf16_host(outs[0]).reshape(S, H, hd)
+    for h in (0, 15):
+        ref = V.attention_full(t[:, 0, h:h + 1].astype(np.float64), t[:, 1, h:h + 1].astype(np.float64),
+                               t[:, 2, h:h + 1].astype(np.float64), hd ** -0.5)
+        assert rel_inf(got[:, h:h + 1], ref) <= 2e-2, h
