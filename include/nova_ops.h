@@ -50,11 +50,14 @@ int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ld
 int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias,
                  int B, int epi, void* stream);
 
-/* TMA-streamed decode linear (bf16 X only): same contract as nova_op_gemv (N % 64 == 0,
- * K % 64 == 0).  ws: f32 workspace of 16*B*N floats for split-K partials; tickets: int32
- * [N/64] zero-initialised once (the kernel leaves them zero).  Deterministic. */
+/* Persistent TMA-streamed decode linear (bf16 X only; PAPER.md P:141, P:283 -- decode is
+ * memory-bound and runs on an SM slice): same contract as nova_op_gemv for the
+ * bf16 / SiLU / f32-residual / f32-store epilogues (N % 64 == 0, K % 64 == 0).  max_ctas =
+ * the SM budget (0 = 148): one CTA per SM streams its units' weight tiles through one smem
+ * ring.  ws: f32 workspace of 16*B*N floats for split-K partials; tickets: int32 [N/64]
+ * zero-initialised once (the kernel leaves them zero).  Bitwise independent of max_ctas and B. */
 int nova_op_gemv_tma(const void* X, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias, int B,
-                     int epi, float* ws, int32_t* tickets, void* stream);
+                     int epi, float* ws, int32_t* tickets, int max_ctas, void* stream);
 
 /* Flash attention (a5 ViT: causal = 0, KV = H; a6 prefill: causal = 1, GQA; PAPER.md
  * Table resource_stage P:139-140 "Attention").  qkv [S][(H + 2 KV) hd] bf16 (ld): q heads,
@@ -101,18 +104,34 @@ int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void*
  *   NOVA_EPI_F32_ARGMAX: logits -> Y f32, and keys[b] (uint64, zero on entry) receives the
  *     packed (order-preserving logit bits << 32 | ~index) maximum: argmax, ties -> lowest
  *     index.  nova_op_argmax_finalize turns keys into tokens.
+ * x_mode 0 with NOVA_EPI_QKV_ROPE_KV runs the persistent TMA-streamed kernel (hd 128).
  * Unused pointer arguments may be NULL.  N % 32 == 0, K % 32 == 0. */
 int nova_op_gemv_fused(const void* X, int x_mode, int ldx, const void* W, int N, int K, void* Y, int ldy,
                        const void* bias, int B, int epi, const void* gamma, float eps, int H, int KV, int hd,
                        float theta, const nova_decode_row* rows, void* kv_pool, int layer, int n_pages,
                        const int32_t* block_tables, int max_pages, uint64_t* keys, void* stream);
 
+/* Streaming layout of a decode weight W [N][K] bf16 (N % 64 == 0, K % 64 == 0): W_blocked
+ * [N/64][K/64] tiles of 64 rows x 64 k, each tile's 128-byte rows with their 16-byte chunks
+ * XOR-swizzled by (row & 7) -- the shared-memory image of a TMA SWIZZLE_128B box, so decode
+ * streams one contiguous 8 KB bulk copy per tile (full DRAM bursts on a small SM slice). */
+int nova_op_block_weights(const void* W, void* W_blocked, int N, int K, void* stream);
+
+/* Persistent decode linear over a weight in the streaming layout (same contract as
+ * nova_op_gemv_tma; max_ctas = SM budget).  X_lo != NULL: the input is f32 given as bf16 hi
+ * rows (X) + lo rows (X_lo) (two products on the tensor core); epi may then be
+ * NOVA_EPI_F32_STORE or NOVA_EPI_F32_ARGMAX (keys as in nova_op_gemv_fused). */
+int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
+                        const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
+                        void* stream);
+
 /* keys[r] (from NOVA_EPI_F32_ARGMAX) -> out_tok[r]; also last_tok[rows[r].slot] (rows != NULL)
  * or last_tok[single_slot] (>= 0); resets keys[r] to 0.  n <= 1024. */
 int nova_op_argmax_finalize(uint64_t* keys, int n, int32_t* out_tok, const nova_decode_row* rows, int32_t* last_tok,
                             int single_slot, void* stream);
 
-/* LayerNorm (ViT, mean/biased variance) and RMSNorm (LLM) of f32 rows [M][d]. */
+/* LayerNorm (ViT, mean/biased variance) and RMSNorm (LLM) of f32 rows [M][d].  RMSNorm y_f32:
+ * 0 bf16 rows, 1 f32 rows, 2 bf16 hi rows at y then bf16 lo rows at y + M*ldy. */
 int nova_op_layernorm(const float* x, int ldx, const void* gamma, const void* beta, void* y, int ldy, int M, int d,
                       float eps, void* stream);
 int nova_op_rmsnorm(const float* x, int ldx, const void* gamma, void* y, int y_f32, int ldy, int M, int d, float eps,

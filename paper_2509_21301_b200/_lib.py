@@ -21,12 +21,14 @@ U64 = C.c_uint64
 OPS_SIGNATURES = {
     "nova_op_gemm": [P, I, P, I, P, I, P, I, I, I, I, I, P],
     "nova_op_gemv": [P, I, I, P, I, I, P, I, P, I, I, P],
-    "nova_op_gemv_tma": [P, I, P, I, I, P, I, P, I, I, P, P, P],
+    "nova_op_gemv_tma": [P, I, P, I, I, P, I, P, I, I, P, P, I, P],
     "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, I, P],
     "nova_op_flash_attn_mma": [P, I, P, I, I, I, I, I, I, P],
     "nova_op_decode_attn": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P, P],
     "nova_op_gemv_fused": [P, I, I, P, I, I, P, I, P, I, I, P, F, I, I, I, F, P, P, I, I, P, I, P, P],
     "nova_op_argmax_finalize": [P, I, P, P, P, I, P],
+    "nova_op_block_weights": [P, P, I, I, P],
+    "nova_op_gemv_stream": [P, P, I, P, I, I, P, I, P, I, I, P, P, P, I, P],
     "nova_op_layernorm": [P, I, P, P, P, I, I, I, F, P],
     "nova_op_rmsnorm": [P, I, P, P, I, I, I, I, F, P],
     "nova_op_patchify": [P, I, I, I, I, I, I, P, P],

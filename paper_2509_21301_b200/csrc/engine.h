@@ -39,6 +39,8 @@ struct VitLayerLayout {
 
 struct LlmLayerW {
   bf16 *ln1, *qkv_w, *qkv_b, *o_w, *ln2, *gu_w, *down_w;
+  // decode copies in the streaming layout (blocked 64 x 64, SW128 pre-swizzled; block_weights)
+  bf16 *qkv_wb, *o_wb, *gu_wb, *down_wb;
 };
 
 struct Weights {
@@ -46,6 +48,7 @@ struct Weights {
   std::vector<bf16*> vit_dev;  // resident: L layer blocks; offload: K slot blocks
   bf16 *mlnq_g, *mlnq_b, *m1_w, *m1_b, *m2_w, *m2_b;
   bf16 *embed, *final_norm, *lm_head;
+  bf16* lm_head_b = nullptr;  // lm_head in the streaming layout
   std::vector<LlmLayerW> llm;
 };
 
@@ -280,7 +283,9 @@ class Engine {
   int front_sms(int s_dec) const { return s_dec <= 0 ? part.total : part.total - s_dec; }
   cudaError_t run_encode(Request* r, cudaStream_t s, int sms);
   cudaError_t run_prefill(Request* r, cudaStream_t s, int sms);
-  cudaError_t run_decode(const std::vector<Request*>& rows, const std::vector<int>& forced, cudaStream_t s);
+  // decode SMs of a pass: the whole GPU when SOLO, else the partition's s_dec
+  int dec_sms(int ctx, int s_dec) const { return (ctx == NOVA_CTX_SOLO || s_dec <= 0 || s_dec >= part.total) ? part.total : s_dec; }
+  cudaError_t run_decode(const std::vector<Request*>& rows, const std::vector<int>& forced, cudaStream_t s, int sms);
   cudaStream_t stream_for(int role, int ctx, int s_dec);
   int s_max_of_public() const;
   nova_status time_pass(int stage, int s, int gh, int gw, int n_prompt, int B, int ctx, int corun, int iters,

@@ -177,7 +177,7 @@ void Worker::run() {
       e = eng->run_prefill(c.reqs[0], s, eng->front_sms(c.s_dec));
       done.kind = NOVA_EV_PREFILL_DONE;
     } else {
-      e = eng->run_decode(c.reqs, c.forced_tok, s);
+      e = eng->run_decode(c.reqs, c.forced_tok, s, eng->dec_sms(c.ctx, c.s_dec));
       done.kind = NOVA_EV_DECODE_DONE;
       for (Request* r : c.reqs) done.key = std::min<uint64_t>(done.key, r->id);
     }
@@ -310,6 +310,21 @@ nova_status Engine::finalize() {
         return fail(NOVA_E_CUDA, "offload preload");
       cudaEventRecord(ev_loaded[k], copy_stream);
     }
+  }
+  {  // decode copies of the LLM linears in the streaming layout (model.cpp plan_weights)
+    const auto& m = dims.m;
+    const int D = m.llm_dim, F = m.llm_ffn, HD = m.llm_heads * m.head_dim;
+    cudaError_t e = cudaSuccess;
+    for (int l = 0; l < m.llm_layers && e == cudaSuccess; ++l) {
+      const LlmLayerW& L = W.llm[l];
+      e = block_weights(L.qkv_w, L.qkv_wb, dims.llm_qkv_n, D, copy_stream);
+      if (e == cudaSuccess) e = block_weights(L.o_w, L.o_wb, D, HD, copy_stream);
+      if (e == cudaSuccess) e = block_weights(L.gu_w, L.gu_wb, 2 * F, D, copy_stream);
+      if (e == cudaSuccess) e = block_weights(L.down_w, L.down_wb, D, F, copy_stream);
+    }
+    if (e == cudaSuccess) e = block_weights(W.lm_head, W.lm_head_b, m.vocab, D, copy_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(copy_stream);
+    if (e != cudaSuccess) return fail(NOVA_E_CUDA, std::string("streaming weight layout: ") + cudaGetErrorString(e));
   }
   cudaMemset(d_pix, 0, pix_stride * 2 * n_slots_total);
   cudaMemset(d_prompt, 0, (size_t)n_slots_total * cfg.max_prompt * 4);

@@ -60,13 +60,25 @@ cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int
 cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K, void* Y, int ldy,
                  const bf16* bias, int B, int epi, cudaStream_t s);
 
-// TMA-streamed decode GEMV (bf16 X): 64-row CTAs, 8-stage smem ring, split-K over P CTAs
-// (P = gemv_tma_splits(N, K), shape-only) with a deterministic last-CTA reduction.
-// ws: P*B*N floats, tickets: N/64 ints (zero-initialised once; the kernel restores them).
-cudaError_t gemv_tma(const bf16* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
-                     int epi, float* ws, int* tickets, cudaStream_t s);
+// Persistent TMA-streamed decode GEMV (bf16 X): grid = the partition's SM budget (max_ctas,
+// 0 = 148), one continuous weight ring per CTA over its static list of (row block x K split)
+// units.  Decomposition from (N, K, epi) only (gemv_tma_plan); split-K partials in ws
+// (P * B * N floats) reduced in split order by the last CTA of a row block (tickets: N / RB
+// ints, zero on entry, left zero).  EPI_QKV_ROPE_KV needs aux (hd 128).
+struct GemvTmaPlan {
+  int RB = 64, P = 1, ks = 0, units = 0;
+};
+GemvTmaPlan gemv_tma_plan(int N, int K, int epi);
 int gemv_tma_splits(int N, int K);
+struct GemvAux;
+// W_blocked: the same weight in the streaming layout (block_weights) -> 8 KB bulk copies
+// instead of tensor-map boxes.  X_lo: f32 x given as bf16 hi (X) + lo rows (rmsnorm mode 2);
+// required by EPI_F32_ARGMAX (lm_head).
+cudaError_t gemv_tma(const bf16* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, const bf16* bias, int B,
+                     int epi, float* ws, int* tickets, cudaStream_t s, int max_ctas = 0,
+                     const GemvAux* aux = nullptr, const bf16* W_blocked = nullptr, const bf16* X_lo = nullptr);
 extern bool g_use_tma_gemv;
+extern int g_dec_tma_mask;  // decode linears on the persistent TMA GEMV: bit 0 qkv, 1 o, 2 gate|up, 3 down, 4 lm_head
 
 // Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).
 // out [S][H * hd] (ldo).  causal: key j <= query i.  Query head h reads KV head h / (H / KV).
@@ -118,8 +130,11 @@ cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf
 
 cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d,
                       float eps, cudaStream_t s);
+// y_f32: 0 bf16 rows, 1 f32 rows, 2 bf16 hi rows at y and bf16 lo rows at y + M * ldy
 cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
                     cudaStream_t s);
+// streaming layout of a decode weight: [N/64][K/64] pre-swizzled 64 x 64 tiles (8 KB each)
+cudaError_t block_weights(const bf16* src, bf16* dst, int N, int K, cudaStream_t s);
 
 // pixels bf16 [C][H][W] -> X0 [N][C*T*P*P] merge-group-major rows
 cudaError_t patchify(const bf16* pix, int C, int H, int W, int P, int T, int merge, bf16* X0, cudaStream_t s);

@@ -103,7 +103,23 @@ __global__ void __launch_bounds__(512) rmsnorm_kernel(const float* __restrict__ 
     const float2 g01 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i));
     const float2 g23 = unpack_bf16(*reinterpret_cast<const uint32_t*>(gm + i + 2));
     const float o0 = xv.x * rs * g01.x, o1 = xv.y * rs * g01.y, o2 = xv.z * rs * g23.x, o3 = xv.w * rs * g23.y;
-    if (y_f32) {
+    if (y_f32 == 2) {  // bf16 hi / lo pair (f32 operand of the decode lm_head on the tensor core)
+      bf16* yh = reinterpret_cast<bf16*>(y) + (size_t)row * ldy + i;
+      bf16* yl = reinterpret_cast<bf16*>(y) + (size_t)M * ldy + (size_t)row * ldy + i;
+      const float o[4] = {o0, o1, o2, o3};
+      bf16 h[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        h[q] = __float2bfloat16_rn(o[q]);
+        lo[q] = __float2bfloat16_rn(o[q] - __bfloat162float(h[q]));
+      }
+      *reinterpret_cast<uint2*>(yh) = make_uint2(
+          (uint32_t)__bfloat16_as_ushort(h[0]) | ((uint32_t)__bfloat16_as_ushort(h[1]) << 16),
+          (uint32_t)__bfloat16_as_ushort(h[2]) | ((uint32_t)__bfloat16_as_ushort(h[3]) << 16));
+      *reinterpret_cast<uint2*>(yl) = make_uint2(
+          (uint32_t)__bfloat16_as_ushort(lo[0]) | ((uint32_t)__bfloat16_as_ushort(lo[1]) << 16),
+          (uint32_t)__bfloat16_as_ushort(lo[2]) | ((uint32_t)__bfloat16_as_ushort(lo[3]) << 16));
+    } else if (y_f32) {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + (size_t)row * ldy + i) = make_float4(o0, o1, o2, o3);
     } else {
       uint2 o;
@@ -313,9 +329,32 @@ __global__ void argmax_finalize_kernel(unsigned long long* __restrict__ keys, in
   else if (single_slot >= 0 && last_tok) last_tok[single_slot] = tok;
 }
 
+// [N][K] row-major -> [N/64][K/64] blocks of [64 rows][64 k], each block's rows 128 B with
+// the 16-byte chunks XOR-swizzled by (row & 7): the byte image TMA SWIZZLE_128B would leave in
+// shared memory, so one 8 KB bulk copy per tile lands ready for ldmatrix.
+__global__ void block_weights_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, int N, int K) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk of dst
+  const size_t nchunks = (size_t)N * K / 8;
+  if (i >= nchunks) return;
+  const size_t blk = i / 512;               // 64 x 64 bf16 = 512 chunks per block
+  const int within = (int)(i % 512), r = within / 8, cpos = within % 8;
+  const int c = cpos ^ (r & 7);             // logical 16-byte chunk stored at position cpos
+  const int kb = K / 64;
+  const size_t n = (blk / kb) * 64 + r, k = (blk % kb) * 64 + c * 8;
+  reinterpret_cast<uint4*>(dst)[i] = *reinterpret_cast<const uint4*>(src + n * K + k);
+}
+
 }  // namespace
 
 std::atomic<unsigned long long> g_kernel_launches{0};
+
+cudaError_t block_weights(const bf16* src, bf16* dst, int N, int K, cudaStream_t s) {
+  if (N % 64 || K % 64) return cudaErrorInvalidValue;
+  const size_t n = (size_t)N * K / 8;
+  count_launch();
+  block_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst, N, K);
+  return cudaGetLastError();
+}
 
 cudaError_t argmax_finalize(unsigned long long* keys, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
                             int single_slot, cudaStream_t s) {

@@ -90,6 +90,18 @@ size_t Engine::plan_weights(const Dims& d, const nova_engine_config& c, Weights*
   }
   W.final_norm = take(D);
   W.lm_head = m.tie_embed ? W.embed : take(V * D);
+  // Decode streams every LLM linear once per iteration from a slice of the SMs; it reads a
+  // second copy in the streaming layout (contiguous, pre-swizzled 64 x 64 tiles: one bulk copy
+  // per tile, full DRAM bursts -- scripts/probe_bw.cu measured row-major 128-byte tile rows at
+  // ~56% of contiguous bandwidth on a 24-SM partition).  The prefill GEMM keeps [out][in].
+  for (int i = 0; i < m.llm_layers; ++i) {
+    LlmLayerW& L = W.llm[i];
+    L.qkv_wb = take((size_t)d.llm_qkv_n * D);
+    L.o_wb = take(D * m.llm_heads * m.head_dim);
+    L.gu_wb = take(2 * F * D);
+    L.down_wb = take(D * F);
+  }
+  W.lm_head_b = take(V * D);
   return off;
 }
 

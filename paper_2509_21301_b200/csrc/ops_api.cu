@@ -20,9 +20,9 @@ int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K,
   return st(gemv(X, x_f32, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, S(stream)));
 }
 int nova_op_gemv_tma(const void* X, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias, int B,
-                     int epi, float* ws, int32_t* tickets, void* stream) {
+                     int epi, float* ws, int32_t* tickets, int max_ctas, void* stream) {
   return st(gemv_tma((const bf16*)X, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, ws, tickets,
-                     S(stream)));
+                     S(stream), max_ctas));
 }
 int nova_op_flash_attn(const void* qkv, int ld, void* out, int ldo, int Sq, int H, int KV, int hd, int causal,
                        int max_ctas, void* stream) {
@@ -56,7 +56,27 @@ int nova_op_gemv_fused(const void* X, int x_mode, int ldx, const void* W, int N,
   a.bt = bt;
   a.max_pages = max_pages;
   a.keys = (unsigned long long*)keys;
+  if (x_mode == 0 && epi == EPI_QKV_ROPE_KV) {  // bf16 x: the persistent TMA-streamed kernel
+    static float* ws = nullptr;  // split-K partials / tickets of this op-level entry point
+    static int* tk = nullptr;
+    if (!ws && (cudaMalloc(&ws, (size_t)16 << 20) != cudaSuccess || cudaMalloc(&tk, 8192 * 4) != cudaSuccess ||
+                cudaMemset(tk, 0, 8192 * 4) != cudaSuccess))
+      return st(cudaErrorMemoryAllocation);
+    return st(gemv_tma((const bf16*)X, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, ws, tk,
+                       S(stream), 0, &a));
+  }
   return st(gemv_ex(X, x_mode, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, a, S(stream)));
+}
+int nova_op_block_weights(const void* W, void* W_blocked, int N, int K, void* stream) {
+  return st(block_weights((const bf16*)W, (bf16*)W_blocked, N, K, S(stream)));
+}
+int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
+                        const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
+                        void* stream) {
+  GemvAux a;
+  a.keys = (unsigned long long*)keys;
+  return st(gemv_tma((const bf16*)X, ldx, nullptr, N, K, Y, ldy, (const bf16*)bias, B, epi, ws, tickets, S(stream),
+                     max_ctas, &a, (const bf16*)W_blocked, (const bf16*)X_lo));
 }
 int nova_op_argmax_finalize(uint64_t* keys, int n, int32_t* out_tok, const nova_decode_row* rows, int32_t* last_tok,
                             int single_slot, void* stream) {

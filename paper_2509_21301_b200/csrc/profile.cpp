@@ -56,6 +56,7 @@ nova_status Engine::time_pass(int stage, int s, int gh, int gw, int n_prompt, in
   const int fsms = front_sms(s);
   cudaStream_t fs = stream_for(0, NOVA_CTX_DV, s);
   cudaStream_t ds = stream_for(1, s == 0 ? NOVA_CTX_SOLO : NOVA_CTX_DV, s == 0 ? part.total : s);
+  const int dsms = dec_sms(s == 0 ? NOVA_CTX_SOLO : NOVA_CTX_DV, s == 0 ? part.total : s);
   cudaEvent_t a, b, c, d;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -68,7 +69,7 @@ nova_status Engine::time_pass(int stage, int s, int gh, int gw, int n_prompt, in
     cudaStream_t st = stage == 2 ? ds : fs;
     for (int it = 0; it <= iters && e == cudaSuccess; ++it) {  // iteration 0 = warm-up
       if (it == 1) e = cudaEventRecord(a, st);
-      if (e == cudaSuccess) e = stage == 2 ? run_decode(dptr, forced, st) : run_front(st);
+      if (e == cudaSuccess) e = stage == 2 ? run_decode(dptr, forced, st, dsms) : run_front(st);
     }
     if (e == cudaSuccess) e = cudaEventRecord(b, st);
     if (e == cudaSuccess) e = cudaEventSynchronize(b);
@@ -81,7 +82,7 @@ nova_status Engine::time_pass(int stage, int s, int gh, int gw, int n_prompt, in
     double fsum = 0, dsum = 0;
     int dn = 0;
     for (int it = 0; it <= iters && e == cudaSuccess; ++it) {
-      e = run_decode(dptr, forced, ds);  // warm decode on its partition
+      e = run_decode(dptr, forced, ds, dsms);  // warm decode on its partition
       if (e == cudaSuccess) e = cudaStreamSynchronize(ds);
       if (e == cudaSuccess) e = cudaEventRecord(a, fs);
       if (e == cudaSuccess) e = run_front(fs);
@@ -90,7 +91,7 @@ nova_status Engine::time_pass(int stage, int s, int gh, int gw, int n_prompt, in
       int n = 0;
       e = cudaEventRecord(c, ds);
       while (e == cudaSuccess && n < 100000) {
-        e = run_decode(dptr, forced, ds);
+        e = run_decode(dptr, forced, ds, dsms);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ds);
         ++n;
         if (cudaEventQuery(b) == cudaSuccess) break;

@@ -77,14 +77,16 @@ static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xmode, int ldx,
 }
 
 // TMA-streamed decode linear (bf16 x): gate|up, where it streams at ~99% of HBM (scripts/kbench.py)
-static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, int N, int K, void* Y, int ldy, int B,
-                              int epi, cudaStream_t s) {
+static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, const bf16* Wb, int N, int K, void* Y,
+                              int ldy, const bf16* bias, int B, int epi, int sms, const GemvAux* aux, cudaStream_t s,
+                              const bf16* X_lo = nullptr, int cls = NOVA_K_DEC_GEMV) {
   const int nout = epi == EPI_BF16_SILUMUL ? N / 2 : N;
-  const double bytes = (double)N * K * 2 + (double)B * K * 2 + (double)B * nout * 2;
+  const int ysz = epi == EPI_F32_RESID ? 8 : ((epi == EPI_F32_STORE || epi == EPI_F32_ARGMAX) ? 4 : 2);
+  const double bytes = (double)N * K * 2 + (double)B * K * (X_lo ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, nullptr, B, epi, E->dw.gemv_ws, E->dw.tickets, s));
-  E->ktimer[1].end(i, NOVA_K_DEC_GEMV, bytes, s);
+  CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms, aux, Wb, X_lo));
+  E->ktimer[1].end(i, cls, bytes, s);
   return cudaSuccess;
 }
 
@@ -206,7 +208,8 @@ cudaError_t Engine::run_prefill(Request* r, cudaStream_t s, int sms) {
 }
 
 // ---------------------------------------------------------------- LLM decode iteration (a7)
-cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vector<int>& forced, cudaStream_t s) {
+cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vector<int>& forced, cudaStream_t s,
+                               int sms) {
   const auto& m = dims.m;
   const int D = m.llm_dim, H = m.llm_heads, KV = m.llm_kv_heads, hd = m.head_dim, F = m.llm_ffn;
   const int B = (int)rq.size(), ldq = dims.llm_qkv_n;
@@ -241,12 +244,23 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
   qa.n_pages = cfg.kv_pages;
   qa.bt = d_bt;
   qa.max_pages = max_pages_per_req;
+  // Per linear: the persistent TMA GEMV over the streaming layout, sized to the decode partition
+  // (sms SMs, 4 CTAs each), or the register-streaming GEMV (fixed grid; RMSNorm on load for qkv).
+  // g_dec_tma_mask bit 0 qkv, 1 o, 2 gate|up, 3 down, 4 lm_head (env NOVA_DEC_TMA overrides).
+  const int tm = g_dec_tma_mask;
+  const bool rope_tma = (tm & 1) && hd == 128;
   for (int l = 0; l < m.llm_layers; ++l) {
     const LlmLayerW& L = W.llm[l];
     qa.gamma = L.ln1;
     qa.layer = l;
-    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.hid, 2, D, L.qkv_w, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV, qa,
-                    s));
+    if (rope_tma) {
+      CUDA_TRY(rmsnorm(dw.hid, D, L.ln1, dw.xb, 0, D, B, D, m.rms_eps, s));
+      CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.qkv_w, L.qkv_wb, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV, sms,
+                          &qa, s));
+    } else {
+      CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.hid, 2, D, L.qkv_w, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV,
+                      qa, s));
+    }
     {
       pass_work[1] += kv_bytes_layer;
       const int i = ktimer[1].begin(s);
@@ -254,19 +268,42 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
                            dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
       ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
     }
-    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.attn, 0, H * hd, L.o_w, D, H * hd, dw.hid, D, nullptr, B, EPI_F32_RESID,
-                    plain, s));
-    // ln2 -> bf16 rows (one small kernel) -> TMA-streamed gate|up GEMV with the SiLU*up epilogue
-    CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
-    CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.gu_w, 2 * F, D, dw.act, F, B, EPI_BF16_SILUMUL, s));
-    CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.act, 0, F, L.down_w, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, plain,
-                    s));
+    if (tm & 2)
+      CUDA_TRY(t_gemv_tma(this, dw.attn, H * hd, L.o_w, L.o_wb, D, H * hd, dw.hid, D, nullptr, B, EPI_F32_RESID, sms,
+                          nullptr, s));
+    else
+      CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.attn, 0, H * hd, L.o_w, D, H * hd, dw.hid, D, nullptr, B,
+                      EPI_F32_RESID, plain, s));
+    if (tm & 4) {
+      CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
+      CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.gu_w, L.gu_wb, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL, sms,
+                          nullptr, s));
+    } else {
+      GemvAux na;
+      na.gamma = L.ln2;
+      na.eps = m.rms_eps;
+      CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.hid, 2, D, L.gu_w, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL,
+                      na, s));
+    }
+    if (tm & 8)
+      CUDA_TRY(t_gemv_tma(this, dw.act, F, L.down_w, L.down_wb, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, sms,
+                          nullptr, s));
+    else
+      CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.act, 0, F, L.down_w, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID,
+                      plain, s));
   }
-  GemvAux la;  // final RMSNorm (f32 rows) -> lm_head (hi/lo f32 input) -> fused greedy argmax
+  // final RMSNorm -> lm_head -> fused greedy argmax (f32 lm_head input, R7)
+  GemvAux la;
   la.keys = dw.keys;
-  CUDA_TRY(rmsnorm(dw.hid, D, W.final_norm, dw.xf, 1, D, B, D, m.rms_eps, s));
-  CUDA_TRY(t_gemv(this, NOVA_K_LM_HEAD, dw.xf, 1, D, W.lm_head, m.vocab, D, dw.logits, m.vocab, nullptr, B,
-                  EPI_F32_ARGMAX, la, s));
+  if (tm & 16) {  // bf16 hi + lo rows into the streaming GEMV (two products)
+    CUDA_TRY(rmsnorm(dw.hid, D, W.final_norm, dw.xb, 2, D, B, D, m.rms_eps, s));
+    CUDA_TRY(t_gemv_tma(this, dw.xb, D, W.lm_head, W.lm_head_b, m.vocab, D, dw.logits, m.vocab, nullptr, B,
+                        EPI_F32_ARGMAX, sms, &la, s, dw.xb + (size_t)B * D, NOVA_K_LM_HEAD));
+  } else {
+    CUDA_TRY(rmsnorm(dw.hid, D, W.final_norm, dw.xf, 1, D, B, D, m.rms_eps, s));
+    CUDA_TRY(t_gemv(this, NOVA_K_LM_HEAD, dw.xf, 1, D, W.lm_head, m.vocab, D, dw.logits, m.vocab, nullptr, B,
+                    EPI_F32_ARGMAX, la, s));
+  }
   CUDA_TRY(argmax_finalize(dw.keys, B, dw.tok, dw.rows, d_last, -1, s));
   CUDA_TRY(cudaMemcpyAsync(dw.h_tok, dw.tok, B * sizeof(int), cudaMemcpyDeviceToHost, s));
   if (cfg.debug_keep_logits)

@@ -36,14 +36,14 @@ def nova_op_gemv(X, W, Y, bias, N, K, B, epi, x_f32=None, ldx=None, ldy=None, st
 _ws_cache = {}
 
 
-def nova_op_gemv_tma(X, W, Y, bias, N, K, B, epi, ldx=None, ldy=None, stream=None):
+def nova_op_gemv_tma(X, W, Y, bias, N, K, B, epi, ldx=None, ldy=None, max_ctas=0, stream=None):
     dev = X.device
     if dev not in _ws_cache:
         _ws_cache[dev] = (torch.empty(16 * 16 * 160000, dtype=torch.float32, device=dev),
                           torch.zeros(8192, dtype=torch.int32, device=dev))
     ws, tk = _ws_cache[dev]
     check(lib().nova_op_gemv_tma(_p(X), ldx or X.stride(0), _p(W), N, K, _p(Y), ldy or Y.stride(0), _p(bias), B,
-                                 epi, _p(ws), _p(tk), _s(stream)), "gemv_tma")
+                                 epi, _p(ws), _p(tk), max_ctas, _s(stream)), "gemv_tma")
 
 
 def nova_op_flash_attn(qkv, out, S, H, KV, hd, causal, max_ctas=0, stream=None):
@@ -86,9 +86,11 @@ def nova_op_layernorm(x, gamma, beta, y, M, d, eps, stream=None):
                                   _s(stream)), "layernorm")
 
 
-def nova_op_rmsnorm(x, gamma, y, M, d, eps, stream=None):
-    check(lib().nova_op_rmsnorm(_p(x), x.stride(0), _p(gamma), _p(y), int(y.dtype == torch.float32), y.stride(0),
-                                M, d, eps, _s(stream)), "rmsnorm")
+def nova_op_rmsnorm(x, gamma, y, M, d, eps, y_mode=None, stream=None):
+    """y_mode: 0 bf16, 1 f32 (default from y's dtype), 2 bf16 hi rows then bf16 lo rows (y [2M][d])."""
+    mode = int(y.dtype == torch.float32) if y_mode is None else y_mode
+    check(lib().nova_op_rmsnorm(_p(x), x.stride(0), _p(gamma), _p(y), mode, y.stride(0), M, d, eps, _s(stream)),
+          "rmsnorm")
 
 
 def nova_op_patchify(pix, P, T, merge, X0, stream=None):
@@ -115,3 +117,18 @@ def nova_op_embed(table, d, ids, rows, last_tok, out, n, stream=None):
 def nova_op_argmax(logits, V, n, out_tok, rows=None, last_tok=None, single_slot=-1, stream=None):
     check(lib().nova_op_argmax(_p(logits), logits.stride(0), V, n, _p(out_tok), _p(rows), _p(last_tok),
                                single_slot, _s(stream)), "argmax")
+
+
+def nova_op_block_weights(W, Wb, N, K, stream=None):
+    check(lib().nova_op_block_weights(_p(W), _p(Wb), N, K, _s(stream)), "block_weights")
+
+
+def nova_op_gemv_stream(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_ctas=0, ldx=None, ldy=None,
+                        stream=None):
+    dev = X.device
+    if dev not in _ws_cache:
+        _ws_cache[dev] = (torch.empty(16 * 16 * 160000, dtype=torch.float32, device=dev),
+                          torch.zeros(8192, dtype=torch.int32, device=dev))
+    ws, tk = _ws_cache[dev]
+    check(lib().nova_op_gemv_stream(_p(X), _p(X_lo), ldx or X.stride(0), _p(Wb), N, K, _p(Y), ldy or Y.stride(0),
+                                    _p(bias), B, epi, _p(ws), _p(tk), _p(keys), max_ctas, _s(stream)), "gemv_stream")

@@ -46,8 +46,11 @@ def test_norm_on_load_is_bitwise_rmsnorm_then_gemv(N, K, epi):
         assert torch.equal(Y0.view(torch.int16), Y1.view(torch.int16)), B
 
 
-@pytest.mark.parametrize("H,KV,hd,D", [(4, 2, 32, 128), (28, 4, 128, 3584)])
-def test_qkv_rope_kv_append_matches_oracle(H, KV, hd, D):
+@pytest.mark.parametrize("H,KV,hd,D,tma", [(4, 2, 32, 128, 0), (28, 4, 128, 3584, 0), (28, 4, 128, 3584, 1),
+                                           (12, 2, 128, 1536, 1)])
+def test_qkv_rope_kv_append_matches_oracle(H, KV, hd, D, tma):
+    """tma = 0: register GEMV with RMSNorm on load; tma = 1: persistent TMA kernel on the
+    bf16-normalized rows (rmsnorm kernel first)."""
     rng = np.random.default_rng(H * 7 + D)
     N = (H + 2 * KV) * hd
     W = rand_bf16(rng, (N, D), D ** -0.5)
@@ -70,9 +73,16 @@ def test_qkv_rope_kv_append_matches_oracle(H, KV, hd, D):
         pool = torch.zeros(2, n_pages, 2, KV, 64, hd, dtype=torch.bfloat16, device="cuda")
         rows = torch.from_numpy(r).cuda()
         Q = torch.zeros(B, N, dtype=torch.bfloat16, device="cuda")
-        O.nova_op_gemv_fused(torch.from_numpy(Xh[:B]).cuda(), O.XM_NORM_BF16, dW, Q, db, N, D, B, O.EPI_QKV_ROPE_KV,
-                             gamma=dg, eps=eps, H=H, KV=KV, hd=hd, theta=theta, rows=rows, kv_pool=pool, layer=1,
-                             n_pages=n_pages, block_tables=bt)
+        Xd = torch.from_numpy(Xh[:B]).cuda()
+        if tma:
+            xb = torch.empty(B, D, dtype=torch.bfloat16, device="cuda")
+            O.nova_op_rmsnorm(Xd, dg, xb, B, D, eps)
+            O.nova_op_gemv_fused(xb, O.XM_BF16, dW, Q, db, N, D, B, O.EPI_QKV_ROPE_KV, H=H, KV=KV, hd=hd,
+                                 theta=theta, rows=rows, kv_pool=pool, layer=1, n_pages=n_pages, block_tables=bt)
+        else:
+            O.nova_op_gemv_fused(Xd, O.XM_NORM_BF16, dW, Q, db, N, D, B, O.EPI_QKV_ROPE_KV,
+                                 gamma=dg, eps=eps, H=H, KV=KV, hd=hd, theta=theta, rows=rows, kv_pool=pool, layer=1,
+                                 n_pages=n_pages, block_tables=bt)
         torch.cuda.synchronize()
         # oracle: bf16-rounded normalized input (the GEMV operand), f64 linear + bias, RoPE at pos
         from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
@@ -131,3 +141,51 @@ def test_lm_head_fused_argmax(V_, D):
         assert last.cpu().numpy()[6 - b] == toks[b]
     assert lg[0, i] == lg[0, j] and toks[0] == i              # exact tie -> lowest index
     assert int(keys.abs().sum().item()) == 0                  # finalize leaves the keys zeroed
+
+
+@pytest.mark.parametrize("N,K", [(4608, 3584), (3584, 18944), (37888, 3584), (256, 128)])
+def test_streaming_layout_gemv_bitwise_equals_rowmajor_and_is_grid_invariant(N, K):
+    """block_weights + bulk-copy tiles == tensor-map tiles of the row-major weight (bitwise),
+    on every SM budget, and both match the oracle linear."""
+    rng = np.random.default_rng(N + 2 * K)
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    X = rand_bf16(rng, (16, K))
+    dW, dX = bf16_dev(W), bf16_dev(X)
+    Wb = torch.empty_like(dW)
+    O.nova_op_block_weights(dW, Wb, N, K)
+    ref = V.linear(X.astype(np.float64), W.astype(np.float64))
+    for B in (1, 7, 16):
+        Y0 = torch.empty(B, N, dtype=torch.float32, device="cuda")
+        O.nova_op_gemv_tma(dX[:B], dW, Y0, None, N, K, B, O.EPI_F32_STORE)
+        torch.cuda.synchronize()
+        assert rel_inf(Y0.cpu().numpy(), ref[:B]) <= 1e-4
+        for ctas in (148, 24, 8):
+            Y1 = torch.empty_like(Y0)
+            O.nova_op_gemv_stream(dX[:B], Wb, Y1, None, N, K, B, O.EPI_F32_STORE, max_ctas=ctas)
+            torch.cuda.synchronize()
+            assert torch.equal(Y0, Y1), (B, ctas)
+
+
+def test_streaming_lm_head_hi_lo_argmax():
+    """Decode lm_head: RMSNorm -> bf16 hi/lo rows -> streaming GEMV with two products ->
+    f32 logits within 1e-4 of the oracle and the exact greedy argmax."""
+    rng = np.random.default_rng(77)
+    V_, D, B = 152064, 3584, 3
+    W = rand_bf16(rng, (V_, D), 2 * D ** -0.5)
+    gam = _gamma(rng, D)
+    Xh = (rng.standard_normal((B, D)) * 2).astype(np.float32)
+    dW, dg = bf16_dev(W), bf16_dev(gam)
+    Wb = torch.empty_like(dW)
+    O.nova_op_block_weights(dW, Wb, V_, D)
+    hl = torch.empty(2 * B, D, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_rmsnorm(torch.from_numpy(Xh).cuda(), dg, hl, B, D, 1e-6, y_mode=2)
+    keys = torch.zeros(B, dtype=torch.int64, device="cuda")
+    L = torch.empty(B, V_, dtype=torch.float32, device="cuda")
+    O.nova_op_gemv_stream(hl[:B], Wb, L, None, V_, D, B, O.EPI_F32_ARGMAX, X_lo=hl[B:], keys=keys, max_ctas=40)
+    tok = torch.empty(B, dtype=torch.int32, device="cuda")
+    O.nova_op_argmax_finalize(keys, B, tok)
+    torch.cuda.synchronize()
+    lg = L.cpu().numpy()
+    ref = V.linear(V.rms_norm(Xh.astype(np.float64), gam, 1e-6), W.astype(np.float64))
+    assert rel_inf(lg, ref) <= 1e-4
+    assert tok.cpu().numpy().tolist() == [V.argmax_lowest(lg[b]) for b in range(B)]
