@@ -43,6 +43,17 @@ enum {
 int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
                  int K, int epi, int max_ctas, void* stream);
 
+/* GEMM tile selection.  nova_op_gemm chooses, from the shape alone (never from max_ctas,
+ * so results stay bitwise independent of the partition), between single-CTA 128 x BN
+ * tiles and CTA-pair (tcgen05 cta_group::2, 2-CTA cluster) 256 x BN tiles.
+ * nova_op_gemm_mode(mode): 0 = automatic (default, or env NOVA_GEMM), 1 = single-CTA
+ * tiles only, 2 = CTA-pair tiles only, >= 1000 = exactly the tile pair * 1000 + BN
+ * (benchmarks); returns the previous mode.  Process-wide, not
+ * thread-safe against concurrent nova_op_gemm calls (a test / benchmark hook).
+ * nova_op_gemm_config(M, N, K): the tile the current mode picks, pair * 1000 + BN. */
+int nova_op_gemm_mode(int mode);
+int nova_op_gemm_config(int M, int N, int K);
+
 /* Decode linear (a7): Y[b][n] = sum_k X[b][k] W[n][k] (+bias) for B <= 16 rows.
  * X bf16 (x_f32 = 0) or f32 (x_f32 = 1).  N % 32 == 0, K % 32 == 0, ldx % 8 == 0.
  * Epilogues NOVA_EPI_BF16 / _SILUMUL / _F32_RESID / _F32_STORE.  Row b of Y is

@@ -20,6 +20,8 @@ U64 = C.c_uint64
 
 OPS_SIGNATURES = {
     "nova_op_gemm": [P, I, P, I, P, I, P, I, I, I, I, I, P],
+    "nova_op_gemm_mode": [I],
+    "nova_op_gemm_config": [I, I, I],
     "nova_op_gemv": [P, I, I, P, I, I, P, I, P, I, I, P],
     "nova_op_gemv_tma": [P, I, P, I, I, P, I, P, I, I, P, P, I, P],
     "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, I, P],

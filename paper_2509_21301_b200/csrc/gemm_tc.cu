@@ -11,6 +11,8 @@
 // two TMEM accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 // Output of a tile depends only on (A rows, W rows, K order): bitwise invariant to
 // the grid size (the SM budget), which co-exec == serial parity relies on.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -226,6 +228,203 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair kernel (cta_group::2)
+// A cluster of 2 CTAs on one TPC computes a 256 x BN tile: CTA r holds A rows [128r, 128r+128)
+// and W rows [r*BN/2, (r+1)*BN/2) of every K block in its own shared memory; the leader (rank 0)
+// issues one tcgen05.mma.cta_group::2 (M = 256) per 16-wide K step that reads both halves, and
+// each CTA's TMEM receives the accumulator rows of its own A half (128 lanes x BN columns).
+// Per SM and per 64-deep K block this moves 16 KB of A + BN/2 x 128 B of W from L2 for
+// 128 x BN x 64 MACs -- half the W traffic of the single-CTA tile, which is what holds the
+// 1-CTA kernel below ~75% of peak (L2 -> SM delivery, not the tensor pipe, is the limit).
+// Barriers (identical smem layout in both CTAs):
+//   full[s]   leader only: the leader's producer posts expect_tx(both halves); both CTAs' TMA
+//             (.cta_group::2) complete_tx on it;
+//   empty[s]  both CTAs: tcgen05.commit multicast (mask 0b11) when the MMAs reading stage s end;
+//   tfull[a]  both CTAs: commit multicast after the last K block of a tile;
+//   tempty[a] leader only: one arrive per epilogue warp of BOTH CTAs (16), remote for rank 1.
+// Output bits depend only on (A rows, W rows, K order) as in the 1-CTA kernel.
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int BNH = BN / 2;  // W rows per CTA
+  static constexpr int STAGES = 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BNH * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+NOVA_DEV uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+NOVA_DEV void cluster_sync2() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion is posted to the LEADER CTA's mbarrier (peer bit cleared).
+NOVA_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
+  const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(b), "r"(x), "r"(y)
+      : "memory");
+}
+NOVA_DEV void umma2_bf16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+NOVA_DEV void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+NOVA_DEV void mbar_arrive_rank(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(384, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank_in_cluster();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 16);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync2();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();
+
+  const int num_m = (g.M + 2 * BM - 1) / (2 * BM);
+  const int num_n = (g.N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int kblocks = (g.K + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs: own halves of A and W)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        const int mb = t % num_m, nb = t / num_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, mb * 2 * BM + rank * BM);
+          tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN + rank * Cfg::BNH);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * 256;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma2_bf16_ss(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                          (kb | k) != 0 ? 1u : 0u);
+          }
+          umma2_commit_both(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma2_commit_both(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue: 8 warps = 4 TMEM lane quarters x 2 column halves
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;
+    constexpr int NCH = BN / 32;  // 32-column chunks per tile
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = pair; t < tiles; t += npairs) {
+      const int mb = t % num_m, nb = t / num_m;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int m = mb * 2 * BM + (int)rank * BM + row;
+#pragma unroll 1
+      for (int c = half; c < NCH; c += 2) {
+        const int n0 = nb * BN + c * 32;
+        if (n0 >= g.N) break;  // ragged last N tile (warp-uniform)
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256 + c * 32, v);
+        if (m < g.M) epilogue32<EPI>(g, m, n0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_rank(&tempty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync2();  // all MMAs retired and both epilogues drained before the pair frees TMEM
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -288,35 +487,139 @@ cudaError_t dispatch_epi(const bf16* A, int lda, const bf16* W, int ldw, const G
   return cudaErrorInvalidValue;
 }
 
+template <int BN, int EPI>
+cudaError_t launch_pair(const bf16* A, int lda, const bf16* W, int ldw, const GemmArgs& g, int max_ctas,
+                        cudaStream_t s) {
+  using Cfg = Gemm2Cfg<BN>;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, g.M, g.K, lda, BM) || !make_map(&mb, W, g.N, g.K, ldw, Cfg::BNH))
+    return cudaErrorInvalidValue;
+  auto kern = gemm_tc2_kernel<BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
+  int pairs = max_ctas / 2;
+  if (pairs > tiles) pairs = tiles;
+  if (pairs < 1) pairs = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_use_pdl ? 2 : 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g);
+}
+
+template <int BN>
+cudaError_t dispatch_pair(const bf16* A, int lda, const bf16* W, int ldw, const GemmArgs& g, int epi, int max_ctas,
+                          cudaStream_t s) {
+  switch (epi) {
+    case EPI_BF16: return launch_pair<BN, EPI_BF16>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_BF16_QGELU: return launch_pair<BN, EPI_BF16_QGELU>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_BF16_GELU: return launch_pair<BN, EPI_BF16_GELU>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_BF16_SILUMUL: return launch_pair<BN, EPI_BF16_SILUMUL>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_F32_RESID: return launch_pair<BN, EPI_F32_RESID>(A, lda, W, ldw, g, max_ctas, s);
+    case EPI_F32_STORE: return launch_pair<BN, EPI_F32_STORE>(A, lda, W, ldw, g, max_ctas, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// GEMM tile configurations: (pair, BN).  eff = throughput of a full wave of that tile relative
+// to the 256x256 CTA-pair tile (B200 kbench); used only to rank configurations.
+struct TileCfg {
+  int pair, bn;
+  double eff;
+};
+constexpr TileCfg kTileCfgs[] = {
+    {1, 256, 1.00}, {1, 224, 0.97}, {1, 192, 0.95}, {1, 160, 0.91}, {1, 128, 0.86},
+    {0, 256, 0.80}, {0, 128, 0.74}, {0, 64, 0.60},
+};
+constexpr int kNumTileCfgs = (int)(sizeof(kTileCfgs) / sizeof(kTileCfgs[0]));
+
+// 0 = auto, 1 = single-CTA tiles only, 2 = CTA-pair tiles only, >= 1000 = exactly the tile
+// pair * 1000 + BN (env NOVA_GEMM)
+int g_gemm_mode = -1;
+int gemm_mode() {
+  if (g_gemm_mode < 0) {
+    const char* e = getenv("NOVA_GEMM");
+    g_gemm_mode = e ? atoi(e) : 0;
+  }
+  return g_gemm_mode;
+}
+
 }  // namespace
+
+int gemm_tc_set_mode(int mode) {
+  const int prev = gemm_mode();
+  g_gemm_mode = mode;
+  return prev;
+}
+
+// Chosen tile configuration for an M x N x K GEMM: index into kTileCfgs, encoded as
+// pair * 1000 + BN (e.g. 1256 = CTA pair, 256 x 256 tile).  Shape only -> bitwise invariance.
+static int gemm_tc_config_index(int M, int N, int K) {
+  (void)K;
+  // Modelled time = waves x per-tile time on the WHOLE GPU (148 SMs, 74 pairs), NOT on the
+  // partition's budget: the tiling must not depend on the partition so that co-executed passes
+  // stay bitwise equal to serial ones.  Per-tile time ~ (rows per SM = 128) x BN / eff.
+  const int mode = gemm_mode();
+  double best = 1e30;
+  int bi = -1;
+  for (int i = 0; i < kNumTileCfgs; ++i) {
+    const TileCfg& c = kTileCfgs[i];
+    if ((mode == 1 && c.pair) || (mode == 2 && !c.pair)) continue;
+    if (mode >= 1000 && mode != c.pair * 1000 + c.bn) continue;  // one forced tile (benchmarks)
+    if (!c.pair && N % c.bn) continue;  // the single-CTA kernel needs whole N tiles
+    const int rows = c.pair ? 2 * BM : BM;
+    const int units = c.pair ? 74 : 148;
+    const long tiles = (long)((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
+    const double t = (double)((tiles + units - 1) / units) * BM * c.bn / c.eff;  // per-SM work of a tile
+    if (t < best - 1e-9) {
+      best = t;
+      bi = i;
+    }
+  }
+  return bi;
+}
+
+int gemm_tc_config(int M, int N, int K) {
+  const int i = gemm_tc_config_index(M, N, K);
+  return i < 0 ? -1 : kTileCfgs[i].pair * 1000 + kTileCfgs[i].bn;
+}
 
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M, int N,
                     int K, int epi, int max_ctas, cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (N % 64 != 0 || K <= 0 || (lda % 8) || (ldw % 8) || (ldc % 8)) return cudaErrorInvalidValue;
   GemmArgs g{C, bias, M, N, K, ldc};
-  // Tile width by modelled time = waves x per-tile time: waves = ceil(tiles / CTAs) (wave
-  // quantisation on the partition's SM budget), per-tile time ~ BN / efficiency(BN) (narrow
-  // tiles re-read A more often: measured ~0.92 at 128, ~0.75 at 64 of the 256-wide rate).
-  // The reference budget is the whole GPU (148 SMs), NOT max_ctas: the tiling must not depend
-  // on the partition so that co-executed passes stay bitwise equal to serial ones.
-  const int mblk = (M + BM - 1) / BM;
-  const int ctas = 148;
-  double best = 1e30;
-  int bn = 64;
-  const int cand[3] = {256, 128, 64};
-  const double eff[3] = {1.0, 0.92, 0.75};
-  for (int i = 0; i < 3; ++i) {
-    if (N % cand[i]) continue;
-    const long tiles = (long)mblk * (N / cand[i]);
-    const double t = (double)((tiles + ctas - 1) / ctas) * cand[i] / eff[i];
-    if (t < best - 1e-9) {
-      best = t;
-      bn = cand[i];
+  const int ci = gemm_tc_config_index(M, N, K);
+  if (ci < 0) return cudaErrorInvalidValue;
+  const TileCfg& c = kTileCfgs[ci];
+  if (c.pair) {  // pairs = max(1, max_ctas / 2)
+    switch (c.bn) {
+      case 256: return dispatch_pair<256>(A, lda, W, ldw, g, epi, max_ctas, s);
+      case 224: return dispatch_pair<224>(A, lda, W, ldw, g, epi, max_ctas, s);
+      case 192: return dispatch_pair<192>(A, lda, W, ldw, g, epi, max_ctas, s);
+      case 160: return dispatch_pair<160>(A, lda, W, ldw, g, epi, max_ctas, s);
+      case 128: return dispatch_pair<128>(A, lda, W, ldw, g, epi, max_ctas, s);
     }
+    return cudaErrorInvalidValue;
   }
-  if (bn == 256) return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
-  if (bn == 128) return dispatch_epi<128>(A, lda, W, ldw, g, epi, max_ctas, s);
+  if (c.bn == 256) return dispatch_epi<256>(A, lda, W, ldw, g, epi, max_ctas, s);
+  if (c.bn == 128) return dispatch_epi<128>(A, lda, W, ldw, g, epi, max_ctas, s);
   return dispatch_epi<64>(A, lda, W, ldw, g, epi, max_ctas, s);
 }
 

@@ -55,6 +55,12 @@ enum Epi {
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M,
                     int N, int K, int epi, int max_ctas, cudaStream_t s);
 
+// Tile-configuration override (0 auto, 1 single-CTA tiles only, 2 CTA-pair tiles only); returns
+// the previous mode.  Test / benchmark hook: a forced mode still picks its tile by shape only.
+int gemm_tc_set_mode(int mode);
+// Tile chosen for a shape: pair * 1000 + BN (e.g. 1256 = CTA pair, 256 x 256 tile).
+int gemm_tc_config(int M, int N, int K);
+
 // Decode GEMV (B <= 16 rows): Y[b][n] = sum_k X[b][k] W[n][k] (+bias), epilogue as above.
 // X bf16 (x_f32 = 0) or f32 (x_f32 = 1, split hi/lo on the tensor core).
 cudaError_t gemv(const void* X, int x_f32, int ldx, const bf16* W, int N, int K, void* Y, int ldy,

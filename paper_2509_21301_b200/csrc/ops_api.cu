@@ -15,6 +15,8 @@ int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ld
   return st(gemm_tc((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, (const bf16*)bias, M, N, K, epi, max_ctas,
                     S(stream)));
 }
+int nova_op_gemm_mode(int mode) { return gemm_tc_set_mode(mode); }
+int nova_op_gemm_config(int M, int N, int K) { return gemm_tc_config(M, N, K); }
 int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias,
                  int B, int epi, void* stream) {
   return st(gemv(X, x_f32, ldx, (const bf16*)W, N, K, Y, ldy, (const bf16*)bias, B, epi, S(stream)));

@@ -27,6 +27,16 @@ def nova_op_gemm(A, W, C, bias, M, N, K, epi, max_ctas=148, lda=None, ldw=None, 
                              _p(bias), M, N, K, epi, max_ctas, _s(stream)), "gemm")
 
 
+def nova_op_gemm_mode(mode: int) -> int:
+    """0 = automatic tile choice, 1 = single-CTA tiles only, 2 = CTA-pair tiles only; returns the previous mode."""
+    return lib().nova_op_gemm_mode(mode)
+
+
+def nova_op_gemm_config(M: int, N: int, K: int) -> int:
+    """Tile the current mode picks for this shape: pair * 1000 + BN."""
+    return lib().nova_op_gemm_config(M, N, K)
+
+
 def nova_op_gemv(X, W, Y, bias, N, K, B, epi, x_f32=None, ldx=None, ldy=None, stream=None):
     xf = int(X.dtype == torch.float32) if x_f32 is None else x_f32
     check(lib().nova_op_gemv(_p(X), xf, ldx or X.stride(0), _p(W), N, K, _p(Y), ldy or Y.stride(0), _p(bias), B,

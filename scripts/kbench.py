@@ -80,6 +80,9 @@ def bench_gemv(iters):
         del Ws
 
 
+GEMM_MODES = [0]
+
+
 def bench_gemm(iters):
     cases = [("vit_qkv", 4888, 3840, 1280, O.EPI_BF16), ("vit_proj", 4888, 1280, 1280, O.EPI_F32_RESID),
              ("vit_fc1", 4888, 5120, 1280, O.EPI_BF16_QGELU), ("vit_fc2", 4888, 1280, 5120, O.EPI_F32_RESID),
@@ -92,12 +95,18 @@ def bench_gemm(iters):
         bias = rnd((N,), scale=0.1) if epi != O.EPI_BF16_SILUMUL else None
         nout = N // 2 if epi == O.EPI_BF16_SILUMUL else N
         C = torch.zeros(M, nout, device="cuda", dtype=torch.float32 if epi == O.EPI_F32_RESID else torch.bfloat16)
-        for sms in (148, 100):
-            ms = timeit(lambda i: O.nova_op_gemm(A, W, C, bias, M, N, K, epi, max_ctas=sms), iters, 1)
-            tf = 2.0 * M * N * K / ms / 1e9
-            print(json.dumps({"kernel": "gemm_tc", "shape": name, "M": M, "N": N, "K": K, "ctas": sms,
-                              "us": round(ms * 1e3, 1), "TFLOP/s": round(tf, 1), "frac_tensor": round(tf / TFL, 3)}),
-                  flush=True)
+        for mode in GEMM_MODES:
+            prev = O.nova_op_gemm_mode(mode)
+            tile = O.nova_op_gemm_config(M, N, K)
+            for sms in ((148, 100) if mode == 0 else (148,)):
+                if tile < 0:
+                    continue
+                ms = timeit(lambda i: O.nova_op_gemm(A, W, C, bias, M, N, K, epi, max_ctas=sms), iters, 1)
+                tf = 2.0 * M * N * K / ms / 1e9
+                print(json.dumps({"kernel": "gemm_tc", "shape": name, "M": M, "N": N, "K": K, "ctas": sms,
+                                  "mode": mode, "tile": tile, "us": round(ms * 1e3, 1), "TFLOP/s": round(tf, 1),
+                                  "frac_tensor": round(tf / TFL, 3)}), flush=True)
+            O.nova_op_gemm_mode(prev)
 
 
 def bench_attn(iters):
@@ -136,7 +145,10 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=None)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--gemm-modes", default="0", help="comma list: 0 auto, 1 single-CTA, 2 pair, or a tile code "
+                    "pair*1000+BN (e.g. 1224)")
     a = ap.parse_args()
+    GEMM_MODES[:] = [int(x) for x in a.gemm_modes.split(",")]
     for nm, fn in [("gemv", bench_gemv), ("gemm", bench_gemm), ("attn", bench_attn), ("dattn", bench_dattn)]:
         if a.only in (None, nm):
             fn(a.iters)

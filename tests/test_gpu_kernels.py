@@ -25,11 +25,22 @@ def interleave_gate_up(wg: np.ndarray, wu: np.ndarray, blk: int = 16) -> np.ndar
     return out
 
 
-GEMM_SHAPES = [(16, 64, 64), (12, 256, 128), (200, 384, 1176), (1286, 4608, 3584), (777, 1280, 5120), (4888, 3840, 1280)]
+GEMM_SHAPES = [(16, 64, 64), (12, 256, 128), (200, 384, 1176), (1286, 4608, 3584), (777, 1280, 5120), (4888, 3840, 1280),
+               (300, 1216, 200), (513, 448, 64)]
+
+
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "cta1", "pair"])
+def gemm_mode(request):
+    """Tile family: automatic, single-CTA 128 x BN only, CTA-pair (cta_group::2) 256 x BN only."""
+    prev = O.nova_op_gemm_mode(request.param)
+    yield request.param
+    O.nova_op_gemm_mode(prev)
 
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_tc_epilogues(M, N, K):
+def test_gemm_tc_epilogues(M, N, K, gemm_mode):
+    if gemm_mode == 1 and N % 64:
+        pytest.skip("single-CTA tiles need N % 64 == 0")
     rng = np.random.default_rng(M + N + K)
     A = rand_bf16(rng, (M, K))
     W = rand_bf16(rng, (N, K), K ** -0.5)
@@ -53,9 +64,9 @@ def test_gemm_tc_epilogues(M, N, K):
     assert rel_inf(Fo.cpu().numpy(), ref_nb) <= 1e-4
 
 
-def test_gemm_silu_mul_and_grid_invariance():
+@pytest.mark.parametrize("M,F,K", [(300, 512, 384), (1286, 1216, 448)])
+def test_gemm_silu_mul_and_grid_invariance(M, F, K, gemm_mode):
     rng = np.random.default_rng(7)
-    M, F, K = 300, 512, 384
     A = rand_bf16(rng, (M, K))
     Wg, Wu = rand_bf16(rng, (F, K), K ** -0.5), rand_bf16(rng, (F, K), K ** -0.5)
     Wi = interleave_gate_up(Wg, Wu)
