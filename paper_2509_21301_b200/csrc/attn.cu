@@ -669,9 +669,9 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
 
 cudaError_t flash_attn(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                        int max_ctas, cudaStream_t s) {
-  // tcgen05 kernel for the bidirectional ViT attention (1.6x the mma.sync kernel, scripts/kbench.py);
-  // the causal prefill keeps the mma.sync kernel until the tcgen05 one balances causal tiles.
-  if (!causal && (hd == 80 || hd == 128)) return flash_attn_tc(qkv, ld, out, ldo, S, H, KV, hd, causal, max_ctas, s);
+  // tcgen05 persistent kernel (v3) for the bidirectional ViT attention and the causal GQA prefill
+  // (longest-first snake schedule of the causal Q-tile pairs); mma.sync kernel for other head dims.
+  if (hd == 80 || hd == 128) return flash_attn_tc(qkv, ld, out, ldo, S, H, KV, hd, causal, max_ctas, s);
   return flash_attn_mma(qkv, ld, out, ldo, S, H, KV, hd, causal, s);
 }
 

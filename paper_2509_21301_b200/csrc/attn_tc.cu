@@ -565,8 +565,10 @@ NOVA_DEV void tmem_ld_wait32(uint32_t* r) {
 // the last chunk to finish.  So the numerics are identical for any SM budget, and on the full
 // GPU the tail wave is ~148 short chunks instead of `rem` full-length units.
 struct Fmha3Plan {
-  int n_q2, n_tiles, units, full, rem, KC, total;
-  __host__ __device__ Fmha3Plan(int S, int H, int split = 1) {
+  int n_q2, n_tiles, units, full, rem, KC, total, causal, H;
+  __host__ __device__ Fmha3Plan(int S, int H_, int split = 1, int causal_ = 0) {
+    H = H_;
+    causal = causal_;
     n_q2 = (S + 2 * FBM - 1) / (2 * FBM);
     n_tiles = (S + FBN - 1) / FBN;
     units = n_q2 * H;
@@ -579,15 +581,26 @@ struct Fmha3Plan {
       if (KC > 16) KC = 16;
       if (KC < 1) KC = 1;
     }
-    if (KC == 1 || !split) {
+    if (KC == 1 || !split || causal) {
       KC = 1;
       full = units;
       rem = 0;
     }
     total = full + rem * KC;
   }
-  // unit -> (head, q pair, key tiles [t0, t1), split slot or -1, chunk index)
+  // unit -> (head, q pair, key tiles [t0, t1), split slot or -1, chunk index).
+  // Causal: units run longest first (q pair n_q2-1 down to 0, heads fastest); the pair's key
+  // range ends at its B tile's diagonal.
   __host__ __device__ void decode(int u, int& h, int& pr, int& t0, int& t1, int& slot, int& ch) const {
+    if (causal) {
+      pr = n_q2 - 1 - u / H;
+      h = u % H;
+      slot = -1;
+      ch = 0;
+      t0 = 0;
+      t1 = min(n_tiles, 2 * pr + 2);
+      return;
+    }
     int base = u;
     ch = 0;
     slot = -1;
@@ -601,9 +614,17 @@ struct Fmha3Plan {
     t0 = slot < 0 ? 0 : (ch * n_tiles) / KC;
     t1 = slot < 0 ? n_tiles : ((ch + 1) * n_tiles) / KC;
   }
+  // k-th unit of CTA c out of G: snake order over rounds (c, then G-1-c, ...), so with units
+  // sorted longest first the per-CTA sums even out; -1 = no unit this round, -2 = done.
+  // Which CTA runs a unit never changes its numerics (a unit is computed whole or as fixed chunks).
+  __host__ __device__ int unit_of(int k, int c, int G) const {
+    if (k * G >= total) return -2;
+    const int u = k * G + ((k & 1) ? G - 1 - c : c);
+    return u < total ? u : -1;
+  }
 };
 
-template <int HD>
+template <int HD, bool CAUSAL>
 __global__ void __launch_bounds__(384, 1)
     fmha3_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, int ldo, int S, int H, int KV,
                  float scale_log2, float* __restrict__ ws, int* __restrict__ tickets, int split) {
@@ -629,7 +650,7 @@ __global__ void __launch_bounds__(384, 1)
   int* s_last = reinterpret_cast<int*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Fmha3Plan plan(S, H, split);
+  const Fmha3Plan plan(S, H, split, CAUSAL ? 1 : 0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
@@ -646,7 +667,8 @@ __global__ void __launch_bounds__(384, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (warp == 0 && lane == 0) {  // ---------------- TMA producer
       int it = 0, nu = 0;
-      for (int u = blockIdx.x; u < plan.total; u += gridDim.x, ++nu) {
+      for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
+        if (u < 0) continue;
         int h, pr, t0, t1, slot, ch;
         plan.decode(u, h, pr, t0, t1, slot, ch);
         const int kvh = h / (H / KV), q0 = pr * 2 * FBM;
@@ -671,6 +693,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + c * FBN * 128, &tm, &v_full[st], vcol + c * CHUNK,
                         j * FBN);
         }
+        ++nu;
       }
     } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer
       const uint32_t tS[2] = {tbase, tbase + FBN};
@@ -693,7 +716,8 @@ __global__ void __launch_bounds__(384, 1)
                        (!first || k > 0) ? 1u : 0u);
       };
       int it = 0, nu = 0;
-      for (int u = blockIdx.x; u < plan.total; u += gridDim.x, ++nu) {
+      for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
+        if (u < 0) continue;
         int h, pr, t0, t1, slot, ch;
         plan.decode(u, h, pr, t0, t1, slot, ch);
         const int n = t1 - t0;
@@ -726,6 +750,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
         umma_commit(o_done);
+        ++nu;
       }
     }
   } else {  // ---------------- softmax warpgroups: x = 0 (warps 4-7, tile A), 1 (warps 8-11, tile B)
@@ -735,10 +760,12 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tS = tbase + x * FBN + lane_off, tO = tbase + (2 + x) * FBN + lane_off;
     int it = 0, nu = 0;
-    for (int u = blockIdx.x; u < plan.total; u += gridDim.x, ++nu) {
+    for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
+      if (u < 0) continue;
       int h, pr, t0, t1, slot, ch;
       plan.decode(u, h, pr, t0, t1, slot, ch);
       const int qrow = pr * 2 * FBM + x * FBM + row;
+      const int qlo = pr * 2 * FBM + x * FBM;  // first query row of this warpgroup's tile
       float m = -1e30f, l = 0.f;
       for (int j = t0; j < t1; ++j, ++it) {
         mbar_wait(&s_full[x], it & 1);
@@ -749,7 +776,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int c = 0; c < FBN / 32; ++c) tmem_ld_wait32(sv + c * 32);
         const int k0 = j * FBN;
-        if (k0 + FBN > S) {  // keys beyond S (TMA zero-filled rows) must not contribute
+        if (CAUSAL) {  // keys after the query row (and beyond S) are masked; interior tiles skip the test
+          if (k0 + FBN - 1 > qlo || k0 + FBN > S) {
+            const int lim = min(S, qrow + 1);
+#pragma unroll
+            for (int i = 0; i < FBN; ++i)
+              if (k0 + i >= lim) sv[i] = __float_as_uint(-1e30f);
+          }
+        } else if (k0 + FBN > S) {  // keys beyond S (TMA zero-filled rows) must not contribute
 #pragma unroll
           for (int i = 0; i < FBN; ++i)
             if (k0 + i >= S) sv[i] = __float_as_uint(-1e30f);
@@ -881,6 +915,7 @@ __global__ void __launch_bounds__(384, 1)
           if (threadIdx.x == 128) tickets[grp] = 0;
         }
       }
+      ++nu;
     }
   }
   tc_fence_before();
@@ -952,12 +987,12 @@ cudaError_t fmha2_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int
 float* g_fmha_ws = nullptr;  // split-chunk partials: <= 148 chunks x 256 rows x (hd + 2) f32
 int* g_fmha_tickets = nullptr;
 
-template <int HD>
+template <int HD, bool CAUSAL>
 cudaError_t fmha3_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int max_ctas,
                          cudaStream_t s) {
   CUtensorMap tm;
   if (!make_qkv_map(&tm, qkv, S, ld)) return cudaErrorInvalidValue;
-  auto kern = fmha3_kernel<HD>;
+  auto kern = fmha3_kernel<HD, CAUSAL>;
   static bool set = false;
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Ft3Cfg<HD>::SMEM);
@@ -971,7 +1006,7 @@ cudaError_t fmha3_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int
       return cudaErrorMemoryAllocation;
   }
   static const int split = getenv("NOVA_FMHA_SPLIT") ? atoi(getenv("NOVA_FMHA_SPLIT")) : 1;  // experiments only
-  const Fmha3Plan plan(S, H, split);
+  const Fmha3Plan plan(S, H, split, CAUSAL ? 1 : 0);
   int grid = max_ctas > 0 ? max_ctas : 148;
   if (grid > plan.total) grid = plan.total;
   const float sl2 = LOG2E_F / sqrtf((float)HD);
@@ -984,10 +1019,12 @@ cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, in
                           int max_ctas, cudaStream_t s) {
   if (S <= 0) return cudaSuccess;
   if (ld % 8 || H % KV || ldo % 8) return cudaErrorInvalidValue;
-  if (g_fmha_version == 3 && !causal) {
+  if (g_fmha_version == 3) {
     switch (hd) {
-      case 80: return fmha3_launch<80>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
-      case 128: return fmha3_launch<128>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
+      case 80: return causal ? fmha3_launch<80, true>(qkv, ld, out, ldo, S, H, KV, max_ctas, s)
+                             : fmha3_launch<80, false>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
+      case 128: return causal ? fmha3_launch<128, true>(qkv, ld, out, ldo, S, H, KV, max_ctas, s)
+                              : fmha3_launch<128, false>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
     }
     return cudaErrorInvalidValue;
   }

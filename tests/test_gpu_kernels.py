@@ -368,3 +368,30 @@ def test_flash_attn_vit_shape_grid_invariant():
         ref = V.attention_full(t[:, 0, h:h + 1].astype(np.float64), t[:, 1, h:h + 1].astype(np.float64),
                                t[:, 2, h:h + 1].astype(np.float64), hd ** -0.5)
         assert rel_inf(got[:, h:h + 1], ref) <= 2e-2, h
+
+
+@pytest.mark.parametrize("S", [1286, 2044, 257])
+def test_flash_attn_prefill_causal_grid_invariant(S):
+    """7B prefill shape (28 query / 4 KV heads, hd 128, causal): the persistent tcgen05 kernel
+    runs the Q-tile pairs longest first in a snake order over the CTAs; output must not depend
+    on the SM budget and matches the oracle on the first and last head of two KV groups."""
+    rng = np.random.default_rng(S)
+    H, KV, hd = 28, 4, 128
+    qkv = rand_bf16(rng, (S, (H + 2 * KV) * hd))
+    d = bf16_dev(qkv)
+    outs = []
+    for ctas in (148, 100, 37, 8):
+        out = torch.empty(S, H * hd, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_flash_attn(d, out, S, H, KV, hd, 1, max_ctas=ctas)
+        torch.cuda.synchronize()
+        outs.append(out)
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16))
+    got = bf16_host(outs[0]).reshape(S, H, hd)
+    q = qkv[:, :H * hd].reshape(S, H, hd).astype(np.float64)
+    k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd).astype(np.float64)
+    v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd).astype(np.float64)
+    for h in (0, 6, 7, 27):
+        g = h // (H // KV)
+        ref = V.attention_causal_gqa(q[:, h:h + 1], k[:, g:g + 1], v[:, g:g + 1], hd ** -0.5, 0)
+        assert rel_inf(got[:, h:h + 1], ref) <= 2e-2, h
