@@ -565,12 +565,13 @@ NOVA_DEV void tmem_ld_wait32(uint32_t* r) {
 // the last chunk to finish.  So the numerics are identical for any SM budget, and on the full
 // GPU the tail wave is ~148 short chunks instead of `rem` full-length units.
 struct Fmha3Plan {
-  int n_q2, n_tiles, units, full, rem, KC, total, causal, H;
-  __host__ __device__ Fmha3Plan(int S, int H_, int split = 1, int causal_ = 0) {
+  int n_q2, n_tiles, units, full, rem, KC, total, causal, H, kt;
+  __host__ __device__ Fmha3Plan(int S, int H_, int split = 1, int causal_ = 0, int kt_ = FBN) {
     H = H_;
     causal = causal_;
+    kt = kt_;
     n_q2 = (S + 2 * FBM - 1) / (2 * FBM);
-    n_tiles = (S + FBN - 1) / FBN;
+    n_tiles = (S + kt - 1) / kt;
     units = n_q2 * H;
     full = (units / 148) * 148;
     rem = units - full;
@@ -598,7 +599,7 @@ struct Fmha3Plan {
       slot = -1;
       ch = 0;
       t0 = 0;
-      t1 = min(n_tiles, 2 * pr + 2);
+      t1 = min(n_tiles, (2 * pr + 2) * FBM / kt);
       return;
     }
     int base = u;
@@ -926,11 +927,369 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// v4: v3's two-Q-tile ping-pong with 64-key tiles and DOUBLE-BUFFERED S per Q tile.  In v3 the
+// S MMA of tile j+1 could only start after softmax j had produced P_j (P aliases S), so every
+// tile paid the chain P_j -> PV_j -> S_{j+1} -> tcgen05.ld before the exps could restart
+// (measured: tensor pipe 32%, MUFU 52% busy on the ViT shape).  Here S_x(j+2) is issued right
+// after PV_x(j) into the buffer P_x(j) occupied, so when softmax x finishes tile j the scores of
+// tile j+1 are already in TMEM and the MUFU alternates A/B without gaps.
+//   TMEM (512 cols): S_A[0] S_A[1] S_B[0] S_B[1] (64 each) | O_A (256..) | O_B (384..)
+//   smem: Q_A, Q_B (128 rows) + 4-stage K and V rings (64-row tiles)
+// O rescaling (rare, lazy) waits for PV_x(j-1) through o_ready[x], since S_x(j) no longer
+// orders after it.  Numerics per (row, head): fixed key order, fixed 64-key tiling.
+__device__ long long g_fmha_dbg[16][512];  // TEMP instrumentation (CTA 0): event x tile -> clock64
+constexpr int KT4 = 64;    // keys per tile
+constexpr int KST4 = 4;    // K / V ring depth
+template <int HD>
+struct Ft4Cfg {
+  static constexpr int NCH = (HD + CHUNK - 1) / CHUNK;
+  static constexpr int Q_BYTES = NCH * FBM * CHUNK * 2;    // one 128-row Q tile
+  static constexpr int KV_BYTES = NCH * KT4 * CHUNK * 2;   // one 64-row K or V tile
+  static constexpr int QA_OFF = 0, QB_OFF = Q_BYTES;
+  static constexpr int K_OFF = 2 * Q_BYTES;
+  static constexpr int V_OFF = K_OFF + KST4 * KV_BYTES;
+  static constexpr int BAR_OFF = V_OFF + KST4 * KV_BYTES;
+  static constexpr int SMEM = 1024 + BAR_OFF + 512;
+};
+
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(384, 1)
+    fmha4_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, int ldo, int S, int H, int KV,
+                 float scale_log2, float* __restrict__ ws, int* __restrict__ tickets, int split, int turns) {
+  using C = Ft4Cfg<HD>;
+  constexpr int NCH = C::NCH;
+  constexpr int PW = HD + 4;
+  constexpr uint32_t IDESC_S = umma_idesc_bf16(FBM, KT4);
+  constexpr uint32_t IDESC_O = umma_idesc_bf16(FBM, HD) | (1u << 16);  // B (V) MN-major
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;    // 256 arrivals
+  uint64_t* k_full = bars + 2;     // [KST4]
+  uint64_t* k_empty = bars + 6;    // [KST4]
+  uint64_t* v_full = bars + 10;    // [KST4]
+  uint64_t* v_empty = bars + 14;   // [KST4]
+  uint64_t* s_full = bars + 18;    // [2 groups][2 buffers]
+  // P_x(g) ready, per (group, S buffer): a group may finish two tiles before the MMA warp has
+  // consumed the first (S_x(g+1) is already issued), so one barrier per group could complete two
+  // phases unobserved; per buffer it cannot (S_x(g+2) waits for PV_x(g)).
+  uint64_t* p_full = bars + 22;    // [2 groups][2 buffers], 128 arrivals
+  uint64_t* o_ready = bars + 26;   // [2]: PV_x(j) complete
+  uint64_t* o_done = bars + 28;
+  uint64_t* turn = bars + 29;      // [2], 128 arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 31);
+  int* s_last = reinterpret_cast<int*>(bars + 32);
+
+  // warp index through a shuffle: provably warp-uniform, so warp-role code keeps its scalars in
+  // uniform registers (MMA descriptors without per-lane R2UR waterfalls)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const Fmha3Plan plan(S, H, split, CAUSAL ? 1 : 0, KT4);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm);
+    for (int i = 0; i < 31; ++i) {
+      uint32_t cnt = 1;
+      if (i == 1) cnt = 256;
+      if ((i >= 22 && i < 26) || i == 29 || i == 30) cnt = 128;
+      mbar_init(&bars[i], cnt);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 0) {  // ---------------- TMA producer (lane 0); the branch is warp-uniform
+     if (lane == 0) {
+      int g = 0, nu = 0;
+      for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
+        if (u < 0) continue;
+        int h, pr, t0, t1, slot, ch;
+        plan.decode(u, h, pr, t0, t1, slot, ch);
+        const int kvh = h / (H / KV), q0 = pr * 2 * FBM;
+        const int qcol = h * HD, kcol = (H + kvh) * HD, vcol = (H + KV + kvh) * HD;
+        mbar_wait(q_empty, (nu & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, 2 * C::Q_BYTES);
+        for (int c = 0; c < NCH; ++c)
+          for (int r = 0; r < 2 * FBM / KT4; ++r)  // Q_A then Q_B rows, 64-row boxes
+            tma_load_2d(smem + (r < FBM / KT4 ? C::QA_OFF : C::QB_OFF) + c * FBM * 128 + (r % (FBM / KT4)) * KT4 * 128,
+                        &tm, q_full, qcol + c * CHUNK, q0 + r * KT4);
+        for (int j = t0; j < t1; ++j, ++g) {
+          const int st = g % KST4;
+          const uint32_t ph = ((g / KST4) & 1) ^ 1;
+          mbar_wait(&k_empty[st], ph);
+          mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_2d(smem + C::K_OFF + st * C::KV_BYTES + c * KT4 * 128, &tm, &k_full[st], kcol + c * CHUNK,
+                        j * KT4);
+          mbar_wait(&v_empty[st], ph);
+          mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_2d(smem + C::V_OFF + st * C::KV_BYTES + c * KT4 * 128, &tm, &v_full[st], vcol + c * CHUNK,
+                        j * KT4);
+        }
+        ++nu;
+      }
+     }
+    } else if (warp == 1) {  // ---------------- MMA issuer: the whole warp waits, lane 0 issues
+      // Descriptors are built once from warp-uniform values (uniform registers); per MMA only a
+      // constant is added to the start-address field (smem < 256 KB: no carry out of it).
+      const uint64_t qd[2] = {umma_desc_sw128(smem_u32(smem + C::QA_OFF)), umma_desc_sw128(smem_u32(smem + C::QB_OFF))};
+      const uint64_t kd0 = umma_desc_sw128(smem_u32(smem + C::K_OFF));
+      const uint64_t vd0 = umma_desc_sw128_mn(smem_u32(smem + C::V_OFF), KT4 * 128);
+      auto tS = [&](int x, int g) { return tbase + (uint32_t)(x * 2 * KT4 + (g & 1) * KT4); };
+      const uint32_t tO[2] = {tbase + 256, tbase + 384};
+      auto issue_s = [&](int x, int g) {  // S_x(g) = Q_x K_g^T -> S buffer g & 1 of group x
+        const uint64_t kb = kd0 + (uint64_t)((g % KST4) * (C::KV_BYTES >> 4));
+        const uint32_t d = tS(x, g);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t qoff = ((k * 16 / CHUNK) * FBM * 128 + (k * 16 % CHUNK) * 2) >> 4;
+          const uint32_t koff = ((k * 16 / CHUNK) * KT4 * 128 + (k * 16 % CHUNK) * 2) >> 4;
+          umma_bf16_ss_warp(d, qd[x] + qoff, kb + koff, IDESC_S, k > 0 ? 1u : 0u);
+        }
+        umma_commit_warp(&s_full[x * 2 + (g & 1)]);
+      };
+      auto issue_pv = [&](int x, int g, bool first) {
+        const uint64_t vb = vd0 + (uint64_t)((g % KST4) * (C::KV_BYTES >> 4));
+        const uint32_t a = tS(x, g), d = tO[x];
+#pragma unroll
+        for (int k = 0; k < KT4 / 16; ++k)  // P: 16 keys = 8 packed TMEM columns per step
+          umma_bf16_ts_warp(d, a + k * 8, vb + (uint64_t)((k * 16 * 128) >> 4), IDESC_O, (!first || k > 0) ? 1u : 0u);
+        umma_commit_warp(&o_ready[x]);
+      };
+      auto commit = [&](uint64_t* bar) { umma_commit_warp(bar); };
+      auto wait_k = [&](int g) {
+        mbar_wait(&k_full[g % KST4], (g / KST4) & 1);
+        tc_fence_after();
+      };
+      int g = 0, nu = 0;
+      for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
+        if (u < 0) continue;
+        int h, pr, t0, t1, slot, ch;
+        plan.decode(u, h, pr, t0, t1, slot, ch);
+        const int n = t1 - t0, g0 = g;
+        mbar_wait(q_full, nu & 1);
+        for (int j = 0; j < 2 && j < n; ++j) {  // prologue: S(0), S(1) of both tiles
+          wait_k(g0 + j);
+          issue_s(0, g0 + j);
+          issue_s(1, g0 + j);
+          commit(&k_empty[(g0 + j) % KST4]);
+        }
+        for (int j = 0; j < n; ++j, ++g) {
+          const int st = g % KST4;
+          const bool more = j + 2 < n;
+          mbar_wait(&v_full[st], (g / KST4) & 1);
+          mbar_wait(&p_full[0 + (g & 1)], (g >> 1) & 1);
+          tc_fence_after();
+          issue_pv(0, g, j == 0);
+          if (more) {
+            wait_k(g + 2);
+            issue_s(0, g + 2);
+          }
+          mbar_wait(&p_full[2 + (g & 1)], (g >> 1) & 1);
+          tc_fence_after();
+          issue_pv(1, g, j == 0);
+          commit(&v_empty[st]);
+          if (more) {
+            issue_s(1, g + 2);
+            commit(&k_empty[(g + 2) % KST4]);
+          }
+        }
+        commit(o_done);
+        ++nu;
+      }
+    }
+  } else {  // ---------------- softmax warpgroups: x = 0 (warps 4-7, tile A), 1 (warps 8-11, tile B)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    const int x = (warp - 4) >> 2;
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tSx = tbase + x * 2 * KT4 + lane_off, tO = tbase + 256 + x * 128 + lane_off;
+    int g = 0, nu = 0;
+    for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
+      if (u < 0) continue;
+      int h, pr, t0, t1, slot, ch;
+      plan.decode(u, h, pr, t0, t1, slot, ch);
+      const int qrow = pr * 2 * FBM + x * FBM + row;
+      const int qlo = pr * 2 * FBM + x * FBM;
+      float m = -1e30f, l = 0.f;
+      for (int j = t0; j < t1; ++j, ++g) {
+        const uint32_t tS = tSx + (g & 1) * KT4;
+        const bool dbg = blockIdx.x == 0 && (warp & 3) == 0 && lane == 0 && g < 512;
+        if (dbg) g_fmha_dbg[x * 4 + 0][g] = clock64();
+        mbar_wait(&s_full[x * 2 + (g & 1)], (g >> 1) & 1);
+        tc_fence_after();
+        if (dbg) g_fmha_dbg[x * 4 + 1][g] = clock64();
+        uint32_t sv[KT4];
+        tmem_ld32_nw<32>(tS, sv);
+        tmem_ld32_nw<32>(tS + 32, sv + 32);
+        tmem_ld_wait32(sv);
+        tmem_ld_wait32(sv + 32);
+        const int k0 = j * KT4;
+        if (CAUSAL) {
+          if (k0 + KT4 - 1 > qlo || k0 + KT4 > S) {
+            const int lim = min(S, qrow + 1);
+#pragma unroll
+            for (int i = 0; i < KT4; ++i)
+              if (k0 + i >= lim) sv[i] = __float_as_uint(-1e30f);
+          }
+        } else if (k0 + KT4 > S) {
+#pragma unroll
+          for (int i = 0; i < KT4; ++i)
+            if (k0 + i >= S) sv[i] = __float_as_uint(-1e30f);
+        }
+        float mxa[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mxa[a] = __uint_as_float(sv[a]);
+#pragma unroll
+        for (int i = 8; i < KT4; i += 8)
+#pragma unroll
+          for (int a = 0; a < 8; ++a) mxa[a] = fmaxf(mxa[a], __uint_as_float(sv[i + a]));
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        const float mnew = fmaxf(m, mx * scale_log2);
+        const bool need = (mnew - m) > 8.0f;
+        if (__any_sync(0xffffffffu, need) && j > t0) {  // lazy rescale of O: PV_x(g-1) must be complete
+          mbar_wait(&o_ready[x], (g - 1) & 1);
+          tc_fence_after();
+          const float f = need ? fast_exp2(m - mnew) : 1.0f;
+#pragma unroll
+          for (int c = 0; c < HD / 16; ++c) {
+            float o[16];
+            tmem_ld16(tO + c * 16, o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] *= f;
+            tmem_st16(tO + c * 16, o);
+          }
+        }
+        if (need) {
+          l *= fast_exp2(m - mnew);
+          m = mnew;
+        }
+        if (turns) {  // optional MUFU ping-pong (A's exps, then B's, ...)
+          if (x == 1) mbar_wait(&turn[1], g & 1);
+          else if (g > 0) mbar_wait(&turn[0], (g - 1) & 1);
+        }
+        if (dbg) g_fmha_dbg[x * 4 + 2][g] = clock64();
+        const float nm = -m;
+        float lsa[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) lsa[a] = 0.f;
+        uint32_t pk[KT4 / 2];
+#pragma unroll
+        for (int i = 0; i < KT4; i += 2) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[i]), scale_log2, nm));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[i + 1]), scale_log2, nm));
+          lsa[(i >> 1) & 7] += p0 + p1;
+          pk[i / 2] = pack_bf16(p0, p1);
+        }
+        tmem_st16u(tS, pk);        // packed P keys 0..31  -> columns 0..15
+        tmem_st16u(tS + 16, pk + 16);  // keys 32..63 -> columns 16..31
+        l += ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
+        if (turns) mbar_arrive(&turn[x ^ 1]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[x * 2 + (g & 1)]);
+        if (dbg) g_fmha_dbg[x * 4 + 3][g] = clock64();
+      }
+      mbar_wait(o_done, nu & 1);
+      tc_fence_after();
+      if (slot < 0) {
+        const float inv = 1.0f / l;
+        bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+          if (qrow < S) {
+            uint4 a = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
+                                 pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
+            uint4 b = make_uint4(pack_bf16(o[8] * inv, o[9] * inv), pack_bf16(o[10] * inv, o[11] * inv),
+                                 pack_bf16(o[12] * inv, o[13] * inv), pack_bf16(o[14] * inv, o[15] * inv));
+            reinterpret_cast<uint4*>(orow + c * 16)[0] = a;
+            reinterpret_cast<uint4*>(orow + c * 16)[1] = b;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(q_empty);
+      } else {  // key chunk: (m, l, O) partial; the last chunk of the unit merges in chunk order
+        float* wr = ws + ((size_t)slot * 2 * FBM + x * FBM + row) * PW;
+        *reinterpret_cast<float4*>(wr) = make_float4(m, l, 0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(wr + 4 + c * 16 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(q_empty);
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int grp = (u - plan.full) / plan.KC;
+        if (threadIdx.x == 128) *s_last = atomicAdd(&tickets[grp], 1) == plan.KC - 1;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (*s_last) {
+          __threadfence();
+          const float* base = ws + ((size_t)grp * plan.KC * 2 * FBM + x * FBM + row) * PW;
+          const size_t cstride = (size_t)2 * FBM * PW;
+          float M = -1e30f;
+          for (int c2 = 0; c2 < plan.KC; ++c2) M = fmaxf(M, __ldcg(base + c2 * cstride));
+          float den = 0.f, acc[HD];
+#pragma unroll
+          for (int d = 0; d < HD; ++d) acc[d] = 0.f;
+          for (int c2 = 0; c2 < plan.KC; ++c2) {
+            const float* pr2 = base + c2 * cstride;
+            const float4 ml = __ldcg(reinterpret_cast<const float4*>(pr2));
+            float4 ov[HD / 4];
+#pragma unroll
+            for (int q = 0; q < HD / 4; ++q) ov[q] = __ldcg(reinterpret_cast<const float4*>(pr2 + 4) + q);
+            const float f = exp2f(ml.x - M);
+            den += f * ml.y;
+#pragma unroll
+            for (int q = 0; q < HD / 4; ++q) {
+              acc[4 * q] += f * ov[q].x;
+              acc[4 * q + 1] += f * ov[q].y;
+              acc[4 * q + 2] += f * ov[q].z;
+              acc[4 * q + 3] += f * ov[q].w;
+            }
+          }
+          const float inv = 1.0f / den;
+          bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
+          if (qrow < S) {
+#pragma unroll
+            for (int d0 = 0; d0 < HD; d0 += 8)
+              *reinterpret_cast<uint4*>(orow + d0) =
+                  make_uint4(pack_bf16(acc[d0] * inv, acc[d0 + 1] * inv), pack_bf16(acc[d0 + 2] * inv, acc[d0 + 3] * inv),
+                             pack_bf16(acc[d0 + 4] * inv, acc[d0 + 5] * inv), pack_bf16(acc[d0 + 6] * inv, acc[d0 + 7] * inv));
+          }
+          if (threadIdx.x == 128) tickets[grp] = 0;
+        }
+      }
+      ++nu;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool make_qkv_map(CUtensorMap* m, const bf16* ptr, int rows, int cols) {
+bool make_qkv_map(CUtensorMap* m, const bf16* ptr, int rows, int cols, int box_rows = FBN) {
   static PFN_encodeTiled_t enc = nullptr;
   if (!enc) {
     void* p = nullptr;
@@ -942,7 +1301,7 @@ bool make_qkv_map(CUtensorMap* m, const bf16* ptr, int rows, int cols) {
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)CHUNK, (cuuint32_t)FBN};
+  cuuint32_t box[2] = {(cuuint32_t)CHUNK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1014,11 +1373,48 @@ cudaError_t fmha3_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int
                   g_fmha_tickets, split);
 }
 
+template <int HD, bool CAUSAL>
+cudaError_t fmha4_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int max_ctas,
+                         cudaStream_t s) {
+  CUtensorMap tm;
+  if (!make_qkv_map(&tm, qkv, S, ld, KT4)) return cudaErrorInvalidValue;
+  auto kern = fmha4_kernel<HD, CAUSAL>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Ft4Cfg<HD>::SMEM);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  if (!g_fmha_ws) {
+    if (cudaMalloc(&g_fmha_ws, (size_t)148 * 2 * FBM * (128 + 4) * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&g_fmha_tickets, 256 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(g_fmha_tickets, 0, 256 * sizeof(int)) != cudaSuccess)
+      return cudaErrorMemoryAllocation;
+  }
+  static const int split = getenv("NOVA_FMHA_SPLIT") ? atoi(getenv("NOVA_FMHA_SPLIT")) : 1;
+  const Fmha3Plan plan(S, H, split, CAUSAL ? 1 : 0, KT4);
+  int grid = max_ctas > 0 ? max_ctas : 148;
+  if (grid > plan.total) grid = plan.total;
+  const float sl2 = LOG2E_F / sqrtf((float)HD);
+  static const int turns = getenv("NOVA_FMHA_TURN") ? atoi(getenv("NOVA_FMHA_TURN")) : 1;  // experiments
+  return launch_k(kern, dim3(grid), dim3(384), Ft4Cfg<HD>::SMEM, s, false, tm, out, ldo, S, H, KV, sl2, g_fmha_ws,
+                  g_fmha_tickets, split, turns);
+}
+
 // ld (the qkv row length in elements) must be a multiple of 8; hd in {80, 128} (64-col SW128 chunks).
 cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                           int max_ctas, cudaStream_t s) {
   if (S <= 0) return cudaSuccess;
   if (ld % 8 || H % KV || ldo % 8) return cudaErrorInvalidValue;
+  if (g_fmha_version == 4) {
+    switch (hd) {
+      case 80: return causal ? fmha4_launch<80, true>(qkv, ld, out, ldo, S, H, KV, max_ctas, s)
+                             : fmha4_launch<80, false>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
+      case 128: return causal ? fmha4_launch<128, true>(qkv, ld, out, ldo, S, H, KV, max_ctas, s)
+                              : fmha4_launch<128, false>(qkv, ld, out, ldo, S, H, KV, max_ctas, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (g_fmha_version == 3) {
     switch (hd) {
       case 80: return causal ? fmha3_launch<80, true>(qkv, ld, out, ldo, S, H, KV, max_ctas, s)
@@ -1046,6 +1442,7 @@ cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, in
   return cudaErrorInvalidValue;
 }
 
-int g_fmha_version = 3;
+int fmha_debug_read(long long* host) { return (int)cudaMemcpyFromSymbol(host, g_fmha_dbg, sizeof(g_fmha_dbg)); }
+int g_fmha_version = getenv("NOVA_FMHA") ? atoi(getenv("NOVA_FMHA")) : 4;
 
 }  // namespace nova

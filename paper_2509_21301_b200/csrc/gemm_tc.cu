@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle: provably warp-uniform, so the MMA warp's descriptors live in
+  // uniform registers and each tcgen05.mma issues without a per-lane waterfall
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -167,8 +169,9 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer: whole warp (convergent), one elected lane issues
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      const uint64_t da0 = umma_desc_sw128(smem_u32(sA)), db0 = umma_desc_sw128(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -180,20 +183,18 @@ __global__ void __launch_bounds__(384, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint64_t a0 = da0 + (uint64_t)(stage * (Cfg::A_BYTES >> 4));
+          const uint64_t b0 = db0 + (uint64_t)(stage * (Cfg::B_BYTES >> 4));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16_ss(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                         (kb | k) != 0 ? 1u : 0u);
-          }
-          umma_commit(&empty[stage]);
+          for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the 128-B swizzle atom
+            umma_bf16_ss_warp(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit_warp(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        umma_commit_warp(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
@@ -270,16 +271,17 @@ NOVA_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, i
       "l"(reinterpret_cast<uint64_t>(m)), "r"(b), "r"(x), "r"(y)
       : "memory");
 }
-NOVA_DEV void umma2_bf16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+NOVA_DEV void umma2_bf16_ss_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
   asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-          tmem_d),
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
-NOVA_DEV void umma2_commit_both(uint64_t* bar) {
+NOVA_DEV void umma2_commit_both_warp(uint64_t* bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
           smem_u32(bar)),
       "h"((uint16_t)3)
       : "memory");
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank_in_cluster();
 
@@ -360,8 +362,9 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+    if (rank == 0) {  // ---------------- MMA issuer (leader CTA; whole warp, one elected lane issues)
       constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+      const uint64_t da0 = umma_desc_sw128(smem_u32(sA)), db0 = umma_desc_sw128(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -373,20 +376,18 @@ __global__ void __launch_bounds__(384, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint64_t a0 = da0 + (uint64_t)(stage * (Cfg::A_BYTES >> 4));
+          const uint64_t b0 = db0 + (uint64_t)(stage * (Cfg::B_BYTES >> 4));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            umma2_bf16_ss(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                          (kb | k) != 0 ? 1u : 0u);
-          }
-          umma2_commit_both(&empty[stage]);
+          for (int k = 0; k < BK / 16; ++k)
+            umma2_bf16_ss_warp(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          umma2_commit_both_warp(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma2_commit_both(&tfull[acc]);
+        umma2_commit_both_warp(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
