@@ -938,7 +938,6 @@ __global__ void __launch_bounds__(384, 1)
 //   smem: Q_A, Q_B (128 rows) + 4-stage K and V rings (64-row tiles)
 // O rescaling (rare, lazy) waits for PV_x(j-1) through o_ready[x], since S_x(j) no longer
 // orders after it.  Numerics per (row, head): fixed key order, fixed 64-key tiling.
-__device__ long long g_fmha_dbg[16][512];  // TEMP instrumentation (CTA 0): event x tile -> clock64
 constexpr int KT4 = 64;    // keys per tile
 constexpr int KST4 = 4;    // K / V ring depth
 template <int HD>
@@ -1122,11 +1121,8 @@ __global__ void __launch_bounds__(384, 1)
       float m = -1e30f, l = 0.f;
       for (int j = t0; j < t1; ++j, ++g) {
         const uint32_t tS = tSx + (g & 1) * KT4;
-        const bool dbg = blockIdx.x == 0 && (warp & 3) == 0 && lane == 0 && g < 512;
-        if (dbg) g_fmha_dbg[x * 4 + 0][g] = clock64();
-        mbar_wait(&s_full[x * 2 + (g & 1)], (g >> 1) & 1);
+        mbar_wait_sleep(&s_full[x * 2 + (g & 1)], (g >> 1) & 1);
         tc_fence_after();
-        if (dbg) g_fmha_dbg[x * 4 + 1][g] = clock64();
         uint32_t sv[KT4];
         tmem_ld32_nw<32>(tS, sv);
         tmem_ld32_nw<32>(tS + 32, sv + 32);
@@ -1174,10 +1170,9 @@ __global__ void __launch_bounds__(384, 1)
           m = mnew;
         }
         if (turns) {  // optional MUFU ping-pong (A's exps, then B's, ...)
-          if (x == 1) mbar_wait(&turn[1], g & 1);
-          else if (g > 0) mbar_wait(&turn[0], (g - 1) & 1);
+          if (x == 1) mbar_wait_sleep(&turn[1], g & 1);
+          else if (g > 0) mbar_wait_sleep(&turn[0], (g - 1) & 1);
         }
-        if (dbg) g_fmha_dbg[x * 4 + 2][g] = clock64();
         const float nm = -m;
         float lsa[8];
 #pragma unroll
@@ -1197,7 +1192,6 @@ __global__ void __launch_bounds__(384, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[x * 2 + (g & 1)]);
-        if (dbg) g_fmha_dbg[x * 4 + 3][g] = clock64();
       }
       mbar_wait(o_done, nu & 1);
       tc_fence_after();
@@ -1442,7 +1436,6 @@ cudaError_t flash_attn_tc(const bf16* qkv, int ld, bf16* out, int ldo, int S, in
   return cudaErrorInvalidValue;
 }
 
-int fmha_debug_read(long long* host) { return (int)cudaMemcpyFromSymbol(host, g_fmha_dbg, sizeof(g_fmha_dbg)); }
 int g_fmha_version = getenv("NOVA_FMHA") ? atoi(getenv("NOVA_FMHA")) : 4;
 
 }  // namespace nova

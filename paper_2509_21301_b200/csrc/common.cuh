@@ -94,6 +94,19 @@ NOVA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// Same, with an explicit suspend-time hint (ns): the waiting warp sleeps until the phase completes
+// (or the hint elapses) instead of re-issuing try_wait, leaving issue slots to co-resident warps.
+NOVA_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
+}
 
 // ------------------------------------------------------------------ TMA
 NOVA_DEV void tma_prefetch_desc(const CUtensorMap* m) {

@@ -94,7 +94,7 @@ cudaError_t flash_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, in
 // tcgen05/TMEM/TMA version (hd 80 / 128); flash_attn() dispatches to it for those head dims.
 cudaError_t flash_attn_tc(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                           int max_ctas, cudaStream_t s);
-extern int g_fmha_version;  // 3: persistent 2-Q-tile ping-pong (default, non-causal); 2: 2 CTAs/SM; 1: P in smem
+extern int g_fmha_version;  // 4 (default, env NOVA_FMHA): v3 + 64-key tiles, double-buffered S; 3: persistent 2-Q-tile ping-pong; 2: 2 CTAs/SM; 1: P in smem
 // legacy warp-MMA (mma.sync) version, kept for head dims 16/32/64 and as the measured baseline
 cudaError_t flash_attn_mma(const bf16* qkv, int ldqkv, bf16* out, int ldo, int S, int H, int KV, int hd, int causal,
                            cudaStream_t s);

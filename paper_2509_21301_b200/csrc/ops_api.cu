@@ -8,9 +8,7 @@ static int st(cudaError_t e) { return e == cudaSuccess ? 0 : -(int)e; }
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static_assert(sizeof(nova_decode_row) == sizeof(DecodeRow), "row layout");
 
-namespace nova { int fmha_debug_read(long long* host); }
 extern "C" {
-int nova_op_fmha_debug(long long* host) { return nova::fmha_debug_read(host); }
 
 int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
                  int K, int epi, int max_ctas, void* stream) {
