@@ -367,23 +367,24 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
 }
 
 // Tensor-core decode attention, one launch, merged through a thread-block cluster (DSMEM).
-// Cluster = DA_CL CTAs per (request, KV head); CTA = 4 warps; the context is cut into 32-key
-// blocks and warp w of cluster rank r owns blocks (r*4 + w), (r*4 + w) + 4*DA_CL, ...  A warp
+// Cluster = DA_CL CTAs per (request, KV head); CTA = DA_W warps; the context is cut into 32-key
+// blocks and warp w of cluster rank r owns blocks (r*DA_W + w), (r*DA_W + w) + DA_W*DA_CL, ...  A warp
 // streams its blocks through a 2-stage cp.async ring in its own smem slice (pages gathered
 // through the block table), and keeps an online softmax over them: S = Q K^T with the G query
 // heads sharing the KV head as the M side of mma.sync m16n8k16 (padded to 16 rows), keys the
-// N side; O += P V.  The 4 warp states are merged in smem in warp order, then rank 0 reads the
+// N side; O += P V.  The DA_W warp states are merged in smem in warp order, then rank 0 reads the
 // DA_CL CTA states from the peers' shared memory (mapa + ld.shared::cluster) and merges them in
 // rank order.  Every reduction order depends only on the context length -> deterministic,
 // batch- and SM-budget-invariant; no global workspace, no second kernel.
 constexpr int TKW = 32;   // keys per block
 constexpr int DA_CL = 4;  // CTAs per (request, KV head)
+constexpr int DA_W = 6;   // warps per CTA (smem: 6 x 2 stages x 17 KB): 24 block streams per (request, KV head)
 template <int HD>
 struct DtcCfg {
   static constexpr int HDP = HD + 8;                       // padded row (conflict-free ldmatrix)
   static constexpr int BLK = 2 * TKW * HDP * 2;            // one K+V block (bytes)
   static constexpr int Q_BYTES = 16 * HDP * 2;
-  static constexpr int RING = 4 * 2 * BLK;                 // 4 warps x 2 stages
+  static constexpr int RING = DA_W * 2 * BLK;              // DA_W warps x 2 stages
   static constexpr int ST_OFF = Q_BYTES + RING;            // CTA state [16][HD + 2] f32
   static constexpr int SMEM = ST_OFF + 16 * (HD + 2) * 4;
 };
@@ -405,7 +406,7 @@ NOVA_DEV float ld_dsmem_f32(uint32_t local_saddr, uint32_t rank) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restrict__ qkv, int ld,
+__global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* __restrict__ qkv, int ld,
                                                              const bf16* __restrict__ pool, int layer, int n_pages,
                                                              int H, int KV, const int* __restrict__ bt, int max_pages,
                                                              const DecodeRow* __restrict__ rows, bf16* __restrict__ out,
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restr
   constexpr int HDP = Cf::HDP, CH = HD / 8, KT = HD / 16, DT = HD / 8, PW = HD + 2;
   extern __shared__ __align__(16) uint8_t dsm[];
   bf16* sQ = reinterpret_cast<bf16*>(dsm);
-  float* sW = reinterpret_cast<float*>(dsm + Cf::Q_BYTES);  // warp states [4][16][PW] (after the ring drains)
+  float* sW = reinterpret_cast<float*>(dsm + Cf::Q_BYTES);  // warp states [DA_W][16][PW] (after the ring drains)
   float* sS = reinterpret_cast<float*>(dsm + Cf::ST_OFF);   // CTA state [16][PW]
   pdl_launch_dependents();
   pdl_wait();
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restr
   const DecodeRow rr = rows[b];
   const int L = rr.ctx + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < 16 * CH; i += 128) {  // Q rows g < G (rows >= G zero)
+  for (int i = tid; i < 16 * CH; i += 32 * DA_W) {  // Q rows g < G (rows >= G zero)
     const int r = i / CH, c = i % CH;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < G) v = *reinterpret_cast<const uint4*>(qkv + (size_t)b * ld + (size_t)(kvh * G + r) * HD + c * 8);
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restr
   const bf16* lbase = pool + (size_t)layer * n_pages * page_stride;
   const int* btr = bt + (size_t)rr.slot * max_pages;
   const int nblk = (L + TKW - 1) / TKW;
-  const int wg = rank * 4 + warp, wstride = 4 * DA_CL;
+  const int wg = rank * DA_W + warp, wstride = DA_W * DA_CL;
   bf16* ring = reinterpret_cast<bf16*>(dsm + Cf::Q_BYTES) + (size_t)warp * 2 * (Cf::BLK / 2);
   auto issue = [&](int blk, int stage) {  // gather K and V rows of block blk into stage
     bf16* wK = ring + (size_t)stage * (Cf::BLK / 2);
@@ -554,18 +555,18 @@ __global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restr
     }
   }
   __syncthreads();
-  // CTA state = merge of the 4 warp states in warp order (warps without blocks: m = -1e30, l = 0)
-  for (int i = tid; i < G * (HD + 2); i += 128) {
+  // CTA state = merge of the DA_W warp states in warp order (warps without blocks: m = -1e30, l = 0)
+  for (int i = tid; i < G * (HD + 2); i += 32 * DA_W) {
     const int row = i / PW, d = i % PW;
     float M = -1e30f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sW[(w * 16 + row) * PW]);
+    for (int w = 0; w < DA_W; ++w) M = fmaxf(M, sW[(w * 16 + row) * PW]);
     float acc = 0.f;
     if (d == 0) {
       acc = M;
     } else {
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
+      for (int w = 0; w < DA_W; ++w) {
         const float* pw = sW + (w * 16 + row) * PW;
         acc += exp2f(pw[0] - M) * pw[d];
       }
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(128) decode_attn_tc_kernel(const bf16* __restr
   cluster_sync_all();  // CTA states visible cluster-wide
   if (rank == 0) {
     const uint32_t base = smem_u32(sS);
-    for (int i = tid; i < G * HD; i += 128) {
+    for (int i = tid; i < G * HD; i += 32 * DA_W) {
       const int row = i / HD, d = i % HD;
       float m[DA_CL], l[DA_CL], v[DA_CL];
 #pragma unroll
@@ -637,7 +638,7 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(DA_CL, KV, B);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(32 * DA_W);
     cfg.dynamicSmemBytes = DtcCfg<HD>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
