@@ -480,7 +480,11 @@ def main():
     if not args.no_compare:
         pols = [("adaptive", policy),
                 ("static_50_50", dict(mode=E.STATIC, sm_decode_dv=72, sm_decode_dp=72, b_max=16)),
-                ("serial", dict(mode=E.SERIAL, b_max=16))]
+                ("serial", dict(mode=E.SERIAL, b_max=16)),
+                # the paper's baselines: prefill-first with decode threshold 5, and
+                # co-running stages with no SM partition (both streams see every SM)
+                ("pf_limit_5", dict(mode=E.PF_LIMIT, pf_threshold=5, b_max=16)),
+                ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16))]
         for rho in args.compare_rho:
             trs = [make_trace(shape, args.requests, rho, t_front, 61 + k) for k in range(args.compare_seeds)]
             runs = {name: [] for name, _ in pols}
@@ -497,7 +501,7 @@ def main():
                 summ[name]["per_seed_max_ms"] = [x["max_ms"] for x in rs]
             ad = runs["adaptive"]
             verdict = {}
-            for name in ("static_50_50", "serial"):
+            for name in [n for n, _ in pols if n != "adaptive"]:
                 xs = runs[name]
                 wins = sum(a["max_ms"] < b["max_ms"] for a, b in zip(ad, xs))
                 verdict[name] = {"lower_mean_max": summ["adaptive"]["max_ms"] < summ[name]["max_ms"],

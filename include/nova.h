@@ -117,7 +117,15 @@ typedef struct {
 nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* req_id);
 
 /* ------------------------------------------------------------------ partition policy */
-enum { NOVA_MODE_SERIAL = 0, NOVA_MODE_STATIC = 1, NOVA_MODE_ADAPTIVE = 2 };
+/* SERIAL: Serial-RR, one pass at a time on all SMs, alternating decode / front (BASELINE).
+ * STATIC: co-run, fixed decode SMs per context.  ADAPTIVE: co-run, Eq. 5 (Nova).
+ * PF_LIMIT: the paper's prefill-first baseline: one pass at a time on all SMs, the
+ *   front stage first; a decode iteration runs when more than pf_threshold requests wait for
+ *   decode, or when no front work is ready.
+ * MULTI_STREAM: the paper's multi-stream baseline: front and decode co-run on two
+ *   streams that both see every SM (no partition; the hardware arbitrates). */
+enum { NOVA_MODE_SERIAL = 0, NOVA_MODE_STATIC = 1, NOVA_MODE_ADAPTIVE = 2, NOVA_MODE_PF_LIMIT = 3,
+       NOVA_MODE_MULTI_STREAM = 4 };
 enum { NOVA_CTX_DV = 0, NOVA_CTX_DP = 1, NOVA_CTX_SOLO = 2 };
 typedef struct {
   int32_t mode;                        /* NOVA_MODE_*                                           */
@@ -125,6 +133,7 @@ typedef struct {
   int32_t sm_op_dv, sm_op_dp, sm_min;  /* ADAPTIVE (Eq. 5)                                       */
   float alpha_dv, alpha_dp;
   int32_t b_max;                       /* decode batch cap (<= max_decode_batch)                 */
+  int32_t pf_threshold;                /* PF_LIMIT: decode when > pf_threshold wait (<= 0: 5)     */
 } nova_partition_policy;
 /* Takes effect at each role's next forward pass.  `applied` (may be NULL)
  * receives the values rounded down to the granularity.  NOVA_E_PARTITION if a

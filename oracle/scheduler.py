@@ -22,6 +22,12 @@ Readings (R13-R17):
   * gen_len counts the prefill token, decode iterations = gen_len - 1.
   * SERIAL (Serial-RR, the BASELINE comparison): one pass at a time on all SMs,
     alternating a decode iteration and a front pass when both are ready.
+  * PF_LIMIT (the paper's baseline): prefill-first -- one pass at a time on
+    all SMs, the front stage first; "LLM decode requests are scheduled when the
+    number of waiting LLM decode requests exceeds a predefined threshold (set to 5)".
+    Reading (R21): decode also runs when no front work is ready.
+  * MULTI_STREAM (the paper's baseline): stages co-run like Nova but every
+    pass sees all SMs ("CUDA's default multi-stream scheduling policy").
 The same state machine drives `simulate` (virtual time, durations from curves),
 which checks the worked example of SURVEY.md §8(c) c6 by hand values.
 """
@@ -32,7 +38,7 @@ from dataclasses import dataclass, field
 
 from .planner import adaptive_sm
 
-SERIAL, STATIC, ADAPTIVE = 0, 1, 2
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM = 0, 1, 2, 3, 4
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 # event kinds (order = tie-break class: completions first)
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
@@ -53,6 +59,7 @@ class Policy:
     alpha_dv: float = 8.0
     alpha_dp: float = 8.0
     b_max: int = 16
+    pf_threshold: int = 5       # PF_LIMIT
 
 
 @dataclass
@@ -141,6 +148,13 @@ class Alg1:
         npend = self.n_pend()
         if self.p.mode == SERIAL:
             self._dispatch_serial(out)
+        elif self.p.mode == PF_LIMIT:
+            self._dispatch_pf_limit(out)
+        elif self.p.mode == MULTI_STREAM:
+            if not self.front_running():
+                self._dispatch_front(out, lambda c: (CTX_SOLO, 0))
+            if self.decode_running is None and self.q_d:
+                self._dispatch_decode(out, CTX_SOLO, self.p.total_sms)
         else:
             self._dispatch_corun(out, npend)
         self.log.extend(out)
@@ -176,6 +190,15 @@ class Alg1:
             else:
                 ctx = CTX_SOLO
             self._dispatch_decode(out, ctx, self.split(ctx, npend))
+
+    def _dispatch_pf_limit(self, out):
+        if self.busy():
+            return
+        front_ready = bool(self.prefill_wait or self.q_v)
+        if self.q_d and (len(self.q_d) > self.p.pf_threshold or not front_ready):
+            self._dispatch_decode(out, CTX_SOLO, self.p.total_sms)
+        elif front_ready:
+            self._dispatch_front(out, lambda c: (CTX_SOLO, 0))
 
     def _dispatch_serial(self, out):
         if self.busy():

@@ -119,6 +119,18 @@ std::vector<Decision> Alg1::tick(std::vector<Event>& evs) {
       else if (dec_ready)
         dispatch_decode(out, NOVA_CTX_SOLO, total_sms);
     }
+  } else if (pol.mode == NOVA_MODE_PF_LIMIT) {  // prefill-first with a decode-queue threshold
+    if (!front_running() && !decode_busy) {
+      const bool front_ready = !prefill_wait.empty() || !q_v.empty();
+      const int thr = pol.pf_threshold > 0 ? pol.pf_threshold : 5;
+      if (!q_d.empty() && ((int)q_d.size() > thr || !front_ready))
+        dispatch_decode(out, NOVA_CTX_SOLO, total_sms);
+      else if (front_ready)
+        dispatch_front(out, false, npend, false);
+    }
+  } else if (pol.mode == NOVA_MODE_MULTI_STREAM) {  // co-run, every pass on all SMs
+    if (!front_running()) dispatch_front(out, false, npend, false);
+    if (!decode_busy && !q_d.empty()) dispatch_decode(out, NOVA_CTX_SOLO, total_sms);
   } else {
     if (!front_running()) {
       const bool has_decode = decode_busy || !q_d.empty();

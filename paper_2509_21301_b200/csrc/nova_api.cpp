@@ -100,7 +100,7 @@ nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* id) {
 nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, nova_partition_policy* applied) {
   if (!e || !p) return NOVA_E_INVAL;
   Engine& E = e->e;
-  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_ADAPTIVE) return E.fail(NOVA_E_INVAL, "mode");
+  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_MULTI_STREAM) return E.fail(NOVA_E_INVAL, "mode");
   const int g = E.alg.granularity, mx = E.alg.max_split;
   nova_partition_policy q = *p;
   auto rnd = [&](int v) { return v / g * g; };
@@ -110,6 +110,7 @@ nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, n
   q.sm_op_dp = rnd(q.sm_op_dp);
   q.sm_min = rnd(q.sm_min);
   if (q.b_max <= 0 || q.b_max > E.cfg.max_decode_batch) q.b_max = E.cfg.max_decode_batch;
+  if (q.pf_threshold <= 0) q.pf_threshold = 5;
   if (q.mode == NOVA_MODE_STATIC && (q.sm_decode_dv < g || q.sm_decode_dp < g || q.sm_decode_dv > mx ||
                                      q.sm_decode_dp > mx))
     return E.fail(NOVA_E_PARTITION, "static decode budget outside [granularity, max split]");

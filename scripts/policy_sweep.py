@@ -1,0 +1,62 @@
+"""Partition-policy sweep on one B200 (R12 evidence): profile the co-run curves once,
+then replay the same bursty traces (3 seeds per offered load) under adaptive policies with
+different SM_min / alpha readings, the static 50/50 split and serial stage execution.
+
+    python scripts/policy_sweep.py [--rho 0.5 0.7] [--seeds 3] [--requests 48]
+Prints one JSON line per (rho, policy) with mean-over-seeds max / p99 / mean E2E and req/s.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench as BN  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rho", type=float, nargs="*", default=[0.5, 0.7])
+    ap.add_argument("--seeds", type=int, default=3)
+    ap.add_argument("--requests", type=int, default=48)
+    ap.add_argument("--sm-min", type=int, nargs="*", default=[8, 16, 24, 32, 40])
+    a = ap.parse_args()
+    import torch
+    from synth import Q7B
+    from paper_2509_21301_b200 import engine as E
+    eng = BN.build_engine(Q7B, 0)
+    curves, plan = BN.profile_and_plan(eng, False, lambda *x: print(*x, file=sys.stderr, flush=True))
+    sv, sp = plan["best"][0], plan["best"][1]
+    print(json.dumps({"plan": {"best": plan["best"][:2], "sm_min": plan["sm_min"]},
+                      "t_d_dv_ms": [round(x, 2) for x in curves["t_d_dv_ms"]],
+                      "t_v_ms": [round(x, 2) for x in curves["t_v_ms"]]}), flush=True)
+    t_front = (0.5 * (curves["t_v_solo_ms"] + curves["t_v_solo_7920_ms"]) + curves["t_p_solo_ms"]) / 1000.0
+    pols = []
+    for smin in a.sm_min:
+        if smin > min(sv, sp):
+            continue
+        pols.append((f"adaptive_smin{smin}", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=smin,
+                                                  alpha_dv=(sv - smin) / 3.0, alpha_dp=(sp - smin) / 3.0, b_max=16)))
+    pols += [("static_50_50", dict(mode=E.STATIC, sm_decode_dv=72, sm_decode_dp=72, b_max=16)),
+             ("serial", dict(mode=E.SERIAL, b_max=16))]
+    for rho in a.rho:
+        trs = [BN.make_trace(Q7B, a.requests, rho, t_front, 61 + k) for k in range(a.seeds)]
+        for name, pol in pols:
+            eng.set_partition(**pol)
+            rs = []
+            for k, tr in enumerate(trs):
+                inputs = BN.make_inputs(Q7B, tr, 400 + k, 0, True)
+                r = BN.replay(eng, inputs)
+                rs.append({"max": max(r["lat_ms"]), "p99": BN.pct(r["lat_ms"], 0.99),
+                           "mean": statistics.mean(r["lat_ms"]), "rps": r["n"] / r["wall_s"]})
+            print(json.dumps({"rho": rho, "policy": name,
+                              **{k: round(statistics.mean(x[k] for x in rs), 2) for k in rs[0]},
+                              "per_seed_max": [round(x["max"], 1) for x in rs]}), flush=True)
+    eng.close()
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()

@@ -4,7 +4,8 @@ import random
 
 import pytest
 
-from oracle.scheduler import (Alg1, Policy, SimCurves, SimRequest, simulate, SERIAL, STATIC, ADAPTIVE,
+from oracle.scheduler import (Alg1, Policy, SimCurves, SimRequest, simulate, SERIAL, STATIC, ADAPTIVE, PF_LIMIT,
+                              MULTI_STREAM,
                               D_VISION, D_PREFILL, D_DECODE, D_FINISH, CTX_DV, CTX_DP, CTX_SOLO)
 
 MS = 1_000_000
@@ -29,6 +30,26 @@ def test_worked_example_nova_and_serial():
     _, tok = simulate(Policy(mode=SERIAL), c, reqs)
     assert tok[1] == [14 * MS, 15 * MS, 26 * MS]
     assert tok[2] == [30 * MS, 31 * MS, 32 * MS]
+
+
+def test_worked_example_paper_baselines():
+    """Same scenario under the paper's baselines, token times by hand.
+    PF-Limit(5): r1 vision 0-10, prefill 10-14 (token 14); r1 waits in Q_d (1 <= 5) while
+    r2 runs vision 14-24 and prefill 24-28 (token 28); no front work left -> decode [r1, r2]
+    at 28-29 and 29-30.  With threshold 0 every waiting decode request preempts the front:
+    the Serial-RR-like 14, 15, 16 / 30, 31, 32.  Multi-stream: decode of r1 co-runs with
+    r2's vision on the full GPU (equal solo durations in this simulation)."""
+    c = _curves_const(10 * MS, 4 * MS, 1 * MS)
+    reqs = [SimRequest(1, 0, 3), SimRequest(2, 0, 3)]
+    _, tok = simulate(Policy(mode=PF_LIMIT, pf_threshold=5), c, reqs)
+    assert tok[1] == [14 * MS, 29 * MS, 30 * MS]
+    assert tok[2] == [28 * MS, 29 * MS, 30 * MS]
+    _, tok = simulate(Policy(mode=PF_LIMIT, pf_threshold=0), c, reqs)
+    assert tok[1] == [14 * MS, 15 * MS, 16 * MS]
+    assert tok[2] == [30 * MS, 31 * MS, 32 * MS]
+    _, tok = simulate(Policy(mode=MULTI_STREAM), c, reqs)
+    assert tok[1] == [14 * MS, 15 * MS, 16 * MS]
+    assert tok[2] == [28 * MS, 29 * MS, 30 * MS]
 
 
 def _random_trace(seed, n=40):
