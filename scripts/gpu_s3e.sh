@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_engine.py -x -q 2>&1 | tail -2
+T0=$(date +%s)
+timeout 1500 python bench.py --out gpurun_out/bench_s3e.json 2>gpurun_out/bench_s3e.err | tail -c 200; tail -3 gpurun_out/bench_s3e.err
+echo "bench wall $(( $(date +%s) - T0 )) s"

@@ -10,6 +10,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -21,7 +22,8 @@ def main():
     ap.add_argument("--rho", type=float, nargs="*", default=[0.5, 0.7])
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--requests", type=int, default=48)
-    ap.add_argument("--sm-min", type=int, nargs="*", default=[8, 16, 24, 32, 40])
+    ap.add_argument("--sm-min", type=int, nargs="*", default=[])
+    ap.add_argument("--sm-op", type=int, nargs="*", default=[], help="adaptive SM_op values (both contexts)")
     a = ap.parse_args()
     import torch
     from synth import Q7B
@@ -33,19 +35,24 @@ def main():
                       "t_d_dv_ms": [round(x, 2) for x in curves["t_d_dv_ms"]],
                       "t_v_ms": [round(x, 2) for x in curves["t_v_ms"]]}), flush=True)
     t_front = (0.5 * (curves["t_v_solo_ms"] + curves["t_v_solo_7920_ms"]) + curves["t_p_solo_ms"]) / 1000.0
-    pols = []
+    pols = [("adaptive_plan", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=plan["sm_min"],
+                                   alpha_dv=plan["alpha_dv"], alpha_dp=plan["alpha_dp"], b_max=16))]
+    for op in a.sm_op:
+        smin = min(plan["sm_min"], op)
+        pols.append((f"adaptive_op{op}", dict(mode=E.ADAPTIVE, sm_op_dv=op, sm_op_dp=op, sm_min=smin,
+                                              alpha_dv=(op - smin) / 3.0, alpha_dp=(op - smin) / 3.0, b_max=16)))
     for smin in a.sm_min:
         if smin > min(sv, sp):
             continue
         pols.append((f"adaptive_smin{smin}", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=smin,
                                                   alpha_dv=(sv - smin) / 3.0, alpha_dp=(sp - smin) / 3.0, b_max=16)))
-    pols += [("static_50_50", dict(mode=E.STATIC, sm_decode_dv=72, sm_decode_dp=72, b_max=16)),
-             ("serial", dict(mode=E.SERIAL, b_max=16))]
+    pols += [("serial", dict(mode=E.SERIAL, b_max=16)), ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16))]
     for rho in a.rho:
         trs = [BN.make_trace(Q7B, a.requests, rho, t_front, 61 + k) for k in range(a.seeds)]
         for name, pol in pols:
             eng.set_partition(**pol)
             rs = []
+            t_pol = time.time()
             for k, tr in enumerate(trs):
                 inputs = BN.make_inputs(Q7B, tr, 400 + k, 0, True)
                 r = BN.replay(eng, inputs)
@@ -53,7 +60,8 @@ def main():
                            "mean": statistics.mean(r["lat_ms"]), "rps": r["n"] / r["wall_s"]})
             print(json.dumps({"rho": rho, "policy": name,
                               **{k: round(statistics.mean(x[k] for x in rs), 2) for k in rs[0]},
-                              "per_seed_max": [round(x["max"], 1) for x in rs]}), flush=True)
+                              "per_seed_max": [round(x["max"], 1) for x in rs],
+                              "wall_s": round(time.time() - t_pol, 1)}), flush=True)
     eng.close()
     torch.cuda.synchronize()
 
