@@ -1173,22 +1173,31 @@ __global__ void __launch_bounds__(384, 1)
           if (x == 1) mbar_wait_sleep(&turn[1], g & 1);
           else if (g > 0) mbar_wait_sleep(&turn[0], (g - 1) & 1);
         }
-        const float nm = -m;
-        float lsa[8];
+        // exponent arguments and row sums on the packed f32x2 pipe (FFMA2 / FADD2): the MUFU is the
+        // bottleneck, so the rest of the phase must issue in as few slots as possible
+        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+        float2 ls2[4];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) lsa[a] = 0.f;
+        for (int a = 0; a < 4; ++a) ls2[a] = make_float2(0.f, 0.f);
         uint32_t pk[KT4 / 2];
 #pragma unroll
         for (int i = 0; i < KT4; i += 2) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[i]), scale_log2, nm));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[i + 1]), scale_log2, nm));
-          lsa[(i >> 1) & 7] += p0 + p1;
+          const float2 xx = __ffma2_rn(make_float2(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sc2, nm2);
+          const float p0 = fast_exp2(xx.x), p1 = fast_exp2(xx.y);
+          ls2[(i >> 1) & 3] = __fadd2_rn(ls2[(i >> 1) & 3], make_float2(p0, p1));
           pk[i / 2] = pack_bf16(p0, p1);
+        }
+        // hand the MUFU to the other tile as soon as the last exponential is in (the data
+        // dependency on pk keeps the arrive after it); P stores and sums finish in its shadow
+        if (turns) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&turn[x ^ 1])), "r"(pk[KT4 / 2 - 1])
+                       : "memory");
         }
         tmem_st16u(tS, pk);        // packed P keys 0..31  -> columns 0..15
         tmem_st16u(tS + 16, pk + 16);  // keys 32..63 -> columns 16..31
-        l += ((lsa[0] + lsa[1]) + (lsa[2] + lsa[3])) + ((lsa[4] + lsa[5]) + (lsa[6] + lsa[7]));
-        if (turns) mbar_arrive(&turn[x ^ 1]);
+        const float2 s01 = __fadd2_rn(ls2[0], ls2[1]), s23 = __fadd2_rn(ls2[2], ls2[3]);
+        const float2 s4 = __fadd2_rn(s01, s23);
+        l += s4.x + s4.y;
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[x * 2 + (g & 1)]);
