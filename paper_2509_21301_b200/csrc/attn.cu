@@ -418,13 +418,35 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
   float* sW = reinterpret_cast<float*>(dsm + Cf::Q_BYTES);  // warp states [DA_W][16][PW] (after the ring drains)
   float* sS = reinterpret_cast<float*>(dsm + Cf::ST_OFF);   // CTA state [16][PW]
   pdl_launch_dependents();
-  pdl_wait();
   const int rank = (int)cluster_rank();
   const int kvh = blockIdx.y, b = blockIdx.z;
   const int G = H / KV;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {
+    // Before griddepcontrol.wait: the rows / block table (uploaded ahead of the pass's first
+    // kernel) and the cached K/V of earlier tokens (written by earlier passes) are final, so warm
+    // this warp's K/V rows into L2 while the qkv linear still runs.  Only the appended token
+    // (written by that linear) may be stale in the prefetch; L2 is coherent, so the real loads
+    // after the wait see it.
+    const DecodeRow r0 = rows[b];
+    const int L0 = r0.ctx + 1, nb = (L0 + TKW - 1) / TKW;
+    const size_t ps = (size_t)2 * KV * 64 * HD;
+    const bf16* lb = pool + (size_t)layer * n_pages * ps;
+    const int* bt0 = bt + (size_t)r0.slot * max_pages;
+    for (int blk = rank * DA_W + warp; blk < nb; blk += DA_W * DA_CL) {
+      const int j = blk * TKW + lane;
+      if (j < L0) {
+        const bf16* kp = lb + (size_t)bt0[j >> 6] * ps + ((size_t)kvh * 64 + (j & 63)) * HD;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + 64));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + (size_t)KV * 64 * HD));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + (size_t)KV * 64 * HD + 64));
+      }
+    }
+  }
+  pdl_wait();
   const DecodeRow rr = rows[b];
   const int L = rr.ctx + 1;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 16 * CH; i += 32 * DA_W) {  // Q rows g < G (rows >= G zero)
     const int r = i / CH, c = i % CH;
     uint4 v = make_uint4(0, 0, 0, 0);
