@@ -123,12 +123,9 @@ nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* req_id)
  *   front stage first; a decode iteration runs when more than pf_threshold requests wait for
  *   decode, or when no front work is ready.
  * MULTI_STREAM: the paper's multi-stream baseline: front and decode co-run on two
- *   streams that both see every SM (no partition; the hardware arbitrates).
- * ADAPTIVE_FLOAT: ADAPTIVE's scheduling and Eq. 5 split, but only the front stage is confined
- *   to its partition; decode passes run on a full-GPU stream (their reserved slice is always
- *   free of front kernels, and idle front SMs between front kernels are usable too). */
+ *   streams that both see every SM (no partition; the hardware arbitrates). */
 enum { NOVA_MODE_SERIAL = 0, NOVA_MODE_STATIC = 1, NOVA_MODE_ADAPTIVE = 2, NOVA_MODE_PF_LIMIT = 3,
-       NOVA_MODE_MULTI_STREAM = 4, NOVA_MODE_ADAPTIVE_FLOAT = 5 };
+       NOVA_MODE_MULTI_STREAM = 4 };
 enum { NOVA_CTX_DV = 0, NOVA_CTX_DP = 1, NOVA_CTX_SOLO = 2 };
 typedef struct {
   int32_t mode;                        /* NOVA_MODE_*                                           */

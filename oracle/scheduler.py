@@ -28,8 +28,6 @@ Readings (R13-R17):
     Reading (R21): decode also runs when no front work is ready.
   * MULTI_STREAM (the paper's baseline): stages co-run like Nova but every
     pass sees all SMs ("CUDA's default multi-stream scheduling policy").
-  * ADAPTIVE_FLOAT (B200 variant, R22): ADAPTIVE's decisions exactly; only the
-    executor differs (decode passes on a full-GPU stream), so the scheduler is the same.
 The same state machine drives `simulate` (virtual time, durations from curves),
 which checks the worked example of SURVEY.md §8(c) c6 by hand values.
 """
@@ -40,7 +38,7 @@ from dataclasses import dataclass, field
 
 from .planner import adaptive_sm
 
-SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, ADAPTIVE_FLOAT = 0, 1, 2, 3, 4, 5
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM = 0, 1, 2, 3, 4
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 # event kinds (order = tie-break class: completions first)
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3

@@ -148,7 +148,6 @@ struct KTimer {
 struct PassCmd {
   int kind;  // NOVA_DEC_VISION / PREFILL / DECODE
   int ctx, s_dec;
-  bool dec_float = false;  // NOVA_MODE_ADAPTIVE_FLOAT decode pass: full-GPU stream, all SMs
   std::vector<Request*> reqs;
   std::vector<int> forced_tok;  // per row, -1 = none
 };

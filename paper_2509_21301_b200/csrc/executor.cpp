@@ -162,9 +162,7 @@ void Worker::run() {
       c = std::move(q.front());
       q.pop_front();
     }
-    // ADAPTIVE_FLOAT: the front stays confined to its Eq. 5 partition, the decode pass may use
-    // every SM (its reserved slice is never occupied by front kernels)
-    cudaStream_t s = c.dec_float ? eng->stream_for(1, NOVA_CTX_SOLO, 0) : eng->stream_for(role, c.ctx, c.s_dec);
+    cudaStream_t s = eng->stream_for(role, c.ctx, c.s_dec);
     cudaError_t e = cudaSuccess;
     const bool timing = eng->sample_every > 0;
     eng->ktimer[role].on = timing && (eng->pass_count[role]++ % eng->sample_every == 0);
@@ -179,7 +177,7 @@ void Worker::run() {
       e = eng->run_prefill(c.reqs[0], s, eng->front_sms(c.s_dec));
       done.kind = NOVA_EV_PREFILL_DONE;
     } else {
-      e = eng->run_decode(c.reqs, c.forced_tok, s, c.dec_float ? eng->dec_sms(NOVA_CTX_SOLO, 0) : eng->dec_sms(c.ctx, c.s_dec));
+      e = eng->run_decode(c.reqs, c.forced_tok, s, eng->dec_sms(c.ctx, c.s_dec));
       done.kind = NOVA_EV_DECODE_DONE;
       for (Request* r : c.reqs) done.key = std::min<uint64_t>(done.key, r->id);
     }
@@ -537,7 +535,6 @@ void Engine::dispatch(const Decision& d) {
   c.kind = d.kind;
   c.ctx = d.ctx;
   c.s_dec = d.s_dec;
-  c.dec_float = d.kind == NOVA_DEC_DECODE && alg.pol.mode == NOVA_MODE_ADAPTIVE_FLOAT;
   c.reqs = d.reqs;
   if (d.kind == NOVA_DEC_DECODE) {
     c.forced_tok.assign(d.reqs.size(), -1);

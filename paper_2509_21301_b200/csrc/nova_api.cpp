@@ -100,7 +100,7 @@ nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* id) {
 nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, nova_partition_policy* applied) {
   if (!e || !p) return NOVA_E_INVAL;
   Engine& E = e->e;
-  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_ADAPTIVE_FLOAT) return E.fail(NOVA_E_INVAL, "mode");
+  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_MULTI_STREAM) return E.fail(NOVA_E_INVAL, "mode");
   const int g = E.alg.granularity, mx = E.alg.max_split;
   nova_partition_policy q = *p;
   auto rnd = [&](int v) { return v / g * g; };
@@ -114,7 +114,7 @@ nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, n
   if (q.mode == NOVA_MODE_STATIC && (q.sm_decode_dv < g || q.sm_decode_dp < g || q.sm_decode_dv > mx ||
                                      q.sm_decode_dp > mx))
     return E.fail(NOVA_E_PARTITION, "static decode budget outside [granularity, max split]");
-  if ((q.mode == NOVA_MODE_ADAPTIVE || q.mode == NOVA_MODE_ADAPTIVE_FLOAT) && (q.sm_min < g || q.sm_op_dv < q.sm_min || q.sm_op_dp < q.sm_min ||
+  if (q.mode == NOVA_MODE_ADAPTIVE && (q.sm_min < g || q.sm_op_dv < q.sm_min || q.sm_op_dp < q.sm_min ||
                                        q.sm_op_dv > mx || q.sm_op_dp > mx || q.alpha_dv < 0 || q.alpha_dp < 0))
     return E.fail(NOVA_E_PARTITION, "adaptive budgets outside [granularity, max split]");
   E.alg.pol = q;

@@ -15,7 +15,7 @@ import numpy as np
 from . import _abi as A
 from ._lib import lib
 
-SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, ADAPTIVE_FLOAT = 0, 1, 2, 3, 4, 5
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM = 0, 1, 2, 3, 4
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 DEC_VISION, DEC_PREFILL, DEC_DECODE, DEC_FINISH = 0, 1, 2, 3
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3

@@ -121,7 +121,7 @@ def _replay(log, reqs, pol):
     return n_dec
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])   # serial, static, adaptive, PF-Limit(5), multi-stream, float
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])   # serial, static, adaptive, PF-Limit(5), multi-stream
 @pytest.mark.parametrize("seed", [1, 2])
 def test_sim_decision_log_replays_on_oracle(E, mode, seed):
     rnd = random.Random(seed)

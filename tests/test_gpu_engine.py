@@ -95,9 +95,7 @@ def test_coexec_bitwise_equals_serial(tiny_setup):
                       ("adaptive", dict(mode=E.ADAPTIVE, sm_op_dv=48, sm_op_dp=40, sm_min=8, alpha_dv=13.0,
                                         alpha_dp=10.0, b_max=5)),
                       ("pf_limit", dict(mode=E.PF_LIMIT, pf_threshold=3)),
-                      ("multi_stream", dict(mode=E.MULTI_STREAM)),
-                      ("adaptive_float", dict(mode=E.ADAPTIVE_FLOAT, sm_op_dv=48, sm_op_dp=40, sm_min=8,
-                                              alpha_dv=13.0, alpha_dp=10.0, b_max=5))]:
+                      ("multi_stream", dict(mode=E.MULTI_STREAM))]:
         e.set_partition(**pol)
         results[name] = _run(e, reqs)
     base = results["serial"]
