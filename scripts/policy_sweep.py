@@ -36,7 +36,7 @@ def main():
                       "t_v_ms": [round(x, 2) for x in curves["t_v_ms"]]}), flush=True)
     t_front = (0.5 * (curves["t_v_solo_ms"] + curves["t_v_solo_7920_ms"]) + curves["t_p_solo_ms"]) / 1000.0
     pols = [("adaptive_plan", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=plan["sm_min"],
-                                   alpha_dv=plan["alpha_dv"], alpha_dp=plan["alpha_dp"], b_max=16)))]
+                                   alpha_dv=plan["alpha_dv"], alpha_dp=plan["alpha_dp"], b_max=16))]
     for op in a.sm_op:
         smin = min(plan["sm_min"], op)
         pols.append((f"adaptive_op{op}", dict(mode=E.ADAPTIVE, sm_op_dv=op, sm_op_dp=op, sm_min=smin,
