@@ -395,6 +395,8 @@ def main():
     else:
         curves, plan = profile_and_plan(eng, args.quick, log)
     sv, sp = plan["best"][0], plan["best"][1]
+    if plan.get("points"):
+        eng.set_frontier(plan["points"], window=16)   # FRONTIER mode
     policy = dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=plan["sm_min"], alpha_dv=plan["alpha_dv"],
                   alpha_dp=plan["alpha_dp"], b_max=16)
     eng.set_partition(**policy)
@@ -489,6 +491,8 @@ def main():
                 # co-running stages with no SM partition (both streams see every SM)
                 ("pf_limit_5", dict(mode=E.PF_LIMIT, pf_threshold=5, b_max=16)),
                 ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16))]
+        if plan.get("points"):   # Pareto point for the estimated arrival rate
+            pols.append(("frontier", dict(mode=E.FRONTIER, b_max=16)))
         for rho in args.compare_rho:
             trs = [make_trace(shape, args.requests, rho, t_front, 61 + k) for k in range(args.compare_seeds)]
             runs = {name: [] for name, _ in pols}

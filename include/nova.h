@@ -123,9 +123,14 @@ nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* req_id)
  *   front stage first; a decode iteration runs when more than pf_threshold requests wait for
  *   decode, or when no front work is ready.
  * MULTI_STREAM: the paper's multi-stream baseline: front and decode co-run on two
- *   streams that both see every SM (no partition; the hardware arbitrates). */
+ *   streams that both see every SM (no partition; the hardware arbitrates).
+ * FRONTIER: SURVEY.md §8(f) f3, the frontier-lookup controller: instead of Eq. 5's linear
+ *   rule, each co-run pass takes the Pareto point (nova_set_frontier) with the lowest Eq. 1
+ *   E2E among those whose Eq. 4 throughput covers the estimated arrival rate (the last
+ *   `window` arrivals); if none does, the highest-throughput point (P:356 -- the frontier is
+ *   the paper's justification for Eq. 5). */
 enum { NOVA_MODE_SERIAL = 0, NOVA_MODE_STATIC = 1, NOVA_MODE_ADAPTIVE = 2, NOVA_MODE_PF_LIMIT = 3,
-       NOVA_MODE_MULTI_STREAM = 4 };
+       NOVA_MODE_MULTI_STREAM = 4, NOVA_MODE_FRONTIER = 5 };
 enum { NOVA_CTX_DV = 0, NOVA_CTX_DP = 1, NOVA_CTX_SOLO = 2 };
 typedef struct {
   int32_t mode;                        /* NOVA_MODE_*                                           */
@@ -257,6 +262,10 @@ typedef struct {
 nova_status nova_plan(const nova_curves* c, double gen_len, double tau, nova_plan_point* pts, int32_t cap,
                       int32_t* n_out, nova_plan_point* best, int32_t* sm_min_out, double* alpha_dv_out,
                       double* alpha_dp_out);
+/* Frontier points for NOVA_MODE_FRONTIER (copied; points with on_frontier == 0 are ignored;
+ * s_v / s_p must be realisable splits).  window >= 2: arrivals in the rate estimate
+ * lambda = (window - 1) / (t_last - t_first).  Set before selecting the mode. */
+nova_status nova_set_frontier(nova_engine* e, const nova_plan_point* pts, int32_t n, int32_t window);
 /* Eq. 5: max(SM_min, floor_g(SM_op - alpha (max(N_pend, 1) - 1))). */
 int32_t nova_adaptive_sm(int32_t sm_op, int32_t sm_min, double alpha, int32_t n_pending, int32_t granularity);
 /* Eq. 7 and Eq. 8 (offload ring). */

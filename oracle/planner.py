@@ -103,6 +103,25 @@ def adaptive_sm(sm_op: int, sm_min: int, alpha: float, n_pend: int, granularity:
     return max(sm_min, floored)
 
 
+def frontier_pick(frontier, lam: float):
+    """SURVEY.md §8(f) f3 frontier lookup (the paper motivates Eq. 5 by the Pareto frontier,
+    P:356): among frontier points (s_v, s_p, e2e, thr) whose Eq. 4 throughput covers the arrival
+    rate lam, the one with the lowest Eq. 1 E2E (ties: larger s_v, then s_p, as Eq. 3); if none
+    covers lam, the highest throughput (ties: lower E2E)."""
+    pts = [(p.s_v, p.s_p, p.e2e, p.thr) if hasattr(p, "s_v") else tuple(p[:4]) for p in frontier]
+    ok = [p for p in pts if p[3] >= lam]
+    if ok:
+        return min(ok, key=lambda p: (p[2], -p[0], -p[1]))
+    return max(pts, key=lambda p: (p[3], -p[2]))
+
+
+def arrival_rate(times_ns) -> float:
+    """req/s over a window of arrival times: (n - 1) / (t_last - t_first); 0 with < 2 arrivals."""
+    if len(times_ns) < 2 or times_ns[-1] <= times_ns[0]:
+        return 0.0
+    return (len(times_ns) - 1) * 1e9 / (times_ns[-1] - times_ns[0])
+
+
 def plan(s, t_v, t_p, td_v, td_p, L, td_full=None, tau=2.5):
     """Whole planner: points, frontier, Eq. 3 best, SM_min, alpha per context."""
     pts = enumerate_points(s, t_v, t_p, td_v, td_p, L)

@@ -28,6 +28,9 @@ Readings (R13-R17):
     Reading (R21): decode also runs when no front work is ready.
   * MULTI_STREAM (the paper's baseline): stages co-run like Nova but every
     pass sees all SMs ("CUDA's default multi-stream scheduling policy").
+  * FRONTIER: co-run like ADAPTIVE, but the decode split of a
+    co-run pass is the Pareto point picked for the arrival rate estimated over the
+    last lam_window arrivals (planner.frontier_pick), instead of Eq. 5.
 The same state machine drives `simulate` (virtual time, durations from curves),
 which checks the worked example of SURVEY.md §8(c) c6 by hand values.
 """
@@ -36,9 +39,9 @@ from __future__ import annotations
 from collections import deque
 from dataclasses import dataclass, field
 
-from .planner import adaptive_sm
+from .planner import adaptive_sm, arrival_rate, frontier_pick
 
-SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM = 0, 1, 2, 3, 4
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, FRONTIER = 0, 1, 2, 3, 4, 5
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 # event kinds (order = tie-break class: completions first)
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
@@ -60,6 +63,8 @@ class Policy:
     alpha_dp: float = 8.0
     b_max: int = 16
     pf_threshold: int = 5       # PF_LIMIT
+    frontier: list = field(default_factory=list)   # FRONTIER: (s_v, s_p, e2e, thr) Pareto points
+    lam_window: int = 16        # FRONTIER: arrivals in the rate estimate
 
 
 @dataclass
@@ -84,6 +89,7 @@ class Alg1:
         self.q_d: list[int] = []            # decode-ready, kept in join order
         self.join_counter = 0
         self.last_pass = None               # SERIAL alternation
+        self.arr_t: deque[int] = deque(maxlen=max(2, policy.lam_window))   # FRONTIER rate estimate
         self.log: list[tuple] = []
 
     # -- Eq. 5 / static split for a co-run context
@@ -93,6 +99,9 @@ class Alg1:
             return p.total_sms
         if p.mode == STATIC:
             return p.sm_decode_dv if ctx == CTX_DV else p.sm_decode_dp
+        if p.mode == FRONTIER and p.frontier:
+            pt = frontier_pick(p.frontier, arrival_rate(list(self.arr_t)))
+            return pt[0] if ctx == CTX_DV else pt[1]
         if ctx == CTX_DV:
             return adaptive_sm(p.sm_op_dv, p.sm_min, p.alpha_dv, n_pend, p.granularity)
         return adaptive_sm(p.sm_op_dp, p.sm_min, p.alpha_dp, n_pend, p.granularity)
@@ -127,11 +136,15 @@ class Alg1:
         self.reqs[rid] = Req(rid, gen_len)
 
     def tick(self, events: list[tuple]) -> list[tuple]:
-        """events: (kind, key, payload) -- payload rid (or list of rids for DECODE_DONE)."""
+        """events: (kind, key, payload[, t_ns]) -- payload rid (or list of rids for DECODE_DONE);
+        arrivals may carry their arrival time (FRONTIER's rate estimate)."""
         out: list[tuple] = []
-        for kind, _, payload in sorted(events, key=lambda e: (e[0] == EV_ARRIVAL, e[1], e[0])):
+        for ev in sorted(events, key=lambda e: (e[0] == EV_ARRIVAL, e[1], e[0])):
+            kind, _, payload = ev[:3]
             if kind == EV_ARRIVAL:
                 self.q_v.append(payload)
+                if len(ev) > 3:
+                    self.arr_t.append(ev[3])
             elif kind == EV_VISION_DONE:
                 self.vision_running = None
                 self.prefill_wait.append(payload)
@@ -261,9 +274,10 @@ def simulate(policy: Policy, curves: SimCurves, requests: list[SimRequest]):
             pending.remove(p)
             evs.append(p[1:])
         while ai < len(arrivals) and arrivals[ai].arrival_ns == t:
-            evs.append((EV_ARRIVAL, arrivals[ai].rid, arrivals[ai].rid))
+            evs.append((EV_ARRIVAL, arrivals[ai].rid, arrivals[ai].rid, arrivals[ai].arrival_ns))
             ai += 1
-        for kind, _, payload in evs:
+        for ev in evs:
+            kind, payload = ev[0], ev[2]
             if kind == EV_PREFILL_DONE:
                 tokens[payload].append(t)
             elif kind == EV_DECODE_DONE:

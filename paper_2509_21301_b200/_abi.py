@@ -84,6 +84,7 @@ ENGINE_SIGNATURES = {
     "nova_query_sms": (R, [E, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
     "nova_submit": (R, [E, C.POINTER(Request), C.POINTER(U64)]),
     "nova_set_partition": (R, [E, C.POINTER(PartitionPolicy), C.POINTER(PartitionPolicy)]),
+    "nova_set_frontier": (R, [E, C.POINTER(PlanPoint), I32, I32]),
     "nova_step": (R, [E, I64, C.POINTER(StepInfo)]),
     "nova_poll_tokens": (R, [E, C.POINTER(Token), I32, C.POINTER(I32)]),
     "nova_request_stats": (R, [E, U64, C.POINTER(ReqStats)]),

@@ -21,9 +21,35 @@ int64_t mono_ns() {
 // ---------------------------------------------------------------- Eq. 5
 static int floor_g(double v, int g) { return (int)std::floor(v / g + 1e-9) * g; }
 
+double Alg1::arrival_rate() const {
+  if (arr_t.size() < 2 || arr_t.back() <= arr_t.front()) return 0.0;
+  return (double)(arr_t.size() - 1) * 1e9 / (double)(arr_t.back() - arr_t.front());
+}
+
+// Frontier lookup: lowest Eq. 1 E2E among the Pareto points whose Eq. 4
+// throughput covers the estimated arrival rate; ties -> more decode SMs (s_v, then s_p, as
+// Eq. 3); if no point covers it, the highest throughput (ties -> lower E2E).
+static const nova_plan_point* frontier_pick(const std::vector<nova_plan_point>& F, double lam) {
+  const nova_plan_point* best = nullptr;
+  for (const auto& p : F) {
+    if (p.thr_rps < lam) continue;
+    if (!best || p.e2e_ms < best->e2e_ms ||
+        (p.e2e_ms == best->e2e_ms && (p.s_v > best->s_v || (p.s_v == best->s_v && p.s_p > best->s_p))))
+      best = &p;
+  }
+  if (best) return best;
+  for (const auto& p : F)
+    if (!best || p.thr_rps > best->thr_rps || (p.thr_rps == best->thr_rps && p.e2e_ms < best->e2e_ms)) best = &p;
+  return best;
+}
+
 int Alg1::split(int ctx, int n_pend) const {
   if (ctx == NOVA_CTX_SOLO) return total_sms;
   if (pol.mode == NOVA_MODE_STATIC) return ctx == NOVA_CTX_DV ? pol.sm_decode_dv : pol.sm_decode_dp;
+  if (pol.mode == NOVA_MODE_FRONTIER && !frontier.empty()) {
+    const nova_plan_point* p = frontier_pick(frontier, arrival_rate());
+    return ctx == NOVA_CTX_DV ? p->s_v : p->s_p;
+  }
   const int op = ctx == NOVA_CTX_DV ? pol.sm_op_dv : pol.sm_op_dp;
   const double a = ctx == NOVA_CTX_DV ? pol.alpha_dv : pol.alpha_dp;
   const int v = floor_g(op - a * (std::max(n_pend, 1) - 1), granularity);
@@ -90,7 +116,11 @@ std::vector<Decision> Alg1::tick(std::vector<Event>& evs) {
   std::vector<Decision> out;
   for (Event& e : evs) {
     switch (e.kind) {
-      case NOVA_EV_ARRIVAL: q_v.push_back(e.reqs[0]); break;
+      case NOVA_EV_ARRIVAL:
+        q_v.push_back(e.reqs[0]);
+        arr_t.push_back(e.t);
+        while ((int)arr_t.size() > std::max(2, lam_window)) arr_t.pop_front();
+        break;
       case NOVA_EV_VISION_DONE:
         vision_running = nullptr;
         prefill_wait.push_back(e.reqs[0]);

@@ -94,6 +94,11 @@ struct Alg1 {
   std::vector<Request*> q_d;
   int64_t join_counter = 0;
   int last_pass = -1;  // 0 front, 1 decode
+  // NOVA_MODE_FRONTIER: Pareto points and the recent arrival times (rate estimate)
+  std::vector<nova_plan_point> frontier;
+  int lam_window = 16;
+  std::deque<int64_t> arr_t;
+  double arrival_rate() const;  // req/s over the last lam_window arrivals (0 if < 2)
   int split(int ctx, int n_pend) const;
   int n_pend() const;
   bool front_running() const { return vision_running || prefill_running; }

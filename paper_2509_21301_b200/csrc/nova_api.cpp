@@ -97,10 +97,29 @@ nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* id) {
   GUARD({ return e->e.submit(r, id); })
 }
 
+nova_status nova_set_frontier(nova_engine* e, const nova_plan_point* pts, int32_t n, int32_t window) {
+  if (!e || (!pts && n > 0) || n < 0 || window < 2) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  const int g = E.alg.granularity, mx = E.alg.max_split;
+  std::vector<nova_plan_point> f;
+  for (int i = 0; i < n; ++i) {
+    if (!pts[i].on_frontier) continue;
+    if (pts[i].s_v < g || pts[i].s_p < g || pts[i].s_v > mx || pts[i].s_p > mx || pts[i].s_v % g || pts[i].s_p % g)
+      return E.fail(NOVA_E_PARTITION, "frontier split not realisable");
+    f.push_back(pts[i]);
+  }
+  if (f.empty()) return E.fail(NOVA_E_INVAL, "no frontier point");
+  E.alg.frontier = f;
+  E.alg.lam_window = window;
+  return NOVA_OK;
+}
+
 nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, nova_partition_policy* applied) {
   if (!e || !p) return NOVA_E_INVAL;
   Engine& E = e->e;
-  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_MULTI_STREAM) return E.fail(NOVA_E_INVAL, "mode");
+  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_FRONTIER) return E.fail(NOVA_E_INVAL, "mode");
+  if (p->mode == NOVA_MODE_FRONTIER && E.alg.frontier.empty())
+    return E.fail(NOVA_E_STATE, "FRONTIER mode needs nova_set_frontier first");
   const int g = E.alg.granularity, mx = E.alg.max_split;
   nova_partition_policy q = *p;
   auto rnd = [&](int v) { return v / g * g; };

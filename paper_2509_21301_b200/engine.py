@@ -15,7 +15,7 @@ import numpy as np
 from . import _abi as A
 from ._lib import lib
 
-SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM = 0, 1, 2, 3, 4
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, FRONTIER = 0, 1, 2, 3, 4, 5
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 DEC_VISION, DEC_PREFILL, DEC_DECODE, DEC_FINISH = 0, 1, 2, 3
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
@@ -148,6 +148,12 @@ class Engine:
         out = A.PartitionPolicy()
         self._check(self.lib.nova_set_partition(self.h, C.byref(p), C.byref(out)), "nova_set_partition")
         return out
+
+    def set_frontier(self, points, window: int = 16) -> None:
+        """points: (s_v, s_p, e2e_ms, thr_rps, on_frontier) tuples (nova_plan's 'points')."""
+        arr = (A.PlanPoint * len(points))(*[A.PlanPoint(int(a), int(b), float(c), float(d), int(f), 0)
+                                            for a, b, c, d, f in points])
+        self._check(self.lib.nova_set_frontier(self.h, arr, len(points), window), "nova_set_frontier")
 
     # -------------------------------------------------------------- serving
     def submit(self, pixels: np.ndarray | None, prompt_ids, gen_len: int, arrival_ns: int = 0, grid=None,

@@ -112,7 +112,7 @@ def _replay(log, reqs, pol):
         for tick, is_ev, kind, ctx, s, ids, tns in ticks[t]:
             if is_ev:
                 payload = list(ids) if kind == OS.EV_DECODE_DONE else ids[0]
-                evs.append((kind, min(ids), payload))
+                evs.append((kind, min(ids), payload, tns))
             else:
                 decs.append((kind, tuple(ids), ctx, s))
         want = alg.tick(evs)
@@ -121,7 +121,7 @@ def _replay(log, reqs, pol):
     return n_dec
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])   # serial, static, adaptive, PF-Limit(5), multi-stream
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])  # serial, static, adaptive, PF-Limit(5), multi-stream, frontier
 @pytest.mark.parametrize("seed", [1, 2])
 def test_sim_decision_log_replays_on_oracle(E, mode, seed):
     rnd = random.Random(seed)
@@ -131,7 +131,18 @@ def test_sim_decision_log_replays_on_oracle(E, mode, seed):
     td = [int(0.7 * MS * max(1.0, 32 / s)) for s in splits]
     pol = dict(sm_decode_dv=48, sm_decode_dp=40, sm_op_dv=64, sm_op_dp=56, sm_min=16, alpha_dv=16.0,
                alpha_dp=13.3, b_max=8)
-    e = _sim_engine(E, mode, splits, tv, tp, td, td, (9 * MS, 3 * MS, int(0.7 * MS)), beta=0.03, **pol)
+    extra = {}
+    if mode == OS.FRONTIER:   # Pareto frontier of the same curves (oracle planner), window 8
+        ms = lambda xs: [x / MS for x in xs]
+        fr = P.pareto_frontier(P.enumerate_points(splits, ms(tv), ms(tp), ms(td), ms(td), 8))
+        extra = dict(frontier=[(p.s_v, p.s_p, p.e2e, p.thr) for p in fr], lam_window=8)
+        e = E.Engine(TINY, E.EngineOptions(backend=E.BACKEND_SIM, max_requests=512, max_gen=512))
+        e.sim_set_curves(splits, tv, tp, td, td, 9 * MS, 3 * MS, int(0.7 * MS), beta=0.03)
+        e.finalize()
+        e.set_frontier([(a, b, c, d, 1) for a, b, c, d in extra["frontier"]], window=8)
+        e.set_partition(mode, **pol)
+    else:
+        e = _sim_engine(E, mode, splits, tv, tp, td, td, (9 * MS, 3 * MS, int(0.7 * MS)), beta=0.03, **pol)
     t, gens = 0, {}
     for i in range(120):
         t += int(rnd.expovariate(1 / 6.0) * MS) if rnd.random() < 0.8 else 0     # bursts of equal timestamps
@@ -142,7 +153,7 @@ def test_sim_decision_log_replays_on_oracle(E, mode, seed):
     while e.step().events:
         pass
     log = e.decision_log()
-    opol = OS.Policy(mode=mode, total_sms=148, granularity=8, **pol)
+    opol = OS.Policy(mode=mode, total_sms=148, granularity=8, **pol, **extra)
     n = _replay(log, gens, opol)
     fin = [r for r in log if not r[1] and r[2] == OS.D_FINISH]
     assert len(fin) == len(gens) and n > 3 * len(gens)

@@ -3,7 +3,8 @@ oracle on the same generated weights and inputs (SURVEY.md §8(c) c1', c6).
 
 - cfg 1 tiny VLM: greedy tokens identical, logits max-abs <= 3e-2 (BASELINE).
 - co-execution == serial: tokens and f32 logits bitwise identical across SERIAL,
-  STATIC splits, ADAPTIVE and the paper's PF-Limit / Multi-Stream baselines on a
+  STATIC splits, ADAPTIVE, the frontier-lookup controller and the paper's PF-Limit /
+  Multi-Stream baselines on a
   20-request trace (BASELINE).
 - offload: K = 2, 3 physical ViT layers give bitwise the all-resident outputs.
 - full width (reduced depth): 2B / 7B widths at the BASELINE image size (N = 4888),
@@ -95,7 +96,10 @@ def test_coexec_bitwise_equals_serial(tiny_setup):
                       ("adaptive", dict(mode=E.ADAPTIVE, sm_op_dv=48, sm_op_dp=40, sm_min=8, alpha_dv=13.0,
                                         alpha_dp=10.0, b_max=5)),
                       ("pf_limit", dict(mode=E.PF_LIMIT, pf_threshold=3)),
-                      ("multi_stream", dict(mode=E.MULTI_STREAM))]:
+                      ("multi_stream", dict(mode=E.MULTI_STREAM)),
+                      ("frontier", dict(mode=E.FRONTIER))]:
+        if pol["mode"] == E.FRONTIER:   # two Pareto points: the lookup switches with the arrival rate
+            e.set_frontier([(48, 40, 100.0, 5.0, 1), (16, 16, 140.0, 50.0, 1)], window=4)
         e.set_partition(**pol)
         results[name] = _run(e, reqs)
     base = results["serial"]

@@ -167,3 +167,26 @@ def test_layer_vision_memory_accounting():
     assert max(inc) - min(inc) <= 0.1 + 1e-9          # printed to 0.1 MB
     per_layer = sum(inc) / len(inc)
     assert t["vit_layers"] * per_layer <= t["raw_MB"]  # the layer stack fits in the raw footprint
+
+
+def test_frontier_lookup_pins():
+    """Frontier-lookup controller against the paper's own planner pieces:
+    at zero load it picks the Eq. 3 optimum (the global E2E minimum lies on the frontier); above
+    every point's throughput it picks the highest-throughput point (the smallest front+prefill
+    time, i.e. the fewest decode SMs here); picks are monotone in the arrival rate; and the rate
+    estimate is exact on evenly spaced arrivals."""
+    s = [8, 16, 24, 32]
+    pts = P.enumerate_points(s, [100, 110, 125, 150], [40, 45, 52, 60], [12, 8, 6, 5.5], [14, 9, 7, 6], 10)
+    fr = P.pareto_frontier(pts)
+    best = P.optimal_static(pts)
+    assert P.frontier_pick(fr, 0.0)[:2] == (best.s_v, best.s_p)
+    top = max(pts, key=lambda p: p.thr)
+    assert P.frontier_pick(fr, 1e9)[:2] == (top.s_v, top.s_p) == (8, 8)
+    lams = [0.0, 5.0, 6.5, 7.0, 7.05, 7.15, 100.0]
+    picks = [P.frontier_pick(fr, lam) for lam in lams]
+    for a, b in zip(picks, picks[1:]):
+        assert b[3] >= a[3] and b[2] >= a[2]
+    for lam, p in zip(lams, picks):   # covers lam whenever some point does
+        assert p[3] >= lam or all(q.thr < lam for q in fr)
+    assert P.arrival_rate([0, 10_000_000, 20_000_000, 30_000_000]) == 100.0
+    assert P.arrival_rate([5]) == 0.0
