@@ -247,11 +247,19 @@ def replay(eng, inputs, t0=None, rank=0, world=1, board=None, policy="jsq"):
     for th in threads:
         th.start()
     toks, first = [], 0
+    last_progress = time.monotonic()
     while True:
         info = eng.step(500)
         if sub_err:
             raise sub_err[0]
         new = eng.poll_tokens(1 << 16)
+        if new or info.events:
+            last_progress = time.monotonic()
+        elif time.monotonic() - last_progress > 120.0:   # watchdog: report a stall instead of hanging
+            log = eng.decision_log()
+            raise RuntimeError(f"replay stalled 120 s: submitted {state['submitted']}, finished "
+                               f"{info.finished - base_finished}, pending {info.n_pending}, active {info.active}, "
+                               f"last decisions {log[-6:]}")
         toks += new
         first += sum(1 for t in new if t[1] == 0)
         if board is not None:
@@ -635,4 +643,12 @@ def main():
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    try:
+        rc = main()
+    except Exception as ex:   # report and exit without joining possibly stuck engine threads
+        import traceback
+        traceback.print_exc()
+        print(json.dumps({"metric": METRIC, "error": f"{type(ex).__name__}: {ex}"[:2000]}), flush=True)
+        sys.stderr.flush()
+        os._exit(1)
+    sys.exit(rc)

@@ -939,6 +939,23 @@ __global__ void __launch_bounds__(384, 1)
 // O rescaling (rare, lazy) waits for PV_x(j-1) through o_ready[x], since S_x(j) no longer
 // orders after it.  Numerics per (row, head): fixed key order, fixed 64-key tiling.
 constexpr int KT4 = 64;    // keys per tile
+// exp2 of a pair on the FMA pipe (FA4's MUFU offload), for x <= 0: x = n + f with n = rint(x)
+// by the 1.5 * 2^23 magic add, f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (max rel err
+// 7.5e-5, far below P's bf16 rounding); 2^n added into the exponent field with one IMAD
+// ((bits(t) << 23) == n << 23 mod 2^32 because bits(1.5 * 2^23) has nine zero low bits).
+NOVA_DEV float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));
+  float2 p = __ffma2_rn(make_float2(0.05517149344f, 0.05517149344f), f, make_float2(0.24261111021f, 0.24261111021f));
+  p = __ffma2_rn(p, f, make_float2(0.69326102734f, 0.69326102734f));
+  p = __ffma2_rn(p, f, make_float2(0.99992805719f, 0.99992805719f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x)),
+                     __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y)));
+}
+constexpr int EXP_POLY_OF_8 = 2;  // pairs of P per 8 whose exponentials run on the FMA pipe
 constexpr int KST4 = 4;    // K / V ring depth
 template <int HD>
 struct Ft4Cfg {
@@ -1183,7 +1200,15 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int i = 0; i < KT4; i += 2) {
           const float2 xx = __ffma2_rn(make_float2(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sc2, nm2);
-          const float p0 = fast_exp2(xx.x), p1 = fast_exp2(xx.y);
+          float p0, p1;
+          if (((i >> 1) & 7) < EXP_POLY_OF_8) {
+            const float2 pp = exp2_fma2(xx);
+            p0 = pp.x;
+            p1 = pp.y;
+          } else {
+            p0 = fast_exp2(xx.x);
+            p1 = fast_exp2(xx.y);
+          }
           ls2[(i >> 1) & 3] = __fadd2_rn(ls2[(i >> 1) & 3], make_float2(p0, p1));
           pk[i / 2] = pack_bf16(p0, p1);
         }
