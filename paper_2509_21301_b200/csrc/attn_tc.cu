@@ -1052,6 +1052,14 @@ __global__ void __launch_bounds__(384, 1)
         }
         ++nu;
       }
+      // producer tail: the MMA warp's releases (asynchronous tcgen05.commit arrives) of the last
+      // ring slots have landed before this CTA can exit and hand its shared memory to a successor
+      for (int i = 0; i < KST4; ++i, ++g) {
+        const int st = g % KST4;
+        const uint32_t ph = ((g / KST4) & 1) ^ 1;
+        mbar_wait(&k_empty[st], ph);
+        mbar_wait(&v_empty[st], ph);
+      }
      }
     } else if (warp == 1) {  // ---------------- MMA issuer: the whole warp waits, lane 0 issues
       // Descriptors are built once from warp-uniform values (uniform registers); per MMA only a
@@ -1120,6 +1128,10 @@ __global__ void __launch_bounds__(384, 1)
         }
         commit(o_done);
         ++nu;
+      }
+      if (g > 0) {  // the last PV releases (o_ready) have landed too (nothing else waits for them)
+        mbar_wait(&o_ready[0], (g - 1) & 1);
+        mbar_wait(&o_ready[1], (g - 1) & 1);
       }
     }
   } else {  // ---------------- softmax warpgroups: x = 0 (warps 4-7, tile A), 1 (warps 8-11, tile B)

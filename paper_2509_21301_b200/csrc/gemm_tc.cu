@@ -167,6 +167,16 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
       }
+      // producer tail: wait until the MMA commits have released every stage, so no asynchronous
+      // mbarrier arrive can land in this CTA's shared memory after it exits (a PDL successor may
+      // already own that memory)
+      for (int i = 0; i < STAGES; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     {  // ---------------- MMA issuer: whole warp (convergent), one elected lane issues
@@ -358,6 +368,14 @@ __global__ void __launch_bounds__(384, 1)
             stage = 0;
             phase ^= 1;
           }
+        }
+      }
+      // producer tail: every multicast release of this CTA's stages has landed before it exits
+      for (int i = 0; i < STAGES; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
