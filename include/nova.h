@@ -139,6 +139,9 @@ typedef struct {
   float alpha_dv, alpha_dp;
   int32_t b_max;                       /* decode batch cap (<= max_decode_batch)                 */
   int32_t pf_threshold;                /* PF_LIMIT: decode when > pf_threshold wait (<= 0: 5)     */
+  int32_t sm_dv_floor;                 /* ADAPTIVE / FRONTIER: decode SMs never below this while
+                                          co-running with vision (offload-aware, see
+                                          nova_offload_floor); 0 = none                       */
 } nova_partition_policy;
 /* Takes effect at each role's next forward pass.  `applied` (may be NULL)
  * receives the values rounded down to the granularity.  NOVA_E_PARTITION if a
@@ -266,6 +269,13 @@ nova_status nova_plan(const nova_curves* c, double gen_len, double tau, nova_pla
  * s_v / s_p must be realisable splits).  window >= 2: arrivals in the rate estimate
  * lambda = (window - 1) / (t_last - t_first).  Set before selecting the mode. */
 nova_status nova_set_frontier(nova_engine* e, const nova_plan_point* pts, int32_t n, int32_t window);
+/* Offload-aware split (Eq. 8): with layer-wise ViT
+ * offload a vision pass cannot finish before its weights stream in (t_h2d_ms), so front SMs
+ * beyond those that meet t_h2d are idle.  Returns the largest decode split s[i] whose vision
+ * time on the complementary partition t_v[i] is still <= t_h2d_ms (those SMs cost the
+ * vision pass nothing), or 0 if no split qualifies.  s ascending, t_v[i] the vision pass with
+ * decode on s[i] SMs. */
+int32_t nova_offload_floor(const int32_t* s, const double* t_v, int32_t n, double t_h2d_ms);
 /* Eq. 5: max(SM_min, floor_g(SM_op - alpha (max(N_pend, 1) - 1))). */
 int32_t nova_adaptive_sm(int32_t sm_op, int32_t sm_min, double alpha, int32_t n_pending, int32_t granularity);
 /* Eq. 7 and Eq. 8 (offload ring). */

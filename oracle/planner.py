@@ -115,6 +115,14 @@ def frontier_pick(frontier, lam: float):
     return max(pts, key=lambda p: (p[3], -p[2]))
 
 
+def offload_floor(s, t_v, t_h2d_ms) -> int:
+    """SURVEY.md §8(f) f3 with PAPER.md Eq. 8: under layer-wise offload a vision pass
+    lasts at least the weight streaming time t_h2d; decode may take every split whose vision
+    time on the remaining SMs still fits in it.  Largest such s, else 0."""
+    ok = [si for si, tv in zip(s, t_v) if tv <= t_h2d_ms]
+    return max(ok) if ok else 0
+
+
 def arrival_rate(times_ns) -> float:
     """req/s over a window of arrival times: (n - 1) / (t_last - t_first); 0 with < 2 arrivals."""
     if len(times_ns) < 2 or times_ns[-1] <= times_ns[0]:

@@ -65,6 +65,7 @@ class Policy:
     pf_threshold: int = 5       # PF_LIMIT
     frontier: list = field(default_factory=list)   # FRONTIER: (s_v, s_p, e2e, thr) Pareto points
     lam_window: int = 16        # FRONTIER: arrivals in the rate estimate
+    sm_dv_floor: int = 0        # offload-aware floor of the decode split while vision co-runs (f3)
 
 
 @dataclass
@@ -99,12 +100,13 @@ class Alg1:
             return p.total_sms
         if p.mode == STATIC:
             return p.sm_decode_dv if ctx == CTX_DV else p.sm_decode_dp
+        fl = p.sm_dv_floor if ctx == CTX_DV else 0
         if p.mode == FRONTIER and p.frontier:
             pt = frontier_pick(p.frontier, arrival_rate(list(self.arr_t)))
-            return pt[0] if ctx == CTX_DV else pt[1]
+            return max(fl, pt[0] if ctx == CTX_DV else pt[1])
         if ctx == CTX_DV:
-            return adaptive_sm(p.sm_op_dv, p.sm_min, p.alpha_dv, n_pend, p.granularity)
-        return adaptive_sm(p.sm_op_dp, p.sm_min, p.alpha_dp, n_pend, p.granularity)
+            return max(fl, adaptive_sm(p.sm_op_dv, p.sm_min, p.alpha_dv, n_pend, p.granularity))
+        return max(fl, adaptive_sm(p.sm_op_dp, p.sm_min, p.alpha_dp, n_pend, p.granularity))
 
     def n_pend(self) -> int:
         return (len(self.q_v) + (self.vision_running is not None) + len(self.prefill_wait)

@@ -33,7 +33,7 @@ class Request(C.Structure):
 class PartitionPolicy(C.Structure):
     _fields_ = [("mode", I32), ("sm_decode_dv", I32), ("sm_decode_dp", I32), ("sm_op_dv", I32),
                 ("sm_op_dp", I32), ("sm_min", I32), ("alpha_dv", F32), ("alpha_dp", F32), ("b_max", I32),
-                ("pf_threshold", I32)]
+                ("pf_threshold", I32), ("sm_dv_floor", I32)]
 
 
 class StepInfo(C.Structure):
@@ -97,6 +97,7 @@ ENGINE_SIGNATURES = {
     "nova_adaptive_sm": (I32, [I32, I32, F64, I32, I32]),
     "nova_next_logical_layer": (I32, [I32, I32, I32]),
     "nova_required_bandwidth": (F64, [F64, F64, I32, I32]),
+    "nova_offload_floor": (I32, [C.POINTER(I32), C.POINTER(F64), I32, F64]),
     "nova_sim_set_curves": (R, [E, C.POINTER(SimCurves)]),
     "nova_kernel_timing": (R, [E, I32]),
     "nova_kernel_stats": (R, [E, I32, C.POINTER(F64)]),

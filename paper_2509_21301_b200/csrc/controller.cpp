@@ -46,14 +46,16 @@ static const nova_plan_point* frontier_pick(const std::vector<nova_plan_point>& 
 int Alg1::split(int ctx, int n_pend) const {
   if (ctx == NOVA_CTX_SOLO) return total_sms;
   if (pol.mode == NOVA_MODE_STATIC) return ctx == NOVA_CTX_DV ? pol.sm_decode_dv : pol.sm_decode_dp;
+  // offload-aware floor (f3): while vision co-runs, decode keeps at least sm_dv_floor SMs
+  const int fl = ctx == NOVA_CTX_DV ? pol.sm_dv_floor : 0;
   if (pol.mode == NOVA_MODE_FRONTIER && !frontier.empty()) {
     const nova_plan_point* p = frontier_pick(frontier, arrival_rate());
-    return ctx == NOVA_CTX_DV ? p->s_v : p->s_p;
+    return std::max(fl, ctx == NOVA_CTX_DV ? p->s_v : p->s_p);
   }
   const int op = ctx == NOVA_CTX_DV ? pol.sm_op_dv : pol.sm_op_dp;
   const double a = ctx == NOVA_CTX_DV ? pol.alpha_dv : pol.alpha_dp;
   const int v = floor_g(op - a * (std::max(n_pend, 1) - 1), granularity);
-  return std::max(pol.sm_min, v);
+  return std::max(fl, std::max(pol.sm_min, v));
 }
 
 int Alg1::n_pend() const {
@@ -187,6 +189,14 @@ int32_t nova_adaptive_sm(int32_t sm_op, int32_t sm_min, double alpha, int32_t n_
 }
 
 int32_t nova_next_logical_layer(int32_t cur, int32_t K, int32_t L) { return (cur + K) % L; }
+
+int32_t nova_offload_floor(const int32_t* s, const double* t_v, int32_t n, double t_h2d_ms) {
+  int32_t best = 0;
+  if (!s || !t_v) return 0;
+  for (int i = 0; i < n; ++i)
+    if (t_v[i] <= t_h2d_ms) best = std::max(best, s[i]);
+  return best;
+}
 
 double nova_required_bandwidth(double bytes, double forward_s, int32_t L, int32_t K) {
   return bytes / forward_s * (double)(L - K) / (double)(L - 2);

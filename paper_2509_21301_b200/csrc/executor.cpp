@@ -240,7 +240,7 @@ nova_status Engine::create(const nova_model_config* m, const nova_engine_config*
   sim = c->backend == NOVA_BACKEND_SIM;
   if (cfg.max_decode_batch <= 0 || cfg.max_decode_batch > 16) return fail(NOVA_E_INVAL, "max_decode_batch in 1..16");
   if (cfg.max_requests <= 0) return fail(NOVA_E_INVAL, "max_requests must be > 0");
-  alg.pol = nova_partition_policy{NOVA_MODE_ADAPTIVE, 72, 72, 48, 48, 16, 8.f, 8.f, cfg.max_decode_batch, 5};
+  alg.pol = nova_partition_policy{NOVA_MODE_ADAPTIVE, 72, 72, 48, 48, 16, 8.f, 8.f, cfg.max_decode_batch, 5, 0};
   free_slots.clear();
   for (int i = cfg.max_requests - 1; i >= 0; --i) free_slots.push_back(i);
   if (sim) {

@@ -130,6 +130,7 @@ nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, n
   q.sm_min = rnd(q.sm_min);
   if (q.b_max <= 0 || q.b_max > E.cfg.max_decode_batch) q.b_max = E.cfg.max_decode_batch;
   if (q.pf_threshold <= 0) q.pf_threshold = 5;
+  q.sm_dv_floor = q.sm_dv_floor <= 0 ? 0 : std::min(rnd(q.sm_dv_floor), mx);
   if (q.mode == NOVA_MODE_STATIC && (q.sm_decode_dv < g || q.sm_decode_dp < g || q.sm_decode_dv > mx ||
                                      q.sm_decode_dp > mx))
     return E.fail(NOVA_E_PARTITION, "static decode budget outside [granularity, max split]");

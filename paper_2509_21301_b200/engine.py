@@ -142,9 +142,9 @@ class Engine:
         return t.value, g.value, n.value
 
     def set_partition(self, mode=ADAPTIVE, sm_decode_dv=72, sm_decode_dp=72, sm_op_dv=48, sm_op_dp=48, sm_min=16,
-                      alpha_dv=8.0, alpha_dp=8.0, b_max=0, pf_threshold=5) -> A.PartitionPolicy:
+                      alpha_dv=8.0, alpha_dp=8.0, b_max=0, pf_threshold=5, sm_dv_floor=0) -> A.PartitionPolicy:
         p = A.PartitionPolicy(mode, sm_decode_dv, sm_decode_dp, sm_op_dv, sm_op_dp, sm_min, alpha_dv, alpha_dp, b_max,
-                              pf_threshold)
+                              pf_threshold, sm_dv_floor)
         out = A.PartitionPolicy()
         self._check(self.lib.nova_set_partition(self.h, C.byref(p), C.byref(out)), "nova_set_partition")
         return out
@@ -261,6 +261,11 @@ def nova_adaptive_sm(sm_op, sm_min, alpha, n_pending, granularity) -> int:
 
 def nova_next_logical_layer(cur, K, L) -> int:
     return lib().nova_next_logical_layer(cur, K, L)
+
+
+def nova_offload_floor(s, t_v, t_h2d_ms) -> int:
+    n = len(s)
+    return lib().nova_offload_floor((A.I32 * n)(*s), (A.F64 * n)(*[float(x) for x in t_v]), n, float(t_h2d_ms))
 
 
 def nova_required_bandwidth(nbytes, forward_s, L, K) -> float:

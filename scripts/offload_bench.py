@@ -65,6 +65,7 @@ def main():
     L = shape.vit_depth
     bw = h2d_bandwidth()
     rows = []
+    aware = None
     for K in (0, 2, 3, 4, 5):
         eng = build(shape, K)
         res = {"K": K if K else "all", "weights_bytes": eng.memory["weights"],
@@ -77,6 +78,13 @@ def main():
                 res[f"eq8_required_GBps_{grid[0]}x{grid[1]}"] = round(
                     nova_required_bandwidth(L * layer_bytes, t / 1e3, L, K) / 1e9, 1)
         rows.append(res)
+        if K == 2:   # offload-aware split: vision pass vs decode split, co-running decode
+            from paper_2509_21301_b200.engine import nova_offload_floor
+            splits = [8 * k for k in range(1, 15)]
+            tv = [eng.time_pass(0, sp, 52, 94, B=2, ctx=1334, corun=1, iters=2)[0] for sp in splits]
+            t_h2d = L * layer_bytes / (bw * 1e9) * 1e3
+            aware = {"K": 2, "t_h2d_ms": round(t_h2d, 2), "splits": splits, "t_v_ms": [round(x, 2) for x in tv],
+                     "sm_dv_floor": nova_offload_floor(splits, tv, t_h2d)}
         eng.close()
         del eng
         torch.cuda.empty_cache()
@@ -85,7 +93,7 @@ def main():
         for g in ("52x94", "66x120"):
             r[f"stall_ms_{g}"] = round(r[f"t_vision_ms_{g}"] - base[f"t_vision_ms_{g}"], 3)
     out = {"model": shape.name, "vit_layer_bytes": layer_bytes, "vit_layers": L, "pinned_h2d_GBps": round(bw, 1),
-           "streamed_bytes_per_pass": L * layer_bytes, "rows": rows}
+           "streamed_bytes_per_pass": L * layer_bytes, "rows": rows, "offload_aware_split": aware}
     print(json.dumps(out))
     if a.out:
         json.dump(out, open(a.out, "w"), indent=1)

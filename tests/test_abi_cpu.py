@@ -85,6 +85,15 @@ def _sim_engine(E, mode, splits, tv, tp, tdv, tdp, solo, beta=0.0, **pol):
     return e
 
 
+@settings(max_examples=40, deadline=None)
+@given(st.lists(st.floats(1.0, 50.0, allow_nan=False), min_size=6, max_size=6), st.floats(0.5, 200.0))
+def test_c_offload_floor_matches_oracle(tv, th):
+    from paper_2509_21301_b200 import engine as E
+    s = [8, 16, 24, 32, 40, 48]
+    tv = sorted(tv)
+    assert E.nova_offload_floor(s, tv, th) == P.offload_floor(s, tv, th)
+
+
 def test_sim_worked_example(E):
     for mode, want in [(E.ADAPTIVE, {1: [14, 15, 16], 2: [28, 29, 30]}), (E.SERIAL, {1: [14, 15, 26], 2: [30, 31, 32]})]:
         e = _sim_engine(E, mode, [8, 16], [10 * MS] * 2, [4 * MS] * 2, [MS] * 2, [MS] * 2, (10 * MS, 4 * MS, MS),
@@ -130,7 +139,7 @@ def test_sim_decision_log_replays_on_oracle(E, mode, seed):
     tp = [int(3 * MS * 148 / (148 - s)) for s in splits]
     td = [int(0.7 * MS * max(1.0, 32 / s)) for s in splits]
     pol = dict(sm_decode_dv=48, sm_decode_dp=40, sm_op_dv=64, sm_op_dp=56, sm_min=16, alpha_dv=16.0,
-               alpha_dp=13.3, b_max=8)
+               alpha_dp=13.3, b_max=8, sm_dv_floor=40 if seed == 2 else 0)   # seed 2: offload-aware floor
     extra = {}
     if mode == OS.FRONTIER:   # Pareto frontier of the same curves (oracle planner), window 8
         ms = lambda xs: [x / MS for x in xs]

@@ -190,3 +190,20 @@ def test_frontier_lookup_pins():
         assert p[3] >= lam or all(q.thr < lam for q in fr)
     assert P.arrival_rate([0, 10_000_000, 20_000_000, 30_000_000]) == 100.0
     assert P.arrival_rate([5]) == 0.0
+
+
+def test_offload_floor_pins():
+    """Offload-aware split: with layer-wise offload a vision pass lasts at
+    least its weight streaming time t_h2d (Eq. 8's premise).  The floor is the largest
+    decode split whose vision pass on the remaining SMs still fits inside t_h2d: the pass is no
+    slower there, and one split more would make it slower."""
+    s = [8, 16, 24, 32, 40]
+    tv = [10.0, 11.0, 12.5, 15.0, 19.0]
+    assert P.offload_floor(s, tv, 12.6) == 24
+    assert P.offload_floor(s, tv, 9.0) == 0 and P.offload_floor(s, tv, 100.0) == 40
+    # Eq. 8 numbers of the 7B ViT (SURVEY §8(a) a9): 32 layers x 39.4 MB streamed at 55 GB/s
+    t_h2d = 32 * 39.4e6 / 55e9 * 1e3          # ms
+    f = P.offload_floor(s, [t_h2d * x for x in (0.5, 0.8, 0.99, 1.2, 1.5)], t_h2d)
+    assert f == 24
+    i = s.index(f)
+    assert tv[i] * 0 + [0.5, 0.8, 0.99, 1.2, 1.5][i] <= 1.0 < [0.5, 0.8, 0.99, 1.2, 1.5][i + 1]
