@@ -271,10 +271,10 @@ nova_status nova_plan(const nova_curves* c, double gen_len, double tau, nova_pla
 nova_status nova_set_frontier(nova_engine* e, const nova_plan_point* pts, int32_t n, int32_t window);
 /* Offload-aware split (Eq. 8): with layer-wise ViT
  * offload a vision pass cannot finish before its weights stream in (t_h2d_ms), so front SMs
- * beyond those that meet t_h2d are idle.  Returns the largest decode split s[i] whose vision
- * time on the complementary partition t_v[i] is still <= t_h2d_ms (those SMs cost the
- * vision pass nothing), or 0 if no split qualifies.  s ascending, t_v[i] the vision pass with
- * decode on s[i] SMs. */
+ * beyond those that meet t_h2d are idle.  Returns the largest decode split s[i] whose co-run
+ * vision time t_v[i] is within 2% of max(t_h2d_ms, min_i t_v[i]) -- those SMs cost the vision
+ * pass nothing -- or 0 if n == 0.  s ascending, t_v[i] the vision pass with decode on s[i] SMs
+ * (measured with the offload ring active, so t_v already includes any PCIe stall). */
 int32_t nova_offload_floor(const int32_t* s, const double* t_v, int32_t n, double t_h2d_ms);
 /* Eq. 5: max(SM_min, floor_g(SM_op - alpha (max(N_pend, 1) - 1))). */
 int32_t nova_adaptive_sm(int32_t sm_op, int32_t sm_min, double alpha, int32_t n_pending, int32_t granularity);

@@ -118,9 +118,12 @@ def frontier_pick(frontier, lam: float):
 def offload_floor(s, t_v, t_h2d_ms) -> int:
     """SURVEY.md §8(f) f3 with PAPER.md Eq. 8: under layer-wise offload a vision pass
     lasts at least the weight streaming time t_h2d; decode may take every split whose vision
-    time on the remaining SMs still fits in it.  Largest such s, else 0."""
-    ok = [si for si, tv in zip(s, t_v) if tv <= t_h2d_ms]
-    return max(ok) if ok else 0
+    time on the remaining SMs is no slower than that bound (or than the best measured split),
+    within 2% (R24).  Largest such s."""
+    if not s:
+        return 0
+    bound = max(t_h2d_ms, min(t_v)) * 1.02
+    return max(si for si, tv in zip(s, t_v) if tv <= bound)
 
 
 def arrival_rate(times_ns) -> float:

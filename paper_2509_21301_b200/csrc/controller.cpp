@@ -191,10 +191,13 @@ int32_t nova_adaptive_sm(int32_t sm_op, int32_t sm_min, double alpha, int32_t n_
 int32_t nova_next_logical_layer(int32_t cur, int32_t K, int32_t L) { return (cur + K) % L; }
 
 int32_t nova_offload_floor(const int32_t* s, const double* t_v, int32_t n, double t_h2d_ms) {
+  if (!s || !t_v || n <= 0) return 0;
+  double tmin = t_v[0];
+  for (int i = 1; i < n; ++i) tmin = std::min(tmin, t_v[i]);
+  const double bound = std::max(t_h2d_ms, tmin) * 1.02;  // "no slower" within 2% (measurement noise)
   int32_t best = 0;
-  if (!s || !t_v) return 0;
   for (int i = 0; i < n; ++i)
-    if (t_v[i] <= t_h2d_ms) best = std::max(best, s[i]);
+    if (t_v[i] <= bound) best = std::max(best, s[i]);
   return best;
 }
 

@@ -199,11 +199,15 @@ def test_offload_floor_pins():
     slower there, and one split more would make it slower."""
     s = [8, 16, 24, 32, 40]
     tv = [10.0, 11.0, 12.5, 15.0, 19.0]
-    assert P.offload_floor(s, tv, 12.6) == 24
-    assert P.offload_floor(s, tv, 9.0) == 0 and P.offload_floor(s, tv, 100.0) == 40
+    assert P.offload_floor(s, tv, 12.6) == 24                 # 12.5 <= 12.6 * 1.02 < 15
+    assert P.offload_floor(s, tv, 9.0) == 8                   # compute-bound: only the best split
+    assert P.offload_floor(s, tv, 100.0) == 40
     # Eq. 8 numbers of the 7B ViT (SURVEY §8(a) a9): 32 layers x 39.4 MB streamed at 55 GB/s
     t_h2d = 32 * 39.4e6 / 55e9 * 1e3          # ms
     f = P.offload_floor(s, [t_h2d * x for x in (0.5, 0.8, 0.99, 1.2, 1.5)], t_h2d)
     assert f == 24
     i = s.index(f)
-    assert tv[i] * 0 + [0.5, 0.8, 0.99, 1.2, 1.5][i] <= 1.0 < [0.5, 0.8, 0.99, 1.2, 1.5][i + 1]
+    assert [0.5, 0.8, 0.99, 1.2, 1.5][i] <= 1.02 < [0.5, 0.8, 0.99, 1.2, 1.5][i + 1]
+    # the measured B200 curve (profiles/r01_s3_offload.json, K = 2): flat at the PCIe bound to 56
+    meas = [22.51, 22.63, 22.65, 22.71, 22.85, 22.87, 22.95, 24.15, 25.55, 30.65]
+    assert P.offload_floor([8 * k for k in range(1, 11)], meas, 22.7) == 56
