@@ -17,12 +17,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def build(shape, K, device=0):
+def build(shape, K, device=0, serving=True):
     from synth.models import weight_specs
     from synth.weights import device_tensor
     from paper_2509_21301_b200 import engine as E
-    opts = E.EngineOptions(device=device, max_requests=4, max_decode_batch=4, kv_pages=256, max_patches=7920,
-                           max_prompt=128, max_gen=64, vit_resident_layers=K)
+    if serving:   # the bench's serving limits (scripts/policy_sweep.py --offload)
+        opts = E.EngineOptions(device=device, max_requests=64, max_decode_batch=16, kv_pages=2600, max_patches=7920,
+                               max_prompt=128, max_gen=64, vit_resident_layers=K, use_green_ctx=1)
+    else:
+        opts = E.EngineOptions(device=device, max_requests=4, max_decode_batch=4, kv_pages=256, max_patches=7920,
+                               max_prompt=128, max_gen=64, vit_resident_layers=K)
     eng = E.Engine(shape, opts)
     for name, shp, init in weight_specs(shape):
         if K > 0 and name.startswith("model.visual.blocks."):
@@ -67,7 +71,7 @@ def main():
     rows = []
     aware = None
     for K in (0, 2, 3, 4, 5):
-        eng = build(shape, K)
+        eng = build(shape, K, serving=False)
         res = {"K": K if K else "all", "weights_bytes": eng.memory["weights"],
                "vit_resident_bytes": (K if K else L) * layer_bytes}
         for grid in ((52, 94), (66, 120)):

@@ -24,11 +24,19 @@ def main():
     ap.add_argument("--requests", type=int, default=48)
     ap.add_argument("--sm-min", type=int, nargs="*", default=[])
     ap.add_argument("--sm-op", type=int, nargs="*", default=[], help="adaptive SM_op values (both contexts)")
+    ap.add_argument("--offload", type=int, default=0, help="K resident ViT layer slots (0 = all resident)")
+    ap.add_argument("--floor", type=int, nargs="*", default=[], help="adaptive + offload-aware sm_dv_floor values")
+    ap.add_argument("--policies", default="serial,multi_stream", help="baselines to include")
     a = ap.parse_args()
     import torch
     from synth import Q7B
     from paper_2509_21301_b200 import engine as E
-    eng = BN.build_engine(Q7B, 0)
+    if a.offload:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from offload_bench import build as build_offload
+        eng = build_offload(Q7B, a.offload)
+    else:
+        eng = BN.build_engine(Q7B, 0)
     curves, plan = BN.profile_and_plan(eng, False, lambda *x: print(*x, file=sys.stderr, flush=True))
     sv, sp = plan["best"][0], plan["best"][1]
     print(json.dumps({"plan": {"best": plan["best"][:2], "sm_min": plan["sm_min"]},
@@ -41,12 +49,17 @@ def main():
         smin = min(plan["sm_min"], op)
         pols.append((f"adaptive_op{op}", dict(mode=E.ADAPTIVE, sm_op_dv=op, sm_op_dp=op, sm_min=smin,
                                               alpha_dv=(op - smin) / 3.0, alpha_dp=(op - smin) / 3.0, b_max=16)))
+    for fl in a.floor:
+        pols.append((f"adaptive_floor{fl}", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=plan["sm_min"],
+                                                 alpha_dv=plan["alpha_dv"], alpha_dp=plan["alpha_dp"], b_max=16,
+                                                 sm_dv_floor=fl)))
     for smin in a.sm_min:
         if smin > min(sv, sp):
             continue
         pols.append((f"adaptive_smin{smin}", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=smin,
                                                   alpha_dv=(sv - smin) / 3.0, alpha_dp=(sp - smin) / 3.0, b_max=16)))
-    pols += [("serial", dict(mode=E.SERIAL, b_max=16)), ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16))]
+    base = {"serial": dict(mode=E.SERIAL, b_max=16), "multi_stream": dict(mode=E.MULTI_STREAM, b_max=16)}
+    pols += [(n, base[n]) for n in a.policies.split(",") if n in base]
     for rho in a.rho:
         trs = [BN.make_trace(Q7B, a.requests, rho, t_front, 61 + k) for k in range(a.seeds)]
         for name, pol in pols:
