@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launch_dec16.csv python scripts/pass_profile.py --stage dec --B 16 --profile > /dev/null 2>&1
+python scripts/ncu_summary.py --launches gpurun_out/launch_dec16.csv --out gpurun_out/launch_dec16.json > /dev/null
+python -c "
+import json; d=json.load(open('gpurun_out/launch_dec16.json'))['launches']
+print('total', sum(x['total_us'] for x in d))
+for x in d: print(x)"
