@@ -41,11 +41,17 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="nova", choices=["nova", "reference"])
-    p.add_argument("--model", default="7b", choices=["7b", "2b"])
+    p.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"],
+                   help="cfg2 = BASELINE configs[1] (2B, steady Poisson stream, static split sweep vs serial; "
+                        "the default, as the metric is quoted on configs[1]); cfg3 = configs[2] (7B, bursty "
+                        "MMPP-2 GUI-agent trace)")
+    p.add_argument("--model", default=None, choices=["7b", "2b"], help="override the workload's model")
+    p.add_argument("--no-solo-7b", action="store_true", help="cfg2: skip the 7B (cfg 3 shape) solo stage passes")
     p.add_argument("--rho", type=float, default=0.7)
     p.add_argument("--requests", type=int, default=48, help="requests per step (per GPU)")
     p.add_argument("--no-compare", action="store_true", help="skip the serial / static-50/50 comparison replays")
-    p.add_argument("--compare-rho", type=float, nargs="*", default=[0.5, 0.7], help="offered loads of the comparison")
+    p.add_argument("--compare-rho", type=float, nargs="*", default=None,
+                   help="offered loads of the comparison (default cfg2: 0.7 0.9, cfg3: 0.5 0.7)")
     p.add_argument("--compare-seeds", type=int, default=3, help="traces per offered load in the comparison")
     p.add_argument("--quick", action="store_true", help="smaller profile sweep (debug)")
     p.add_argument("--skip-profile", action="store_true", help="no co-run curve sweep (ncu launch-list runs)")
@@ -157,9 +163,38 @@ def profile_and_plan(eng, quick=False, log=print):
     return curves, plan
 
 
-def make_trace(shape, n, rho, t_front_s, seed):
-    from synth.inputs import mmpp2_trace
+def make_trace(shape, n, rho, t_front_s, seed, kind="mmpp"):
+    """cfg 3: MMPP-2 bursty GUI-agent mix at rho = lambda x T_front; cfg 2: Poisson arrivals at
+    lambda = rho / T_front with fixed 52x94 screenshots, prompt 64, gen_len 48 (SURVEY.md §8(d) d1')."""
+    from synth.inputs import mmpp2_trace, poisson_trace
+    if kind == "poisson":
+        return poisson_trace(n, rho / t_front_s, seed)
     return mmpp2_trace(n, rho, t_front_s, seed)
+
+
+def solo_stage_fracs(shape, tv_ms, tp_ms, td_ms, td_hot_ms, hbm, tfl, B_ref=2, ctx=1334):
+    """Solo stage passes on the full GPU against the measured peaks: algorithmic FLOPs / bytes of
+    SURVEY.md §8(d) d2 (N = 4888 patches, S = 1222 + 64 tokens, decode B_ref at ctx) over the time."""
+    D, F, V = shape.llm_dim, shape.llm_ffn, shape.vocab
+    N = 52 * 94
+    fl_v = 32 * (2 * N * (1280 * 3840 + 1280 ** 2 + 2 * 1280 * 5120) + 4 * N * N * 1280) + \
+        2 * N * 1176 * 1280 + 2 * (N // 4) * (5120 ** 2 + 5120 * D)
+    S, H, KV, hd = 1222 + 64, shape.llm_heads, shape.llm_kv_heads, shape.head_dim
+    fl_p = shape.llm_layers * (2 * S * (D * (D + 2 * KV * hd) + D * D + 3 * D * F) + 2 * S * S * H * hd) + 2 * D * V
+    out = {}
+    for name, fl, ms in (("vision_encode_N4888", fl_v, tv_ms), ("prefill_S1286", fl_p, tp_ms)):
+        if ms:
+            ach = fl / (ms / 1e3) / 1e12
+            out[name] = {"ms": round(ms, 3), "achieved": round(ach, 1), "unit": "TFLOP/s", "peak": tfl,
+                         "frac": round(ach / tfl, 4), "bound": "tensor"}
+    Wb = shape.llm_layers * 2 * (D * (D + 2 * KV * hd) + D * D + 3 * D * F) + 2 * D * V   # bf16 bytes
+    kvb = B_ref * (ctx + 1) * shape.llm_layers * 2 * KV * hd * 2
+    for tag, ms in (("", td_ms), ("_after_front_passes", td_hot_ms)):
+        if ms:
+            ach = (Wb + kvb) / (ms / 1e3) / 1e9
+            out[f"decode_B{B_ref}_ctx{ctx}{tag}"] = {"ms": round(ms, 3), "achieved": round(ach, 1), "unit": "GB/s",
+                                                     "peak": hbm, "frac": round(ach / hbm, 4), "bound": "hbm"}
+    return out
 
 
 def make_inputs(shape, rows, seed, device, resident):
@@ -346,7 +381,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     from synth import Q7B, Q2B
-    shape = Q7B if args.model == "7b" else Q2B
+    model = args.model or ("2b" if args.workload == "cfg2" else "7b")
+    shape = Q7B if model == "7b" else Q2B
     for _ in range(args.warmup):
         cpu_oracle_sample(shape)
     vals = []
@@ -362,7 +398,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el * 1000 / args.steps, 1),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": "cfg3 7B bursty GUI-agent trace (single-request latency, CPU)",
+            "data": "synthetic", "config": {"workload": ("BASELINE configs[1]: 2B-shaped, Poisson stream (single-request "
+                                                         "latency of the CPU oracle)" if args.workload == "cfg2" else
+                                                         "BASELINE configs[2]: 7B-shaped bursty GUI-agent trace "
+                                                         "(single-request latency of the CPU oracle)"),
                                             "model": shape.name},
             "cpu_baseline": {"value": round(value, 1), "unit": "ms", "cores": cores, "kind": "oracle",
                              "sample": sample},
@@ -396,7 +435,10 @@ def main():
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
     from synth import Q7B, Q2B
     from paper_2509_21301_b200 import engine as E
-    shape = Q7B if args.model == "7b" else Q2B
+    model = args.model or ("2b" if args.workload == "cfg2" else "7b")
+    shape = Q7B if model == "7b" else Q2B
+    kind = "poisson" if args.workload == "cfg2" else "mmpp"
+    compare_rho = args.compare_rho if args.compare_rho is not None else ([0.7, 0.9] if kind == "poisson" else [0.5, 0.7])
     pk = peaks()
     t_setup = time.time()
     eng = build_engine(shape, local)
@@ -414,10 +456,14 @@ def main():
     policy = dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=plan["sm_min"], alpha_dv=plan["alpha_dv"],
                   alpha_dp=plan["alpha_dp"], b_max=16)
     eng.set_partition(**policy)
-    # T_front: request-mix mean of solo t_v + t_p (half 4888-patch, half 7920-patch screenshots)
-    t_front = (0.5 * (curves["t_v_solo_ms"] + curves["t_v_solo_7920_ms"]) + curves["t_p_solo_ms"]) / 1000.0
+    # T_front: request-mix mean of solo t_v + t_p (cfg 3: half 4888-patch, half 7920-patch screenshots;
+    # cfg 2: 4888-patch screenshots, prompt 64)
+    if kind == "poisson":
+        t_front = (curves["t_v_solo_ms"] + curves["t_p_solo_ms"]) / 1000.0
+    else:
+        t_front = (0.5 * (curves["t_v_solo_ms"] + curves["t_v_solo_7920_ms"]) + curves["t_p_solo_ms"]) / 1000.0
     # global trace (identical on every rank): world x requests at world x the per-GPU load (weak scaling)
-    traces = [make_trace(shape, args.requests * world, args.rho * world, t_front, 31 + i)
+    traces = [make_trace(shape, args.requests * world, args.rho * world, t_front, 31 + i, kind)
               for i in range(args.warmup + 2 * args.steps + 2)]
     counter = [0]
 
@@ -507,8 +553,11 @@ def main():
                 ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16))]
         if plan.get("points"):   # Pareto point for the estimated arrival rate
             pols.append(("frontier", dict(mode=E.FRONTIER, b_max=16)))
-        for rho in args.compare_rho:
-            trs = [make_trace(shape, args.requests, rho, t_front, 61 + k) for k in range(args.compare_seeds)]
+        if kind == "poisson":    # cfg 2: the static SM-split sweep
+            pols += [(f"static_{s_}", dict(mode=E.STATIC, sm_decode_dv=s_, sm_decode_dp=s_, b_max=16))
+                     for s_ in (24, 48, 96)]
+        for rho in compare_rho:
+            trs = [make_trace(shape, args.requests, rho, t_front, 61 + k, kind) for k in range(args.compare_seeds)]
             runs = {name: [] for name, _ in pols}
             for k, tr in enumerate(trs):
                 for name, pol in pols:
@@ -583,40 +632,28 @@ def main():
     stages = {k: v for k, v in kernels.items() if k.endswith("_pass")}
     # Solo stage passes on the full GPU (the §8(d) bars apply here), timed with CUDA events in this
     # run by the curve profiler: algorithmic FLOPs / bytes of SURVEY.md §8(d) d2 over the pass time
-    stages_solo = {}
-    if curves.get("t_v_solo_ms") and curves.get("t_p_solo_ms"):
-        D, F, V = shape.llm_dim, shape.llm_ffn, shape.vocab
-        N = 52 * 94
-        fl_v = 32 * (2 * N * (1280 * 3840 + 1280 ** 2 + 2 * 1280 * 5120) + 4 * N * N * 1280) + \
-            2 * N * 1176 * 1280 + 2 * (N // 4) * (5120 ** 2 + 5120 * D)
-        S, H, KV, hd = 1222 + 64, shape.llm_heads, shape.llm_kv_heads, shape.head_dim
-        fl_p = shape.llm_layers * (2 * S * (D * (D + 2 * KV * hd) + D * D + 3 * D * F) + 2 * S * S * H * hd) + 2 * D * V
-        for name, fl, ms in (("vision_encode_N4888", fl_v, curves["t_v_solo_ms"]),
-                             ("prefill_S1286", fl_p, curves["t_p_solo_ms"])):
-            ach = fl / (ms / 1e3) / 1e12
-            stages_solo[name] = {"ms": round(ms, 3), "achieved": round(ach, 1), "unit": "TFLOP/s",
-                                 "peak": tfl, "frac": round(ach / tfl, 4), "bound": "tensor"}
-        Wb = shape.llm_layers * 2 * (D * (D + 2 * KV * hd) + D * D + 3 * D * F) + 2 * D * V
-        for key, tag in (("t_d_full_ms", ""), ("t_d_full_after_front_ms", "_after_front_passes")):
-            if curves.get(key):
-                kvb = curves["B_ref"] * (curves["ctx_ref"] + 1) * shape.llm_layers * 2 * KV * hd * 2
-                ach = (Wb + kvb) / (curves[key] / 1e3) / 1e9
-                stages_solo[f"decode_B{curves['B_ref']}_ctx{curves['ctx_ref']}{tag}"] = {
-                    "ms": round(curves[key], 3), "achieved": round(ach, 1), "unit": "GB/s", "peak": hbm,
-                    "frac": round(ach / hbm, 4), "bound": "hbm"}
+    stages_solo = solo_stage_fracs(shape, curves.get("t_v_solo_ms"), curves.get("t_p_solo_ms"),
+                                   curves.get("t_d_full_ms"), curves.get("t_d_full_after_front_ms"), hbm, tfl,
+                                   curves.get("B_ref", 2), curves.get("ctx_ref", 1334)) if curves.get("t_v_solo_ms") else {}
 
     line = {"metric": METRIC, "value": round(mx, 2), "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 1), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, "
-            "seeded screenshots/prompts, MMPP-2 bursty arrivals)",
+            "seeded screenshots/prompts, " + ("Poisson arrivals)" if kind == "poisson" else "MMPP-2 bursty arrivals)"),
             "p99_ms": round(p99, 2), "req_per_s": round(n_all / wall, 3),
-            "config": {"workload": "BASELINE configs[2]: Qwen2-VL-7B-shaped random init, bursty synthetic "
-                                   "GUI-agent trace, adaptive Pareto repartitioning",
+            "config": {"workload": ("BASELINE configs[1]: Qwen2-VL-2B-shaped random init, steady Poisson request "
+                                    "stream, static SM-split sweep vs serial execution" if kind == "poisson" else
+                                    "BASELINE configs[2]: Qwen2-VL-7B-shaped random init, bursty synthetic "
+                                    "GUI-agent trace, adaptive Pareto repartitioning"),
                        "model": shape.name, "requests_per_step_per_gpu": args.requests, "rho": args.rho,
-                       "t_front_ms": round(t_front * 1000, 2), "images": "50% 52x94 (4888 patches) / 50% 66x120 "
-                       "(7920 patches)", "prompt": "U{32..128}", "gen_len": "U{32..64}",
+                       "t_front_ms": round(t_front * 1000, 2),
+                       "images": ("52x94 (4888 patches)" if kind == "poisson" else
+                                  "50% 52x94 (4888 patches) / 50% 66x120 (7920 patches)"),
+                       "prompt": "64" if kind == "poisson" else "U{32..128}",
+                       "gen_len": "48" if kind == "poisson" else "U{32..64}",
                        "policy": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in policy.items()},
-                       "l2": "weights 16.5 GB >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world} ({args.dispatch} dispatcher)"},
+                       "l2": f"weights {eng.memory['weights'] / 1e9:.1f} GB streamed per pass >> 126 MB L2 "
+                             "(no flush needed)", "parallelism": f"replicas x{world} ({args.dispatch} dispatcher)"},
             "e2e": {"value": round(mx_e, 2), "unit": "ms", "p99_ms": round(p99_e, 2),
                     "req_per_s": round(n_all_e / wall_e, 3), "h2d_bytes_per_step": int(Ae["h2d"]),
                     "d2h_bytes_per_step": int(Ae["d2h"])},
@@ -628,6 +665,22 @@ def main():
                      "sm_min": plan["sm_min"], "alpha_dv": round(plan["alpha_dv"], 3),
                      "alpha_dp": round(plan["alpha_dp"], 3)},
             "compare": compare, "mg1": mg1, "clocks": clk}
+    if kind == "poisson" and not args.no_solo_7b and world == 1:
+        # the §8(d) stage bars are stated at the cfg 3 (7B) shapes: time those solo passes too
+        try:
+            eng.close()
+            eng = None
+            eng7 = build_engine(Q7B, local)
+            eng7.time_pass(2, 0, B=2, ctx=1334, iters=3)
+            td7 = eng7.time_pass(2, 0, B=2, ctx=1334, iters=10)[0]
+            eng7.time_pass(0, 0, 52, 94, iters=1)
+            tv7 = eng7.time_pass(0, 0, 52, 94, iters=2)[0]
+            tp7 = eng7.time_pass(1, 0, 52, 94, 64, iters=2)[0]
+            td7h = eng7.time_pass(2, 0, B=2, ctx=1334, iters=10)[0]
+            line["stages_solo_cfg3_7b"] = solo_stage_fracs(Q7B, tv7, tp7, td7, td7h, hbm, tfl)
+            eng7.close()
+        except Exception as ex:  # pragma: no cover
+            line["stages_solo_cfg3_7b"] = {"error": str(ex)}
     if rank == 0 and world == 1:
         try:
             v, med, cores = cpu_oracle_sample(shape)
@@ -641,7 +694,8 @@ def main():
         print(json.dumps(line), flush=True)
         if args.out:
             open(args.out, "w").write(json.dumps(line) + "\n")
-    eng.close()
+    if eng is not None:
+        eng.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
