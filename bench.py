@@ -48,7 +48,8 @@ def parse():
     p.add_argument("--model", default=None, choices=["7b", "2b"], help="override the workload's model")
     p.add_argument("--no-solo-7b", action="store_true", help="cfg2: skip the 7B (cfg 3 shape) solo stage passes")
     p.add_argument("--rho", type=float, default=0.7)
-    p.add_argument("--requests", type=int, default=48, help="requests per step (per GPU)")
+    p.add_argument("--requests", type=int, default=None,
+                   help="requests per step (per GPU); default cfg2: 96 (~2.4 s of Poisson arrivals), cfg3: 48")
     p.add_argument("--no-compare", action="store_true", help="skip the serial / static-50/50 comparison replays")
     p.add_argument("--compare-rho", type=float, nargs="*", default=None,
                    help="offered loads of the comparison (default cfg2: 0.7 0.9, cfg3: 0.5 0.7)")
@@ -438,6 +439,8 @@ def main():
     model = args.model or ("2b" if args.workload == "cfg2" else "7b")
     shape = Q7B if model == "7b" else Q2B
     kind = "poisson" if args.workload == "cfg2" else "mmpp"
+    if args.requests is None:
+        args.requests = 96 if kind == "poisson" else 48
     compare_rho = args.compare_rho if args.compare_rho is not None else ([0.7, 0.9] if kind == "poisson" else [0.5, 0.7])
     pk = peaks()
     t_setup = time.time()
