@@ -621,7 +621,7 @@ def main():
     traffic = None
     try:
         nc = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = nc.get(dom)
+        traffic = nc.get(shape.name, {}).get(dom)   # per model (profiles/ncu_traffic.json)
     except Exception:
         pass
     roof = None

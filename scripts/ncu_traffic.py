@@ -3,7 +3,8 @@ decode pass (and optionally one ViT pass):
 
   ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \\
       --csv --log-file gpurun_out/traffic_dec.csv python scripts/pass_profile.py --stage dec --profile
-  python scripts/ncu_traffic.py gpurun_out/traffic_dec.csv [gpurun_out/traffic_vit.csv] --out profiles/ncu_traffic.json
+  python scripts/ncu_traffic.py gpurun_out/traffic_dec.csv [gpurun_out/traffic_vit.csv] --out profiles/ncu_traffic.json \
+      [--model qwen2vl-2b]   (entries are kept per model name)
 
 Writes {class: mean (read + write) bytes per launch} for the classes bench.py reports
 (dec_gemv = decode linears except lm_head; lm_head; dec_attn; vit_gemm; vit_attn).
@@ -31,7 +32,8 @@ def classify(name, stage):
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else "profiles/ncu_traffic.json"
-    args = [a for a in args if a != out]
+    model = sys.argv[sys.argv.index("--model") + 1] if "--model" in sys.argv else "qwen2vl-7b"
+    args = [a for a in args if a not in (out, model)]
     per = defaultdict(lambda: defaultdict(float))   # (launch id) -> metric
     names = {}
     res = defaultdict(list)
@@ -58,8 +60,15 @@ def main():
     summary["_launches"] = {k: len(v) for k, v in res.items()}
     summary["_how"] = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over one solo pass "
                        "(scripts/pass_profile.py --profile); mean bytes per launch per class")
-    json.dump(summary, open(out, "w"), indent=1)
-    print(json.dumps(summary))
+    try:
+        allm = json.load(open(out))
+        if "dec_gemv" in allm:          # older flat file: the 7B numbers
+            allm = {"qwen2vl-7b": allm}
+    except Exception:
+        allm = {}
+    allm[model] = summary
+    json.dump(allm, open(out, "w"), indent=1)
+    print(json.dumps(allm))
 
 
 if __name__ == "__main__":
