@@ -74,7 +74,7 @@ struct PGemvArgs {
 };
 
 template <int RB, int NT, int EPI, int XHL>
-__global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel(const __grid_constant__ CUtensorMap tmW,
+__global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC), 4) gemv_tma_kernel(const __grid_constant__ CUtensorMap tmW,
                                                                           const __grid_constant__ CUtensorMap tmX,
                                                                           const __grid_constant__ CUtensorMap tmX2,
                                                                           PGemvArgs a) {
@@ -94,11 +94,32 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int kblocks = a.K / KC;
-  // k blocks of unit u (the last K split may be shorter) and its ring stages
-  auto unit_kb = [&](int u) {
-    const int p = u % a.P;
+  // k blocks of K split p (the last split may be shorter) and its ring stages
+  auto unit_kb = [&](int p) {
     const int k0 = p * a.ks, k1 = min(a.K, k0 + a.ks);
     return (k1 - k0 + KC - 1) / KC;
+  };
+  // The unit sequence of this CTA (the producer and the consumers walk the same one).  With
+  // split-K (P > 1) and at least G row blocks, the first R = blocks / G rounds give each CTA WHOLE
+  // row blocks: it streams the P splits of a block back to back and adds their partials in
+  // split order in registers (0 + s_0 + s_1 + ... -- the same fp32 operations as the workspace
+  // reduction, so the result is bitwise the same for any grid) with no workspace round trip,
+  // ticket or stall between units; the remaining blocks go out as split units as before.
+  const int blocks = a.units / a.P;
+  const int R = a.P > 1 ? blocks / G : 0;
+  auto unit_at = [&](int i, int& blk, int& p, bool& local) -> bool {
+    if (i < R * a.P) {
+      blk = (i / a.P) * G + blockIdx.x;
+      p = i % a.P;
+      local = true;
+      return true;
+    }
+    const int u = blockIdx.x + (i - R * a.P) * G;
+    if (u >= (blocks - R * G) * a.P) return false;
+    blk = R * G + u / a.P;
+    p = u % a.P;
+    local = false;
+    return true;
   };
   // one ring stage: n k blocks starting at k (global), row block blk
   auto load_stage = [&](int st, int k, int n, int blk, bool with_w, bool with_x) {
@@ -141,9 +162,11 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel
   if (warp == 0) {
     if (lane == 0) {  // ---------------- producer: one continuous ring over all units of this CTA
       // pass 1 (before griddepcontrol.wait): weights of the first STAGES ring slots
-      int u = blockIdx.x, kb = 0, nkb = u < a.units ? unit_kb(u) : 0, i = 0;
-      while (u < a.units && i < STAGES) {
-        const int blk = u / a.P, p = u % a.P;
+      int ui = 0, blk = 0, p = 0, kb = 0, i = 0;
+      bool loc;
+      bool have = unit_at(ui, blk, p, loc);
+      int nkb = have ? unit_kb(p) : 0;
+      while (have && i < STAGES) {
         const int n = min(SKB, nkb - kb);
         mbar_arrive_expect_tx(&full[i], n * (C::KB_W + C::XT * X_BYTES));
         load_stage(i, p * a.ks + kb * KC, n, blk, true, false);
@@ -151,18 +174,18 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel
         kb += n;
         if (kb == nkb) {
           kb = 0;
-          u += G;
-          nkb = u < a.units ? unit_kb(u) : 0;
+          have = unit_at(++ui, blk, p, loc);
+          nkb = have ? unit_kb(p) : 0;
         }
       }
       pdl_launch_dependents();
       pdl_wait();  // x is written by the previous kernel
       // pass 2: x of those slots, then the steady-state ring
-      u = blockIdx.x;
+      ui = 0;
       kb = 0;
-      nkb = u < a.units ? unit_kb(u) : 0;
-      for (int j = 0; u < a.units; ++j) {
-        const int blk = u / a.P, p = u % a.P;
+      have = unit_at(ui, blk, p, loc);
+      nkb = have ? unit_kb(p) : 0;
+      for (int j = 0; have; ++j) {
         const int st = j % STAGES;
         const int n = min(SKB, nkb - kb);
         const int k = p * a.ks + kb * KC;
@@ -176,8 +199,8 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel
         kb += n;
         if (kb == nkb) {
           kb = 0;
-          u += G;
-          nkb = u < a.units ? unit_kb(u) : 0;
+          have = unit_at(++ui, blk, p, loc);
+          nkb = have ? unit_kb(p) : 0;
         }
       }
     }
@@ -189,10 +212,12 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel
   const int t = (warp - 1) % NW, h = NWC > NW ? (warp - 1) / NW : 0;
   const int g = lane >> 2, c = lane & 3;
   int j = 0;  // ring position
-  for (int u = blockIdx.x; u < a.units; u += G) {
-    const int blk = u / a.P, p = u % a.P;
+  float sum[NT][4];  // whole-block split sum (local units)
+  int blk, p;
+  bool local;
+  for (int ui = 0; unit_at(ui, blk, p, local); ++ui) {
     const int r0 = blk * RB;
-    const int nkb = unit_kb(u);
+    const int nkb = unit_kb(p);
     float acc[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
@@ -242,7 +267,17 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC)) gemv_tma_kernel
     if (h == 1) continue;
     }
     // acc[nt]: c0:(row g, batch 2c) c1:(g, 2c+1) c2:(g+8, 2c) c3:(g+8, 2c+1)
-    if (a.P > 1) {  // split-K: partials, then the last CTA of the row block reduces in split order
+    if (local) {  // split partials summed in split order in registers (== the workspace reduction)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) sum[nt][jj] = (p == 0 ? 0.f : sum[nt][jj]) + acc[nt][jj];
+      if (p < a.P - 1) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[nt][jj] = sum[nt][jj];
+    } else if (a.P > 1) {  // split-K: partials, then the last CTA of the row block reduces in split order
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
