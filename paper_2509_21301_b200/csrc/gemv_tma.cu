@@ -473,14 +473,17 @@ cudaError_t launch_nt(const CUtensorMap& mw, const CUtensorMap& mx, const CUtens
 
 // Shape-only work decomposition: row block RB (128 for the RoPE epilogue, else 64) and the K
 // split P that makes units / 592 (4 CTAs x 148 SMs) closest to a whole number of waves (chunks
-// >= 256 k, P <= 16).
+// >= 256 k, P <= 8).
 GemvTmaPlan gemv_tma_plan(int N, int K, int epi) {
   GemvTmaPlan pl;
   pl.RB = epi == EPI_QKV_ROPE_KV ? 128 : 64;
   const int blocks = N / pl.RB;
   int bestP = 1;
   double best = 1e30;
-  const int maxP = epi == EPI_F32_ARGMAX ? 1 : 16;
+  // P <= 8: decode iterations on 8..112-SM slices 6-11% (2B) / 0-4% (7B) faster than P <= 16 at equal
+  // full-GPU time (scripts/gpu_maxp.sh); env NOVA_GEMV_MAXP is the sweep knob
+  static const int env_maxp = getenv("NOVA_GEMV_MAXP") ? atoi(getenv("NOVA_GEMV_MAXP")) : 8;
+  const int maxP = epi == EPI_F32_ARGMAX ? 1 : env_maxp;
   for (int P = 1; P <= maxP; ++P) {
     const int ks = ((K + P - 1) / P + KC - 1) / KC * KC;
     const int Pe = (K + ks - 1) / ks;
