@@ -367,18 +367,21 @@ __global__ void __launch_bounds__(DCHUNK) decode_attn_partial(const bf16* __rest
 }
 
 // Tensor-core decode attention, one launch, merged through a thread-block cluster (DSMEM).
-// Cluster = DA_CL CTAs per (request, KV head); CTA = DA_W warps; the context is cut into 32-key
-// blocks and warp w of cluster rank r owns blocks (r*DA_W + w), (r*DA_W + w) + DA_W*DA_CL, ...  A warp
+// Cluster = CL = da_cluster(KV) CTAs per (request, KV head); CTA = DA_W warps; the context is cut into 32-key
+// blocks and warp w of cluster rank r owns blocks (r*DA_W + w), (r*DA_W + w) + DA_W*CL, ...  A warp
 // streams its blocks through a 2-stage cp.async ring in its own smem slice (pages gathered
 // through the block table), and keeps an online softmax over them: S = Q K^T with the G query
 // heads sharing the KV head as the M side of mma.sync m16n8k16 (padded to 16 rows), keys the
 // N side; O += P V.  The DA_W warp states are merged in smem in warp order, then rank 0 reads the
-// DA_CL CTA states from the peers' shared memory (mapa + ld.shared::cluster) and merges them in
+// CL CTA states from the peers' shared memory (mapa + ld.shared::cluster) and merges them in
 // rank order.  Every reduction order depends only on the context length -> deterministic,
 // batch- and SM-budget-invariant; no global workspace, no second kernel.
 constexpr int TKW = 32;   // keys per block
-constexpr int DA_CL = 4;  // CTAs per (request, KV head)
-constexpr int DA_W = 6;   // warps per CTA (smem: 6 x 2 stages x 17 KB): 24 block streams per (request, KV head)
+// CTAs per (request, KV head): 8 when the model has <= 2 KV heads (2B: B x 2 x 4 CTAs leave most
+// of a decode slice idle at the paper's small batches), else 4.  Depends on the model shape only, so
+// a request's result does not depend on the batch or the partition.
+inline int da_cluster(int KV) { return KV <= 2 ? 8 : 4; }
+constexpr int DA_W = 6;   // warps per CTA (smem: 6 x 2 stages x 17 KB): DA_W x CL block streams per (request, KV head)
 template <int HD>
 struct DtcCfg {
   static constexpr int HDP = HD + 8;                       // padded row (conflict-free ldmatrix)
@@ -405,7 +408,7 @@ NOVA_DEV float ld_dsmem_f32(uint32_t local_saddr, uint32_t rank) {
   return v;
 }
 
-template <int HD>
+template <int HD, int CL>
 __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* __restrict__ qkv, int ld,
                                                              const bf16* __restrict__ pool, int layer, int n_pages,
                                                              int H, int KV, const int* __restrict__ bt, int max_pages,
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
     const size_t ps = (size_t)2 * KV * 64 * HD;
     const bf16* lb = pool + (size_t)layer * n_pages * ps;
     const int* bt0 = bt + (size_t)r0.slot * max_pages;
-    for (int blk = rank * DA_W + warp; blk < nb; blk += DA_W * DA_CL) {
+    for (int blk = rank * DA_W + warp; blk < nb; blk += DA_W * CL) {
       const int j = blk * TKW + lane;
       if (j < L0) {
         const bf16* kp = lb + (size_t)bt0[j >> 6] * ps + ((size_t)kvh * 64 + (j & 63)) * HD;
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
   const bf16* lbase = pool + (size_t)layer * n_pages * page_stride;
   const int* btr = bt + (size_t)rr.slot * max_pages;
   const int nblk = (L + TKW - 1) / TKW;
-  const int wg = rank * DA_W + warp, wstride = DA_W * DA_CL;
+  const int wg = rank * DA_W + warp, wstride = DA_W * CL;
   bf16* ring = reinterpret_cast<bf16*>(dsm + Cf::Q_BYTES) + (size_t)warp * 2 * (Cf::BLK / 2);
   auto issue = [&](int blk, int stage) {  // gather K and V rows of block blk into stage
     bf16* wK = ring + (size_t)stage * (Cf::BLK / 2);
@@ -600,9 +603,9 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
     const uint32_t base = smem_u32(sS);
     for (int i = tid; i < G * HD; i += 32 * DA_W) {
       const int row = i / HD, d = i % HD;
-      float m[DA_CL], l[DA_CL], v[DA_CL];
+      float m[CL], l[CL], v[CL];
 #pragma unroll
-      for (int q = 0; q < DA_CL; ++q) {
+      for (int q = 0; q < CL; ++q) {
         const uint32_t a = base + (uint32_t)(row * PW) * 4u;
         m[q] = ld_dsmem_f32(a, q);
         l[q] = ld_dsmem_f32(a + 4u, q);
@@ -610,10 +613,10 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
       }
       float M = m[0];
 #pragma unroll
-      for (int q = 1; q < DA_CL; ++q) M = fmaxf(M, m[q]);
+      for (int q = 1; q < CL; ++q) M = fmaxf(M, m[q]);
       float num = 0.f, den = 0.f;
 #pragma unroll
-      for (int q = 0; q < DA_CL; ++q) {
+      for (int q = 0; q < CL; ++q) {
         const float f = exp2f(m[q] - M);
         den += f * l[q];
         num += f * v[q];
@@ -651,21 +654,24 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
   if (H / KV > 16) return cudaErrorInvalidValue;
   const float sl2 = LOG2E / sqrtf((float)HD);
   cudaError_t e;
-  if (g_decode_attn_tc) {  // tensor-core version: one cluster of DA_CL CTAs per (request, KV head)
+  if (g_decode_attn_tc) {  // tensor-core version: one cluster of da_cluster(KV) CTAs per (request, KV head)
     if (H / KV > 16) return cudaErrorInvalidValue;
+    const int CLN = da_cluster(KV);
+    auto kern = CLN == 8 ? decode_attn_tc_kernel<HD, 8> : decode_attn_tc_kernel<HD, 4>;
     static bool set = false;
     if (!set) {
-      cudaFuncSetAttribute(decode_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD>::SMEM);
       set = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(DA_CL, KV, B);
+    cfg.gridDim = dim3(CLN, KV, B);
     cfg.blockDim = dim3(32 * DA_W);
     cfg.dynamicSmemBytes = DtcCfg<HD>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = DA_CL;
+    at[0].val.clusterDim.x = CLN;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -673,7 +679,7 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
     cfg.attrs = at;
     cfg.numAttrs = g_use_pdl ? 2 : 1;
     count_launch();
-    e = cudaLaunchKernelEx(&cfg, decode_attn_tc_kernel<HD>, qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages, rows,
+    e = cudaLaunchKernelEx(&cfg, kern, qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages, rows,
                            out, ldo, sl2);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
