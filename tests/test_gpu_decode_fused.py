@@ -143,7 +143,7 @@ def test_lm_head_fused_argmax(V_, D):
     assert int(keys.abs().sum().item()) == 0                  # finalize leaves the keys zeroed
 
 
-@pytest.mark.parametrize("N,K", [(4608, 3584), (3584, 18944), (37888, 3584), (256, 128)])
+@pytest.mark.parametrize("N,K", [(4608, 3584), (3584, 18944), (37888, 3584), (256, 128), (17920, 1536)])
 def test_streaming_layout_gemv_bitwise_equals_rowmajor_and_is_grid_invariant(N, K):
     """block_weights + bulk-copy tiles == tensor-map tiles of the row-major weight (bitwise),
     on every SM budget, and both match the oracle linear."""
@@ -159,7 +159,8 @@ def test_streaming_layout_gemv_bitwise_equals_rowmajor_and_is_grid_invariant(N, 
         O.nova_op_gemv_tma(dX[:B], dW, Y0, None, N, K, B, O.EPI_F32_STORE)
         torch.cuda.synchronize()
         assert rel_inf(Y0.cpu().numpy(), ref[:B]) <= 1e-4
-        for ctas in (148, 24, 8):
+        # 148: split units only; 24 / 32 / 8: whole-row-block units first, split units for the rest
+        for ctas in (148, 32, 24, 8):
             Y1 = torch.empty_like(Y0)
             O.nova_op_gemv_stream(dX[:B], Wb, Y1, None, N, K, B, O.EPI_F32_STORE, max_ctas=ctas)
             torch.cuda.synchronize()
