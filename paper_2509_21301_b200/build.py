@@ -19,7 +19,7 @@ LIB = os.path.join(PKG, "libnova.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-          "-I", CSRC, "--expt-relaxed-constexpr"]
+          "-I", CSRC, "--expt-relaxed-constexpr"] + os.environ.get("NOVA_NVCC_EXTRA", "").split()
 
 
 def _headers_mtime() -> float:

@@ -6,17 +6,18 @@
 // The paper's decode stage is memory-bound and Nova gives it a SLICE
 // of the SMs, so the kernel must stream HBM at full rate from however many SMs the
 // partition owns.  Design:
-//  * grid = the partition's SM budget (one CTA per SM, ~100 KB of smem so a PDL successor fits
-//    beside it); each CTA walks a static list of work units (row block x K split) and streams
-//    every weight tile of its units through ONE continuous mbarrier ring (10 x 8 KB for 64-row
-//    blocks), so the bytes in flight per SM stay constant across unit boundaries;
+//  * grid = 4 CTAs per SM of the partition's budget (~40 KB of smem each); each CTA walks a
+//    static list of work units (row block x K split) and streams every weight tile of its units
+//    through ONE continuous mbarrier ring (3 x 8 KB), so the bytes in flight per SM stay constant
+//    across unit boundaries;
 //  * warp 0 (one lane) is the TMA producer: [RB x 64] weight tiles (SWIZZLE_128B) + the matching
 //    [16 x 64] x tile; before griddepcontrol.wait it already requests the weight tiles of the
 //    first ring slots (weights never depend on the previous kernel), x after;
 //  * RB/16 consumer warps, one m16 tile each: swap-AB mma.sync m16n8k16 (weights on M, batch on
 //    N) from ldmatrix on the swizzled tiles;
 //  * the work decomposition (RB, split count P, unit order) depends only on (N, K, epilogue):
-//    P is chosen so units / 148 is close to a whole number of waves on the full GPU.  Split-K
+//    P <= 8 is chosen so units / 592 is close to a whole number of waves on the full GPU; on a
+//    smaller grid a CTA first takes whole row blocks (split partials summed in registers).  Split-K
 //    partials go to a workspace and the last CTA of a row block (atomic ticket) adds them in
 //    split order 0..P-1 -> the result is bitwise independent of the grid and of the batch;
 //  * epilogues: bf16 / f32 store / f32 residual add / SiLU(gate)*up (interleaved 16-row gate|up
@@ -36,24 +37,37 @@ int g_dec_tma_mask = getenv("NOVA_DEC_TMA") ? atoi(getenv("NOVA_DEC_TMA")) : 28;
 
 namespace {
 
+// Ring geometry (scripts/gpu_ring2.sh, decode iterations on 8..112-SM slices and the full GPU):
+// 3 stages x one 8 KB weight tile per CTA, 4 CTAs per SM beat 2 x 16 KB (-8% on 32 SMs, -2% full
+// GPU), 4 x 8 KB, 3 x 16 KB at 3 CTAs/SM, and 5-6 CTAs/SM: the ring's handoff latency, not the
+// bytes in flight, limits a slice -- finer stages release the consumer sooner.
+#ifndef GEMV_STAGES
+#define GEMV_STAGES 3  // ring stages per CTA
+#endif
+#ifndef GEMV_SKB64
+#define GEMV_SKB64 1   // 64-k blocks per stage (64-row blocks)
+#endif
+#ifndef GEMV_CPS
+#define GEMV_CPS 4     // CTAs per SM of the budget
+#endif
 constexpr int KC = 64;        // k per stage (128-byte rows -> SWIZZLE_128B)
 constexpr int XR = 16;        // x rows per stage tile (batch padded to 16)
 constexpr int X_BYTES = XR * KC * 2;
 
-// Ring geometry: ~45 KB per CTA and FOUR CTAs per SM of the budget.  scripts/probe_bw.cu on
+// Ring geometry: ~40 KB per CTA and FOUR CTAs per SM of the budget.  scripts/probe_bw.cu on
 // B200 partitions: bulk-copy streaming scales with the number of independent producer CTAs per
 // SM (1 CTA x 24 x 8 KB: 77 GB/s/SM; 4 CTAs x 6 x 8 KB: 215 GB/s/SM on a 24-SM slice), not
 // with the bytes in flight.
 template <int RB, int XHL>
 struct PCfg {
   static constexpr int NW = RB / 16;                 // m16 tiles = epilogue warps
-  static constexpr int SKB = RB == 64 ? 2 : 1;       // 64-k blocks per ring stage (16 KB of weights)
+  static constexpr int SKB = RB == 64 ? GEMV_SKB64 : 1;  // 64-k blocks per ring stage
   static constexpr int NWC = SKB >= 2 ? 2 * NW : NW; // consumer warps: (m tile, k half)
   static constexpr int KB_W = RB * KC * 2;           // weight bytes per k block
   static constexpr int W_BYTES = SKB * KB_W;
   static constexpr int XT = XHL ? 2 : 1;             // x tiles per k block (hi, lo)
   static constexpr int XS_BYTES = SKB * X_BYTES;     // x bytes per stage (per part)
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = GEMV_STAGES;
   static constexpr int RED_FLOATS = NW * 2 * 32 * 4; // epilogue exchange (NT <= 2)
   static constexpr int SMEM = 1024 + STAGES * (W_BYTES + XT * XS_BYTES) + 8 * (2 * STAGES) + 64 + 2 * RED_FLOATS * 4;
 };
@@ -74,7 +88,7 @@ struct PGemvArgs {
 };
 
 template <int RB, int NT, int EPI, int XHL>
-__global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC), 4) gemv_tma_kernel(const __grid_constant__ CUtensorMap tmW,
+__global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC), GEMV_CPS) gemv_tma_kernel(const __grid_constant__ CUtensorMap tmW,
                                                                           const __grid_constant__ CUtensorMap tmX,
                                                                           const __grid_constant__ CUtensorMap tmX2,
                                                                           PGemvArgs a) {
@@ -525,7 +539,7 @@ cudaError_t gemv_tma(const bf16* X, int ldx, const bf16* W, int N, int K, void* 
   if (pl.P > 1 && (!ws || !tickets)) return cudaErrorInvalidValue;
   PGemvArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks, pl.P, pl.units, aux ? *aux : GemvAux{}};
   // four CTAs per SM of the budget (PCfg)
-  int grid = 4 * (max_ctas > 0 ? max_ctas : 148);
+  int grid = GEMV_CPS * (max_ctas > 0 ? max_ctas : 148);
   if (grid > pl.units) grid = pl.units;
   if (X_lo) {  // f32 x given as bf16 hi + lo (decode lm_head)
     if (epi == EPI_F32_ARGMAX) return launch_nt<64, EPI_F32_ARGMAX, 1>(mw, mx, mx2, a, grid, s);
