@@ -33,7 +33,7 @@
 namespace nova {
 
 bool g_use_tma_gemv = true;
-int g_dec_tma_mask = getenv("NOVA_DEC_TMA") ? atoi(getenv("NOVA_DEC_TMA")) : 28;  // measured best: scripts/gpu_mask.sh
+int g_dec_tma_mask = getenv("NOVA_DEC_TMA") ? atoi(getenv("NOVA_DEC_TMA")) : -1;  // -1: per-shape rule (stages.cpp)
 
 namespace {
 

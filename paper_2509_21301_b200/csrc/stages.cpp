@@ -247,7 +247,10 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
   // Per linear: the persistent TMA GEMV over the streaming layout, sized to the decode partition
   // (sms SMs, 4 CTAs each), or the register-streaming GEMV (fixed grid; RMSNorm on load for qkv).
   // g_dec_tma_mask bit 0 qkv, 1 o, 2 gate|up, 3 down, 4 lm_head (env NOVA_DEC_TMA overrides).
-  const int tm = g_dec_tma_mask;
+  // Default, from the model shape only (scripts/gpu_s3p.sh, decode iterations on 8..148 SMs):
+  // gate|up, down and lm_head on the TMA GEMV; o as well once it is >= 8 M weights (7B: 4-15%
+  // faster on slices, level on the full GPU; 2B's 2.4 M o-proj is faster on the register GEMV).
+  const int tm = g_dec_tma_mask >= 0 ? g_dec_tma_mask : (28 | ((size_t)D * H * hd >= (size_t)8 << 20 ? 2 : 0));
   const bool rope_tma = (tm & 1) && hd == 128;
   for (int l = 0; l < m.llm_layers; ++l) {
     const LlmLayerW& L = W.llm[l];
