@@ -91,9 +91,52 @@ __global__ void __launch_bounds__(512) rmsnorm_kernel(const float* __restrict__ 
                                                       void* __restrict__ y, int y_f32, int ldy, int M, int d, float eps) {
   __shared__ float red[4][4];
   pdl_launch_dependents();
-  pdl_wait();
   const int grp = threadIdx.x >> 7, v = threadIdx.x & 127;
   const int row = blockIdx.x * 4 + grp;
+  const int nch = d >> 2;
+  if (nch <= 8 * NORM_LANES && y_f32 == 0) {
+    // d <= 4096, bf16 out (the decode norms before the TMA GEMVs): gamma is requested before
+    // griddepcontrol.wait and the row stays in registers between the statistics and the output --
+    // the same operations in the same order as row_sumsq_canonical + the loop below (same bits)
+    uint2 gv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = v + i * NORM_LANES;
+      gv[i] = f < nch ? *reinterpret_cast<const uint2*>(gm + 4 * f) : make_uint2(0u, 0u);
+    }
+    pdl_wait();
+    if (row >= M) return;
+    const float* xr = x + (size_t)row * ldx;
+    float4 xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = v + i * NORM_LANES;
+      xv[i] = f < nch ? reinterpret_cast<const float4*>(xr)[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float sq = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = v + i * NORM_LANES;
+      if (f < nch) sq += (xv[i].x * xv[i].x + xv[i].y * xv[i].y) + (xv[i].z * xv[i].z + xv[i].w * xv[i].w);
+    }
+    sq = warp_sum(sq);
+    if ((v & 31) == 0) red[grp][v >> 5] = sq;
+    asm volatile("bar.sync %0, 128;" ::"r"(grp + 1) : "memory");
+    const float t = ((red[grp][0] + red[grp][1]) + red[grp][2]) + red[grp][3];
+    const float rs = rsqrtf(t / d + eps);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = v + i * NORM_LANES;
+      if (f >= nch) continue;
+      const float2 g01 = unpack_bf16(gv[i].x), g23 = unpack_bf16(gv[i].y);
+      uint2 o;
+      o.x = pack_bf16(xv[i].x * rs * g01.x, xv[i].y * rs * g01.y);
+      o.y = pack_bf16(xv[i].z * rs * g23.x, xv[i].w * rs * g23.y);
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(y) + (size_t)row * ldy + 4 * f) = o;
+    }
+    return;
+  }
+  pdl_wait();
   if (row >= M) return;  // whole 128-thread group: named barrier grp + 1 stays consistent
   const float* xr = x + (size_t)row * ldx;
   const float rs = rsqrtf(row_sumsq_canonical(xr, d, v, red[grp], grp + 1) / d + eps);
