@@ -67,9 +67,12 @@ typedef struct {
   int32_t max_prompt;           /* max prompt tokens                                           */
   int32_t max_gen;              /* max generated tokens per request (gen_len)                  */
   int32_t vit_resident_layers;  /* K physical ViT layer slots (Eq. 7); 0 = all layers resident */
-  int32_t use_green_ctx;        /* 1: SM partitions via green contexts; 0: primary context only */
+  int32_t use_green_ctx;        /* 1: SM partitions via green contexts (nova_finalize fails with
+                                   NOVA_E_CUDA if the driver cannot split the SMs); 0: primary
+                                   context only (every split runs on all SMs)                    */
   int32_t debug_keep_logits;    /* keep every step's f32 logits for nova_debug_logits          */
-  int32_t reserved;
+  int32_t finished_retention;   /* finished requests kept for nova_request_stats / debug_logits;
+                                   older ones are released oldest-first (0 = 4096, < 0 = all)   */
 } nova_engine_config;
 
 /* Device buffer sizes the caller must provide (GPU backend); pinned_host_bytes is
@@ -183,6 +186,9 @@ typedef struct {
   int32_t n_tokens, finished;
 } nova_req_stats;
 nova_status nova_request_stats(nova_engine* e, uint64_t req_id, nova_req_stats* out);
+/* Release a FINISHED request's record (stats, tokens, debug logits) now instead of at the
+ * finished_retention bound.  NOVA_E_NOTFOUND if unknown, NOVA_E_STATE if not finished. */
+nova_status nova_release_request(nova_engine* e, uint64_t req_id);
 
 /* Decision log of Algorithm 1 (for replay against the oracle). */
 enum { NOVA_DEC_VISION = 0, NOVA_DEC_PREFILL = 1, NOVA_DEC_DECODE = 2, NOVA_DEC_FINISH = 3 };
@@ -197,9 +203,15 @@ typedef struct {
   int32_t n_ids;
   uint64_t ids[16];  /* request ids (batch for decode)                            */
 } nova_log_record;
-/* Copy log records [start, start + cap) ; n_out = records copied; total = all records. */
+/* The log is a bounded ring of NOVA_LOG_CAPACITY records: record indices are absolute (0 = the
+ * first record ever written); records below nova_decision_log_base() have been dropped.
+ * Copy log records [start, start + cap) ; n_out = records copied; total = all records ever
+ * written.  NOVA_E_NOTFOUND if start < nova_decision_log_base(). */
+#define NOVA_LOG_CAPACITY (1 << 18)
 nova_status nova_decision_log(nova_engine* e, int64_t start, nova_log_record* buf, int32_t cap, int32_t* n_out,
                               int64_t* total);
+/* Index of the oldest retained log record (0 until the ring first wraps); -1 for a NULL engine. */
+int64_t nova_decision_log_base(nova_engine* e);
 
 /* ------------------------------------------------------------------ debug / parity */
 /* f32 logits of token `index` of a request (needs debug_keep_logits). */

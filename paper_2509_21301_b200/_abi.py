@@ -16,7 +16,7 @@ class ModelConfig(C.Structure):
 class EngineConfig(C.Structure):
     _fields_ = [(n, I32) for n in ("backend", "device", "max_requests", "max_decode_batch", "kv_pages",
                                    "max_patches", "max_prompt", "max_gen", "vit_resident_layers",
-                                   "use_green_ctx", "debug_keep_logits", "reserved")]
+                                   "use_green_ctx", "debug_keep_logits", "finished_retention")]
 
 
 class Buffers(C.Structure):
@@ -89,6 +89,8 @@ ENGINE_SIGNATURES = {
     "nova_poll_tokens": (R, [E, C.POINTER(Token), I32, C.POINTER(I32)]),
     "nova_request_stats": (R, [E, U64, C.POINTER(ReqStats)]),
     "nova_decision_log": (R, [E, I64, C.POINTER(LogRecord), I32, C.POINTER(I32), C.POINTER(I64)]),
+    "nova_decision_log_base": (I64, [E]),
+    "nova_release_request": (R, [E, U64]),
     "nova_debug_logits": (R, [E, U64, I32, C.POINTER(F32), I32]),
     "nova_debug_force_tokens": (R, [E, U64, C.POINTER(I32), I32]),
     "nova_time_pass": (R, [E, I32, I32, I32, I32, I32, I32, I32, I32, I32, C.POINTER(F64)]),

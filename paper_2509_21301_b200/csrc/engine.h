@@ -177,8 +177,9 @@ class Engine {
  public:
   Dims dims;
   nova_engine_config cfg{};
-  std::string err;
-  bool failed = false;
+  std::string err;             // guarded by err_mu (written by the role workers, submit, step)
+  mutable std::mutex err_mu;
+  std::atomic<bool> failed{false};
   bool finalized = false;
   bool sim = false;
 
@@ -187,6 +188,10 @@ class Engine {
   Weights W;
   VitLayerLayout vl;
   int vit_K = 0;  // physical slots (0 = resident)
+  // offload ring: physical slot holding each logical ViT layer (-1 = not resident).  Updated at
+  // every swap-in, so the mapping stays right across passes when K does not divide L (Eq. 7
+  // refills slot (l mod K) only in the first pass; afterwards the slots rotate).
+  std::vector<int> vit_slot_of;
   uint16_t* host_vit = nullptr;  // pinned arena of all ViT layers (offload)
   cudaStream_t copy_stream = nullptr, upload_stream = nullptr;
   std::vector<cudaEvent_t> ev_loaded, ev_free;
@@ -242,7 +247,9 @@ class Engine {
   std::vector<int> free_slots, free_pages;
   std::deque<nova_token> tok_q;
   std::mutex tok_mu;
-  std::vector<nova_log_record> log;
+  std::deque<nova_log_record> log;  // bounded ring (NOVA_LOG_CAPACITY); log[i] is record log_base + i
+  int64_t log_base = 0;
+  std::deque<uint64_t> finished_ids;  // release order for cfg.finished_retention
   int tick_no = 0;
   int finished = 0;
   nova_step_info last_info{};
@@ -265,9 +272,16 @@ class Engine {
   void shutdown();
   ~Engine() { shutdown(); }
   nova_status fail(nova_status s, const std::string& m) {
-    err = m;
-    if (s == NOVA_E_CUDA) failed = true;
+    {
+      std::lock_guard<std::mutex> g(err_mu);
+      err = m;
+    }
+    if (s == NOVA_E_CUDA) failed.store(true);
     return s;
+  }
+  std::string last_error() const {
+    std::lock_guard<std::mutex> g(err_mu);
+    return err;
   }
 
   // memory plans
@@ -282,6 +296,7 @@ class Engine {
   void post_completion(Event&& e);
   void finish_request(Request* r);
   void log_event(const Event& e);
+  void log_push(const nova_log_record& r);
   void log_decision(const Decision& d, int64_t t);
 
   // stage programs (model.cpp); return cudaError

@@ -88,6 +88,9 @@ std::string Partition::init(int device, bool use_green) {
       green = true;
       return "";
     }
+    // Partitioning was requested but the driver cannot split the SMs: fail loudly rather than
+    // run every policy on one shared stream while reporting splits that isolate nothing.
+    return "green-context SM split unavailable (fewer than 2 groups of 8 SMs); use_green_ctx = 0 runs unpartitioned";
   }
   // no partitioning: every role stream is a plain primary-context stream
   granularity = 8;
@@ -202,8 +205,7 @@ void Worker::run() {
       eng->ktimer[role].harvest(eng->kstats, eng->kmu);
     }
     if (e != cudaSuccess) {
-      eng->err = std::string("CUDA error in stage pass: ") + cudaGetErrorString(e);
-      eng->failed = true;
+      eng->fail(NOVA_E_CUDA, std::string("CUDA error in stage pass: ") + cudaGetErrorString(e));
     } else {
       const int V = eng->dims.m.vocab;
       if (c.kind == NOVA_DEC_PREFILL) {
@@ -300,6 +302,8 @@ nova_status Engine::finalize() {
   for (auto& ev : ev_upload)
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(NOVA_E_CUDA, "events");
   if (vit_K > 0) {  // preload logical layers 0..K-1 into the physical slots
+    vit_slot_of.assign(dims.m.vit_depth, -1);
+    for (int k = 0; k < vit_K; ++k) vit_slot_of[k] = k;
     ev_loaded.assign(vit_K, nullptr);
     ev_free.assign(vit_K, nullptr);
     for (int k = 0; k < vit_K; ++k) {
@@ -382,7 +386,7 @@ void Engine::shutdown() {
 
 // ---------------------------------------------------------------- requests
 nova_status Engine::submit(const nova_request* q, uint64_t* id) {
-  if (failed) return fail(NOVA_E_STATE, "engine failed: " + err);
+  if (failed) return fail(NOVA_E_STATE, "engine failed: " + last_error());
   if (!finalized) return fail(NOVA_E_STATE, "nova_finalize first");
   const auto& m = dims.m;
   const int unit = m.patch * m.merge;
@@ -458,6 +462,23 @@ void Engine::finish_request(Request* r) {
   for (int p : r->pages) free_pages.push_back(p);
   r->pages.clear();
   free_slots.push_back(r->slot);
+  // Bounded memory for a long-running server: keep the records of the last `retention` finished
+  // requests (no pass or scheduler queue references a finished request any more).
+  finished_ids.push_back(r->id);
+  const int ret = cfg.finished_retention == 0 ? 4096 : cfg.finished_retention;
+  if (ret > 0)
+    while ((int)finished_ids.size() > ret) {
+      reqs.erase(finished_ids.front());  // no-op if already released by nova_release_request
+      finished_ids.pop_front();
+    }
+}
+
+void Engine::log_push(const nova_log_record& r) {
+  log.push_back(r);
+  while (log.size() > (size_t)NOVA_LOG_CAPACITY) {
+    log.pop_front();
+    log_base++;
+  }
 }
 
 void Engine::log_event(const Event& e) {
@@ -468,7 +489,7 @@ void Engine::log_event(const Event& e) {
   rec.kind = e.kind;
   rec.n_ids = (int)std::min<size_t>(16, e.reqs.size());
   for (int i = 0; i < rec.n_ids; ++i) rec.ids[i] = e.reqs[i]->id;
-  log.push_back(rec);
+  log_push(rec);
 }
 
 void Engine::log_decision(const Decision& d, int64_t t) {
@@ -481,7 +502,7 @@ void Engine::log_decision(const Decision& d, int64_t t) {
   rec.s_dec = d.s_dec;
   rec.n_ids = (int)std::min<size_t>(16, d.reqs.size());
   for (int i = 0; i < rec.n_ids; ++i) rec.ids[i] = d.reqs[i]->id;
-  log.push_back(rec);
+  log_push(rec);
 }
 
 static int64_t curve_at(const std::vector<int32_t>& s, const std::vector<int64_t>& t, int v) {
@@ -550,7 +571,7 @@ void Engine::dispatch(const Decision& d) {
 }
 
 nova_status Engine::step(int64_t max_wait_us, nova_step_info* out) {
-  if (failed) return fail(NOVA_E_STATE, "engine failed: " + err);
+  if (failed) return fail(NOVA_E_STATE, "engine failed: " + last_error());
   if (!finalized) return fail(NOVA_E_STATE, "nova_finalize first");
   std::vector<Event> evs;
   int64_t now;
@@ -610,7 +631,7 @@ nova_status Engine::step(int64_t max_wait_us, nova_step_info* out) {
       g.unlock();
       gather();
     }
-    if (failed) return fail(NOVA_E_STATE, "engine failed: " + err);
+    if (failed) return fail(NOVA_E_STATE, "engine failed: " + last_error());
     now = mono_ns();
   }
   // completions: stamp stats, emit tokens

@@ -51,7 +51,7 @@ nova_status nova_create(const nova_model_config* m, const nova_engine_config* c,
     nova_engine* e = new nova_engine();
     nova_status s = e->e.create(m, c, b);
     if (s != NOVA_OK) {
-      g_create_err = e->e.err;
+      g_create_err = e->e.last_error();
       delete e;
       *out = nullptr;
       return s;
@@ -80,7 +80,12 @@ nova_status nova_destroy(nova_engine* e) {
   })
 }
 
-const char* nova_last_error(nova_engine* e) { return e ? e->e.err.c_str() : g_create_err.c_str(); }
+// A thread-local copy: the engine's message may be rewritten by its worker threads at any time.
+const char* nova_last_error(nova_engine* e) {
+  static thread_local std::string msg;
+  msg = e ? e->e.last_error() : g_create_err;
+  return msg.c_str();
+}
 
 nova_status nova_query_sms(nova_engine* e, int32_t* total, int32_t* gran, int32_t* n_splits) {
   if (!e) return NOVA_E_INVAL;
@@ -174,11 +179,26 @@ nova_status nova_decision_log(nova_engine* e, int64_t start, nova_log_record* bu
                               int64_t* total) {
   if (!e || start < 0) return NOVA_E_INVAL;
   Engine& E = e->e;
-  const int64_t tot = (int64_t)E.log.size();
+  const int64_t tot = E.log_base + (int64_t)E.log.size();
+  if (start < E.log_base) return E.fail(NOVA_E_NOTFOUND, "decision log records before the ring base were dropped");
+  if (cap > 0 && !buf) return NOVA_E_INVAL;
   int n = 0;
-  for (int64_t i = start; i < tot && n < cap; ++i) buf[n++] = E.log[i];
+  for (int64_t i = start; i < tot && n < cap; ++i) buf[n++] = E.log[(size_t)(i - E.log_base)];
   if (n_out) *n_out = n;
   if (total) *total = tot;
+  return NOVA_OK;
+}
+
+int64_t nova_decision_log_base(nova_engine* e) { return e ? e->e.log_base : -1; }
+
+nova_status nova_release_request(nova_engine* e, uint64_t id) {
+  if (!e) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  std::lock_guard<std::mutex> g(E.ctl_mu);
+  auto it = E.reqs.find(id);
+  if (it == E.reqs.end()) return NOVA_E_NOTFOUND;
+  if (!it->second->st.finished) return E.fail(NOVA_E_STATE, "request not finished");
+  E.reqs.erase(it);
   return NOVA_OK;
 }
 

@@ -104,8 +104,9 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
   for (int l = 0; l < L; ++l) {
     bf16* blk;
     int k = 0;
-    if (vit_K > 0) {  // Eq. 7 ring: slot l mod K holds logical layer l
-      k = l % vit_K;
+    if (vit_K > 0) {  // Eq. 7 ring: the slot that received logical layer l
+      k = vit_slot_of[l];
+      if (k < 0) return cudaErrorInvalidValue;  // ring bookkeeping broken (never expected)
       CUDA_TRY(cudaStreamWaitEvent(s, ev_loaded[k], 0));
       blk = W.vit_dev[k];
     } else {
@@ -133,6 +134,8 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
       CUDA_TRY(cudaEventRecord(ev_free[k], s));
       CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_free[k], 0));
       const int nxt = (l + vit_K) % L;
+      vit_slot_of[l] = -1;
+      vit_slot_of[nxt] = k;
       CUDA_TRY(cudaMemcpyAsync(W.vit_dev[k], host_vit + (size_t)nxt * vl.elems, vl.elems * 2, cudaMemcpyHostToDevice,
                                copy_stream));
       CUDA_TRY(cudaEventRecord(ev_loaded[k], copy_stream));

@@ -57,11 +57,12 @@ class EngineOptions:
     vit_resident_layers: int = 0
     use_green_ctx: int = 1
     debug_keep_logits: int = 0
+    finished_retention: int = 0   # 0: the engine default (4096 finished requests), < 0: keep all
 
     def cstruct(self) -> A.EngineConfig:
         ec = A.EngineConfig()
         for f in ("backend", "device", "max_requests", "max_decode_batch", "kv_pages", "max_patches", "max_prompt",
-                  "max_gen", "vit_resident_layers", "use_green_ctx", "debug_keep_logits"):
+                  "max_gen", "vit_resident_layers", "use_green_ctx", "debug_keep_logits", "finished_retention"):
             setattr(ec, f, int(getattr(self, f)))
         return ec
 
@@ -196,8 +197,12 @@ class Engine:
         self._check(self.lib.nova_request_stats(self.h, rid, C.byref(s)), "nova_request_stats")
         return {f: getattr(s, f) for f, _ in A.ReqStats._fields_}
 
+    def release(self, rid: int) -> None:
+        self._check(self.lib.nova_release_request(self.h, rid), "nova_release_request")
+
     def decision_log(self) -> list:
-        out, start = [], 0
+        """Retained records (the log is a bounded ring: records before nova_decision_log_base are gone)."""
+        out, start = [], self.lib.nova_decision_log_base(self.h)
         buf = (A.LogRecord * 4096)()
         while True:
             n, tot = A.I32(), A.I64()

@@ -203,3 +203,44 @@ def test_submit_validation(E):
         e.submit(None, [1], 2, 0, grid=(3, 4))        # not a multiple of patch*merge
     with pytest.raises(E.NovaError):
         e.set_partition(E.STATIC, sm_decode_dv=0, sm_decode_dp=8)
+
+
+def test_finished_retention_and_release(E):
+    """Bounded memory: finished requests beyond finished_retention are released
+    oldest-first; nova_release_request frees one early; unfinished ones cannot be released."""
+    e = E.Engine(TINY, E.EngineOptions(backend=E.BACKEND_SIM, max_requests=64, max_gen=64, finished_retention=3))
+    e.sim_set_curves([8], [MS], [MS], [MS], [MS], MS, MS, MS)
+    e.finalize()
+    e.set_partition(E.SERIAL)
+    ids = [e.submit(None, [1], 2, i * MS, grid=(4, 4)) for i in range(6)]
+    late = e.submit(None, [1], 2, 10_000 * MS, grid=(4, 4))
+    while e.step().finished < 6:
+        pass
+    for rid in ids[:3]:          # released by the retention bound
+        with pytest.raises(E.NovaError):
+            e.stats(rid)
+    assert all(e.stats(rid)["finished"] for rid in ids[3:])
+    e.release(ids[3])
+    with pytest.raises(E.NovaError):
+        e.stats(ids[3])
+    with pytest.raises(E.NovaError):
+        e.release(late)          # not finished yet
+    assert e.stats(late)["finished"] == 0
+
+
+def test_decision_log_ring_base(E):
+    """The decision log is a bounded ring with absolute record indices (base 0 until it wraps)."""
+    import ctypes as C
+    from paper_2509_21301_b200 import _abi as A
+    e = _sim_engine(E, E.SERIAL, [8], [MS], [MS], [MS], [MS], (MS, MS, MS))
+    for i in range(4):
+        e.submit(None, [1], 3, i * MS, grid=(4, 4))
+    while e.step().events:
+        pass
+    assert e.lib.nova_decision_log_base(e.h) == 0
+    log = e.decision_log()
+    n, tot = A.I32(), A.I64()
+    buf = (A.LogRecord * 8)()
+    assert e.lib.nova_decision_log(e.h, 2, buf, 8, C.byref(n), C.byref(tot)) == 0
+    assert tot.value == len(log) and n.value == 8 and buf[0].tick == log[2][0]
+    assert e.lib.nova_decision_log(e.h, -1, buf, 8, C.byref(n), C.byref(tot)) != 0

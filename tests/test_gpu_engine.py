@@ -6,7 +6,8 @@ oracle on the same generated weights and inputs (SURVEY.md §8(c) c1', c6).
   STATIC splits, ADAPTIVE, the frontier-lookup controller and the paper's PF-Limit /
   Multi-Stream baselines on a
   20-request trace (BASELINE).
-- offload: K = 2, 3 physical ViT layers give bitwise the all-resident outputs.
+- offload: K = 2, 3, 4 physical ViT layers give bitwise the all-resident outputs over several
+  vision passes, with a depth (7) that no K divides (the ring's slots rotate across passes).
 - full width (reduced depth): 2B / 7B widths at the BASELINE image size (N = 4888),
   S = 1286, tokens teacher-forced, logits within tolerance.
 """
@@ -116,11 +117,11 @@ def test_coexec_bitwise_equals_serial(tiny_setup):
 
 def test_offload_bitwise_equals_resident():
     from paper_2509_21301_b200 import engine as E
-    s = replace(TINY, name="tiny-d6", vit_depth=6)
+    s = replace(TINY, name="tiny-d7", vit_depth=7)   # 7 % K != 0 for every K below
     bits = gen_weights(s, 4)
-    reqs = [make_request(s, (4, 4), 6, 4, 200 + i) for i in range(3)]
+    reqs = [make_request(s, (4, 4), 6, 4, 200 + i) for i in range(4)]   # 4 vision passes
     outs = []
-    for K in (0, 2, 3):
+    for K in (0, 2, 3, 4):
         e = _engine(s, bits, vit_resident_layers=K)
         e.set_partition(E.ADAPTIVE, sm_op_dv=32, sm_op_dp=32, sm_min=8, alpha_dv=8.0, alpha_dp=8.0)
         outs.append(_run(e, reqs))
