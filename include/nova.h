@@ -220,6 +220,15 @@ nova_status nova_debug_logits(nova_engine* e, uint64_t req_id, int32_t index, fl
  * of step k-1.  Must be called right after nova_submit. */
 nova_status nova_debug_force_tokens(nova_engine* e, uint64_t req_id, const int32_t* tokens, int32_t n);
 
+/* Copy an internal decode workspace buffer to host memory (parity debugging; synchronizes the
+ * device).  name: "dec_hid" (f32 [max_decode_batch][llm_dim]), "dec_xg" / "dec_xlo" (bf16
+ * [max_decode_batch][llm_dim]), "dec_qkvf" (f32 [max_decode_batch][(H + 2 KV) hd]), "dec_attn"
+ * (bf16 [max_decode_batch][H hd]), "dec_act" (bf16 [max_decode_batch][ffn]), "dec_ss" (f32
+ * [max_decode_batch][ceil4(llm_dim / 64)]); layer-0 weights "w_o0" (o_proj, [out][in]), "w_ob0" /
+ * "w_qkvb0" (o / qkv in the decode streaming layout); "dec_dbg" (fused-decode phase timeline, u64).  bytes <= the buffer size, else NOVA_E_INVAL;
+ * unknown name -> NOVA_E_NOTFOUND.  Works on a FAILED engine (post-mortem). */
+nova_status nova_debug_read_buffer(nova_engine* e, const char* name, void* out, uint64_t bytes);
+
 /* ------------------------------------------------------------------ live kernel timing */
 /* Kernel classes with their ALGORITHMIC work unit (what the method must move or
  * compute, no padding):                                        */
@@ -234,7 +243,8 @@ enum {
   NOVA_K_VIT_PASS = 7,   /* whole vision pass: flops (SURVEY §8(d) d2 a5 formula)           */
   NOVA_K_PRE_PASS = 8,   /* whole prefill pass: flops (a6 formula)                          */
   NOVA_K_DEC_PASS = 9,   /* whole decode iteration: bytes = weights + KV read (a7 formula)  */
-  NOVA_K_COUNT = 10
+  NOVA_K_DEC_FUSED = 10, /* fused decode-iteration kernel (one launch): bytes = a7 formula    */
+  NOVA_K_COUNT = 11
 };
 /* every_n = 0 disables; n >= 1 brackets the kernels of every n-th pass of each role
  * with CUDA events on the stream they are launched on (whole passes: every pass). */

@@ -92,6 +92,7 @@ ENGINE_SIGNATURES = {
     "nova_decision_log_base": (I64, [E]),
     "nova_release_request": (R, [E, U64]),
     "nova_debug_logits": (R, [E, U64, I32, C.POINTER(F32), I32]),
+    "nova_debug_read_buffer": (R, [E, C.c_char_p, C.c_void_p, U64]),
     "nova_debug_force_tokens": (R, [E, U64, C.POINTER(I32), I32]),
     "nova_time_pass": (R, [E, I32, I32, I32, I32, I32, I32, I32, I32, I32, C.POINTER(F64)]),
     "nova_plan": (R, [C.POINTER(Curves), F64, F64, C.POINTER(PlanPoint), I32, C.POINTER(I32), C.POINTER(PlanPoint),

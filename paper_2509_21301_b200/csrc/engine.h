@@ -215,6 +215,9 @@ class Engine {
   } fw{};
   struct DecWS {
     float *hid, *xf, *logits, *attn_ws, *gemv_ws;
+    float *qkvf, *ss;           // fused decode: f32 raw qkv rows, per-64-column sums of squares
+    bf16* xlo;                  // fused decode: lo tile of the f32 lm_head input
+    unsigned long long* bar;    // fused decode: grid-barrier counter (monotone; see dec_bar_base)
     int* tickets;               // [0, 4096): gemv_tma row blocks; [4096, 8192): decode attention
     unsigned long long* keys;  // greedy argmax, zero between passes
     bf16 *xb, *qkv, *attn, *act;
@@ -226,6 +229,8 @@ class Engine {
     float* h_logits;
   } dw{};
   Partition part;
+  DecFusedState* dfs = nullptr;     // fused decode kernel state (null: per-op decode path)
+  unsigned long long dec_bar_base = 0;  // grid-barrier counter value at the next fused launch
   Worker front_w, dec_w;
   KTimer ktimer[2];                  // per role (0 front, 1 decode)
   KStat kstats[NOVA_K_COUNT];

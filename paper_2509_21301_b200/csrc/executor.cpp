@@ -336,6 +336,25 @@ nova_status Engine::finalize() {
   cudaMemset(d_last, 0, (size_t)n_slots_total * 4);
   cudaMemset(dw.tickets, 0, 8192 * 4);
   cudaMemset(dw.keys, 0, (size_t)cfg.max_decode_batch * 8);
+  cudaMemset(dw.bar, 0, 512 * 8);
+  dec_bar_base = 0;
+  {  // fused decode iteration: tensor maps of the activation tiles and the paged pool
+    const auto& m = dims.m;
+    if (g_dec_fused && decode_fused_supported(m.llm_dim, m.llm_heads, m.llm_kv_heads, m.head_dim, m.llm_ffn, m.vocab)) {
+      DecFusedSetup su;
+      su.L = m.llm_layers, su.D = m.llm_dim, su.H = m.llm_heads, su.KV = m.llm_kv_heads, su.hd = m.head_dim;
+      su.F = m.llm_ffn, su.V = m.vocab, su.bmax = cfg.max_decode_batch, su.n_pages = cfg.kv_pages;
+      su.xg = dw.xb, su.xlo = dw.xlo, su.attn = dw.attn, su.act = dw.act;
+      su.pool = reinterpret_cast<const bf16*>(buf.kv_dev);
+      for (const LlmLayerW& L : W.llm) {
+        su.ln1.push_back(L.ln1), su.ln2.push_back(L.ln2), su.qkv_b.push_back(L.qkv_b);
+        su.qkv_wb.push_back(L.qkv_wb), su.o_wb.push_back(L.o_wb), su.gu_wb.push_back(L.gu_wb);
+        su.down_wb.push_back(L.down_wb);
+      }
+      dfs = decode_fused_create(su);
+      if (!dfs) return fail(NOVA_E_CUDA, "fused decode setup (tensor maps / layer table)");
+    }
+  }
   cudaMemset(fw.keys, 0, 16 * 8);
   ktimer[0].init(512);
   ktimer[1].init(512);
@@ -359,6 +378,8 @@ void Engine::shutdown() {
     cudaDeviceSynchronize();
     ktimer[0].destroy();
     ktimer[1].destroy();
+    decode_fused_destroy(dfs);
+    dfs = nullptr;
     part.destroy();
     for (auto ev : ev_upload) cudaEventDestroy(ev);
     for (auto ev : ev_loaded) cudaEventDestroy(ev);

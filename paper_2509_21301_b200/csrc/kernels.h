@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <vector>
 
 namespace nova {
 
@@ -122,6 +123,54 @@ struct GemvAux {
 // x modes: 0 bf16, 1 f32 (hi/lo split), 2 f32 residual + RMSNorm on load -> bf16, 3 same -> hi/lo
 cudaError_t gemv_ex(const void* X, int xmode, int ldx, const bf16* W, int N, int K, void* Y, int ldy,
                     const bf16* bias, int B, int epi, const GemvAux& aux, cudaStream_t s);
+// Fused persistent decode iteration (decode_fused.cu): ONE launch runs embed -> L x (qkv,
+// attention, o, gate|up, down) -> lm_head + argmax for B <= 16 rows on a grid of 4 CTAs per SM of
+// the decode partition, phases separated by in-kernel grid barriers (decode_fused_barriers(L) <= 512
+// monotone per-phase counters, each gaining `grid` per launch; the caller keeps the running base).  Bitwise
+// independent of the grid size.  Supported shapes: decode_fused_supported().
+extern int g_dec_fused;  // env NOVA_DEC_FUSED=1: use the fused kernel where supported (default 0: the per-op path is faster)
+struct DecFusedState;
+struct DecFusedSetup {
+  int L, D, H, KV, hd, F, V, bmax, n_pages;
+  const bf16 *xg, *xlo, *attn, *act, *pool;  // activation tile buffers [bmax][cols]; paged pool
+  std::vector<const bf16*> ln1, ln2, qkv_b, qkv_wb, o_wb, gu_wb, down_wb;
+};
+struct DecFusedRun {
+  int L, D, H, KV, hd, F, V, B, max_ctx;
+  float eps, theta;
+  const bf16 *embed, *final_norm, *lm_wb;
+  float* hid;
+  bf16 *xg, *xlo;
+  float* qkvf;
+  bf16 *attn, *act;
+  float* ss;
+  float* logits;
+  unsigned long long* keys;
+  float* ws;
+  int* tickets;
+  float* aws;
+  int* atk;
+  unsigned long long* bar;
+  unsigned long long bar_base;
+  bf16* pool;
+  int n_pages, max_pages;
+  const int* bt;
+  const DecodeRow* rows;
+  int* last_tok;
+  int* tok_out;
+  int store_logits;
+  int mch;     // aws chunk capacity per (request, KV head): >= ceil((max_ctx + 1) / 128)
+  int ph_end;  // 0 = whole iteration; k > 0: stop before phase k (debug bisection)
+};
+int decode_fused_phase_chunk();  // keys per attention chunk (aws sizing)
+bool decode_fused_supported(int D, int H, int KV, int hd, int F, int V);
+DecFusedState* decode_fused_create(const DecFusedSetup& su);
+void decode_fused_destroy(DecFusedState* st);
+int decode_fused_barriers(int L);
+int decode_fused_smem();
+int decode_fused_grid(int sms);  // CTAs of a launch on an sms-SM partition (0 = whole GPU)
+cudaError_t decode_fused(DecFusedState* st, const DecFusedRun& r, int sms, cudaStream_t s);
+
 // keys[r] -> out_tok[r], last_tok[rows[r].slot] (or last_tok[single_slot]); keys reset to 0
 cudaError_t argmax_finalize(unsigned long long* keys, int n, int* out_tok, const DecodeRow* rows, int* last_tok,
                             int single_slot, cudaStream_t s);

@@ -149,9 +149,15 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   w.logits = (float*)take(B * V * 4);
   const size_t nch = (max_ctx + 255) / 256;
   const size_t nparts = std::max(nch, (size_t)(max_ctx + 127) / 128 * 4);  // >= 128-key chunks of the fused kernel  // decode attention partials per head
-  w.attn_ws = (float*)take(B * m.llm_heads * nparts * (m.head_dim + 2) * 4);
+  // >= the fused decode's chunk partials: B x KV x ceil((max_ctx + 1) / 128) x (32 + (H / KV) hd)
+  const size_t fused_parts = B * m.llm_kv_heads * ((max_ctx + 1 + 127) / 128) * (32 + (size_t)(m.llm_heads / m.llm_kv_heads) * m.head_dim);
+  w.attn_ws = (float*)take(std::max(B * m.llm_heads * nparts * (m.head_dim + 2), fused_parts) * 4);
   w.gemv_ws = (float*)take((size_t)16 * B * std::max(std::max(D, F), (size_t)d.llm_qkv_n) * 4);
   w.tickets = (int*)take(8192 * 4);
+  w.qkvf = (float*)take(B * d.llm_qkv_n * 4);
+  w.ss = (float*)take(B * ((D / 64 + 3) / 4 * 4) * 4);
+  w.xlo = (bf16*)take(B * D * 2);
+  w.bar = (unsigned long long*)take(512 * 8);  // per-phase counters of the fused decode kernel
   w.rows = (DecodeRow*)take(B * sizeof(DecodeRow));
   w.tok = (int*)take(B * 4);
   w.keys = (unsigned long long*)take(B * 8);

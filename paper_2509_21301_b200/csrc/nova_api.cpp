@@ -215,6 +215,33 @@ nova_status nova_debug_logits(nova_engine* e, uint64_t id, int32_t index, float*
   return NOVA_OK;
 }
 
+nova_status nova_debug_read_buffer(nova_engine* e, const char* name, void* out, uint64_t bytes) {
+  if (!e || !name || !out) return NOVA_E_INVAL;
+  Engine& E = e->e;
+  if (E.sim || !E.finalized) return E.fail(NOVA_E_STATE, "no device buffers");
+  const auto& m = E.dims.m;
+  const uint64_t B = E.cfg.max_decode_batch, D = m.llm_dim;
+  const std::string n(name);
+  const void* src = nullptr;
+  uint64_t cap = 0;
+  if (n == "dec_hid") src = E.dw.hid, cap = B * D * 4;
+  else if (n == "dec_xg") src = E.dw.xb, cap = B * D * 2;
+  else if (n == "dec_xlo") src = E.dw.xlo, cap = B * D * 2;
+  else if (n == "dec_qkvf") src = E.dw.qkvf, cap = B * E.dims.llm_qkv_n * 4;
+  else if (n == "dec_attn") src = E.dw.attn, cap = B * m.llm_heads * m.head_dim * 2;
+  else if (n == "dec_act") src = E.dw.act, cap = B * m.llm_ffn * 2;
+  else if (n == "dec_ss") src = E.dw.ss, cap = B * ((D / 64 + 3) / 4 * 4) * 4;
+  else if (n == "dec_dbg") src = E.dw.logits + (size_t)15 * m.vocab, cap = (uint64_t)m.vocab * 4;
+  else if (n == "w_o0") src = E.W.llm[0].o_w, cap = D * m.llm_heads * m.head_dim * 2;
+  else if (n == "w_ob0") src = E.W.llm[0].o_wb, cap = D * m.llm_heads * m.head_dim * 2;
+  else if (n == "w_qkvb0") src = E.W.llm[0].qkv_wb, cap = (uint64_t)E.dims.llm_qkv_n * D * 2;
+  else return NOVA_E_NOTFOUND;
+  if (bytes > cap) return NOVA_E_INVAL;
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return E.fail(NOVA_E_CUDA, "debug read");
+  return NOVA_OK;
+}
+
 nova_status nova_debug_force_tokens(nova_engine* e, uint64_t id, const int32_t* tokens, int32_t n) {
   if (!e || (!tokens && n > 0) || n < 0) return NOVA_E_INVAL;
   Engine& E = e->e;

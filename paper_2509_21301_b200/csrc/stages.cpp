@@ -233,8 +233,49 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
       dw.h_forced[b] = forced[b];
       CUDA_TRY(cudaMemcpyAsync(d_last + rq[b]->slot, dw.h_forced + b, 4, cudaMemcpyHostToDevice, s));
     }
-  CUDA_TRY(embed(W.embed, D, nullptr, dw.rows, d_last, dw.hid, D, B, s));
   bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
+  int l0 = 0, sub0 = 0;  // where the per-op path starts (layer, sub-step)
+  if (dfs) {  // one persistent launch for the whole iteration (decode_fused.cu)
+    const size_t wbytes = ((size_t)m.llm_layers * ((size_t)ldq * D + (size_t)D * H * hd + 3 * (size_t)F * D) +
+                           (size_t)m.vocab * D) * 2;
+    const double bytes = (double)wbytes + kv_bytes_layer * m.llm_layers;
+    pass_work[1] = bytes;
+    DecFusedRun fr{};
+    fr.L = m.llm_layers, fr.D = D, fr.H = H, fr.KV = KV, fr.hd = hd, fr.F = F, fr.V = m.vocab, fr.B = B;
+    fr.max_ctx = max_ctx, fr.eps = m.rms_eps, fr.theta = m.llm_theta;
+    fr.embed = W.embed, fr.final_norm = W.final_norm, fr.lm_wb = W.lm_head_b;
+    fr.hid = dw.hid, fr.xg = dw.xb, fr.xlo = dw.xlo, fr.qkvf = dw.qkvf, fr.attn = dw.attn, fr.act = dw.act;
+    fr.ss = dw.ss, fr.logits = dw.logits, fr.keys = dw.keys, fr.ws = dw.gemv_ws, fr.tickets = dw.tickets;
+    fr.aws = dw.attn_ws, fr.atk = dw.tickets + 4096, fr.bar = dw.bar, fr.bar_base = dec_bar_base;
+    fr.pool = pool, fr.n_pages = cfg.kv_pages, fr.max_pages = max_pages_per_req, fr.bt = d_bt, fr.rows = dw.rows;
+    fr.last_tok = d_last, fr.tok_out = dw.tok, fr.store_logits = cfg.debug_keep_logits;
+    fr.mch = (s_max_of_public() + cfg.max_gen + 1 + decode_fused_phase_chunk() - 1) / decode_fused_phase_chunk();
+    // debug bisection (env NOVA_DEC_FUSED_STOP = k): the fused kernel runs phases < k (0 embed,
+    // 1 + 5 l + {0 qkv, 1 attention, 2 o, 3 gate|up, 4 down}, 5 L + 1 lm_head), the per-op path
+    // finishes the iteration from there (k = 1 + 5 l + {0, 2, 3, 4} or 5 L + 1)
+    static const int stop = getenv("NOVA_DEC_FUSED_STOP") ? atoi(getenv("NOVA_DEC_FUSED_STOP")) : 0;
+    fr.ph_end = stop;
+    const int i = ktimer[1].begin(s);
+    CUDA_TRY(decode_fused(dfs, fr, sms, s));
+    ktimer[1].end(i, NOVA_K_DEC_FUSED, bytes, s);
+    dec_bar_base += (unsigned long long)decode_fused_grid(sms);  // every phase counter gains one arrival per CTA
+    static const int halt = getenv("NOVA_DEC_FUSED_HALT") ? atoi(getenv("NOVA_DEC_FUSED_HALT")) : 0;
+    if (halt) {  // debug: stop the engine right after the (partial) fused kernel, buffers intact
+      CUDA_TRY(cudaStreamSynchronize(s));
+      return cudaErrorNotReady;
+    }
+    if (stop <= 0) {
+      CUDA_TRY(cudaMemcpyAsync(dw.h_tok, dw.tok, B * sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (cfg.debug_keep_logits)
+        CUDA_TRY(cudaMemcpyAsync(dw.h_logits, dw.logits, (size_t)B * m.vocab * 4, cudaMemcpyDeviceToHost, s));
+      return cudaSuccess;
+    }
+    l0 = stop > 5 * m.llm_layers ? m.llm_layers : (stop - 1) / 5;
+    sub0 = stop > 5 * m.llm_layers ? 0 : (stop - 1) % 5;
+    if (sub0 == 1) return cudaErrorInvalidValue;  // the per-op path cannot resume at attention
+  } else {
+    CUDA_TRY(embed(W.embed, D, nullptr, dw.rows, d_last, dw.hid, D, B, s));
+  }
   GemvAux plain;
   GemvAux qa;  // RMSNorm(ln1) on load; bias + RoPE + KV append epilogue
   qa.eps = m.rms_eps;
@@ -255,10 +296,12 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
   // faster on slices, level on the full GPU; 2B's 2.4 M o-proj is faster on the register GEMV).
   const int tm = g_dec_tma_mask >= 0 ? g_dec_tma_mask : (28 | ((size_t)D * H * hd >= (size_t)8 << 20 ? 2 : 0));
   const bool rope_tma = (tm & 1) && hd == 128;
-  for (int l = 0; l < m.llm_layers; ++l) {
+  for (int l = l0; l < m.llm_layers; ++l) {
     const LlmLayerW& L = W.llm[l];
     qa.gamma = L.ln1;
     qa.layer = l;
+    const int sub = l == l0 ? sub0 : 0;
+    if (sub > 0) goto resume;
     if (rope_tma) {
       CUDA_TRY(rmsnorm(dw.hid, D, L.ln1, dw.xb, 0, D, B, D, m.rms_eps, s));
       CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.qkv_w, L.qkv_wb, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV, sms,
@@ -274,12 +317,16 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
                            dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
       ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
     }
+  resume:
+    if (sub <= 2) {
     if (tm & 2)
       CUDA_TRY(t_gemv_tma(this, dw.attn, H * hd, L.o_w, L.o_wb, D, H * hd, dw.hid, D, nullptr, B, EPI_F32_RESID, sms,
                           nullptr, s));
     else
       CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.attn, 0, H * hd, L.o_w, D, H * hd, dw.hid, D, nullptr, B,
                       EPI_F32_RESID, plain, s));
+    }
+    if (sub <= 3) {
     if (tm & 4) {
       CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
       CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.gu_w, L.gu_wb, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL, sms,
@@ -290,6 +337,7 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
       na.eps = m.rms_eps;
       CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.hid, 2, D, L.gu_w, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL,
                       na, s));
+    }
     }
     if (tm & 8)
       CUDA_TRY(t_gemv_tma(this, dw.act, F, L.down_w, L.down_wb, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, sms,

@@ -22,10 +22,10 @@ EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
 BACKEND_GPU, BACKEND_SIM = 0, 1
 # NOVA_K_* classes (nova.h) and the unit of their algorithmic work
 KERNEL_CLASSES = ["dec_gemv", "vit_gemm", "llm_gemm", "vit_attn", "pre_attn", "dec_attn", "lm_head", "vit_pass",
-                  "pre_pass", "dec_pass"]
+                  "pre_pass", "dec_pass", "dec_fused"]
 KERNEL_UNITS = {"dec_gemv": "bytes", "vit_gemm": "flops", "llm_gemm": "flops", "vit_attn": "flops",
                 "pre_attn": "flops", "dec_attn": "bytes", "lm_head": "bytes", "vit_pass": "flops",
-                "pre_pass": "flops", "dec_pass": "bytes"}
+                "pre_pass": "flops", "dec_pass": "bytes", "dec_fused": "bytes"}
 
 
 class NovaError(RuntimeError):
@@ -231,6 +231,12 @@ class Engine:
         self._check(self.lib.nova_time_pass(self.h, stage, s, gh, gw, n_prompt, B, ctx, corun, iters, out),
                     "nova_time_pass")
         return out[0], out[1]
+
+    def debug_read_buffer(self, name: str, nbytes: int) -> bytes:
+        """Raw bytes of an internal decode workspace buffer (nova_debug_read_buffer)."""
+        buf = C.create_string_buffer(nbytes)
+        self._check(self.lib.nova_debug_read_buffer(self.h, name.encode(), buf, nbytes), "nova_debug_read_buffer")
+        return buf.raw
 
     def kernel_timing(self, every_n: int) -> None:
         self._check(self.lib.nova_kernel_timing(self.h, every_n), "nova_kernel_timing")

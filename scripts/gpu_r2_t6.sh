@@ -1,0 +1,7 @@
+#!/bin/bash
+timeout 300 python tests/dbg_fused.py 0 2>&1 | grep -a stop
+for cfg in 0 1 2 3; do for s in 0 32; do
+NOVA_DEC_CFG=$cfg timeout 300 python scripts/fd_timeline.py --model 2b --s $s 2>&1 | grep "^{" | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); print('cfg=$cfg', 's=$s', d['ms'], json.dumps(d['last_layer_span_us']))"
+done; done

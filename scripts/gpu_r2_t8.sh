@@ -1,0 +1,7 @@
+#!/bin/bash
+timeout 300 python tests/dbg_fused.py 0 2>&1 | grep -a stop
+for dbg in 4 20; do for s in 0 32; do
+NOVA_DEC_FUSED_DBGX=$dbg timeout 300 python scripts/fd_timeline.py --model 2b --s $s 2>&1 | grep "^{" | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); print('dbg=$dbg', 's=$s', d['ms'], json.dumps(d['last_layer_span_us']))"
+done; done

@@ -1,0 +1,64 @@
+"""Fused persistent decode-iteration kernel (csrc/decode_fused.cu, env NOVA_DEC_FUSED=1).
+
+Experimental path (default off; DESIGN.md §11 has the measurements): the whole decode iteration
+ in one launch.  Checked here against the CPU oracle (cfg T end to end,
+greedy tokens identical, logits within BASELINE's 3e-2) and for bitwise invariance under SM
+partitioning (SERIAL on all SMs vs STATIC splits), in subprocesses so the env switch takes effect.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, os, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+from synth import TINY, gen_weights, tiny_request
+from oracle import vlm as V
+from paper_2509_21301_b200 import engine as E
+seed = json.load(open(os.path.join(%(root)r, "tests", "golden", "tiny_seed.json")))["seed"]
+bits = gen_weights(TINY, seed)
+req = tiny_request(TINY, seed)
+ref = V.generate(V.OracleWeights(bits, np.float32), req.pixels, req.prompt_ids, req.gen_len, TINY)
+out = {}
+for name, mode, kw in [("serial", E.SERIAL, {}), ("static16", E.STATIC, dict(sm_decode_dv=16, sm_decode_dp=16)),
+                       ("static64", E.STATIC, dict(sm_decode_dv=64, sm_decode_dp=64))]:
+    eng = E.Engine(TINY, E.EngineOptions(max_requests=4, kv_pages=16, max_patches=64, max_prompt=16, max_gen=16,
+                                         debug_keep_logits=1))
+    eng.load_weights(bits)
+    eng.finalize()
+    eng.set_partition(mode, **kw)
+    rids = [eng.submit(req.pixels, req.prompt_ids, req.gen_len) for _ in range(2)]
+    done = 0
+    while done < 2:
+        done = eng.step(2000).finished
+    toks = {r: [t for _, t in sorted((i, t) for q, i, t, _, _ in eng.poll_tokens() if q == r)] for r in rids}
+    lg = np.stack([eng.debug_logits(rids[0], k) for k in range(req.gen_len)])
+    out[name] = {"tokens": toks[rids[0]], "tokens2": toks[rids[1]], "logits": lg.tobytes().hex(),
+                 "err": float(np.abs(lg - ref["logits"]).max())}
+    eng.close()
+out["ref_tokens"] = ref["tokens"].tolist()
+print("RESULT " + json.dumps(out))
+"""
+
+
+@pytest.mark.gpu
+def test_fused_decode_kernel_matches_oracle_and_is_partition_invariant():
+    env = dict(os.environ, NOVA_DEC_FUSED="1")
+    r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT}], env=env, capture_output=True, text=True,
+                       timeout=600)
+    line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
+    assert line, r.stdout[-2000:] + r.stderr[-2000:]
+    out = json.loads(line[0][7:])
+    for name in ("serial", "static16", "static64"):
+        assert out[name]["tokens"] == out["ref_tokens"], name
+        assert out[name]["tokens2"] == out["ref_tokens"], name
+        assert out[name]["err"] <= 3e-2, (name, out[name]["err"])
+    # bitwise: the same logits on every partition (the fused kernel's reduction orders are shape-only)
+    assert out["static16"]["logits"] == out["serial"]["logits"]
+    assert out["static64"]["logits"] == out["serial"]["logits"]
