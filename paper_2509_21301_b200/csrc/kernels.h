@@ -85,6 +85,16 @@ cudaError_t gemv_tma(const bf16* X, int ldx, const bf16* W, int N, int K, void* 
                      int epi, float* ws, int* tickets, cudaStream_t s, int max_ctas = 0,
                      const GemvAux* aux = nullptr, const bf16* W_blocked = nullptr, const bf16* X_lo = nullptr);
 extern bool g_use_tma_gemv;
+// Decode GEMV on tcgen05 (gemv_umma.cu): weights (streaming layout) as the M = 128 operand, x as
+// N = 16; one thread issues the MMAs and tcgen05.commit releases each ring stage.  Same contract as
+// gemv_tma (shape-only split plan, bitwise grid / batch invariant); epilogues BF16, SILUMUL,
+// F32_RESID, F32_STORE, F32_ARGMAX (X_lo required: f32 x as hi + lo).  sms = partition budget.
+extern int g_dec_umma;  // env NOVA_DEC_UMMA (default 1): decode linears on gemv_umma where supported
+GemvTmaPlan gemv_umma_plan(int N, int K, int epi);
+bool gemv_umma_supported(int N, int K, int epi);
+cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int K, void* Y, int ldy, const bf16* bias,
+                      int B, int epi, float* ws, int* tickets, cudaStream_t s, int sms, unsigned long long* keys,
+                      const bf16* X_lo);
 extern int g_dec_tma_mask;  // decode linears on the persistent TMA GEMV: bit 0 qkv, 1 o, 2 gate|up, 3 down, 4 lm_head
 
 // Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).

@@ -80,6 +80,13 @@ int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_
   return st(gemv_tma((const bf16*)X, ldx, nullptr, N, K, Y, ldy, (const bf16*)bias, B, epi, ws, tickets, S(stream),
                      max_ctas, &a, (const bf16*)W_blocked, (const bf16*)X_lo));
 }
+int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
+                      const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
+                      void* stream) {
+  return st(gemv_umma((const bf16*)X, ldx, (const bf16*)W_blocked, N, K, Y, ldy, (const bf16*)bias, B, epi, ws,
+                      tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo));
+}
+int nova_op_gemv_umma_splits(int N, int K, int epi) { return gemv_umma_plan(N, K, epi).P; }
 int nova_op_argmax_finalize(uint64_t* keys, int n, int32_t* out_tok, const nova_decode_row* rows, int32_t* last_tok,
                             int single_slot, void* stream) {
   return st(argmax_finalize((unsigned long long*)keys, n, out_tok, (const DecodeRow*)rows, last_tok, single_slot,

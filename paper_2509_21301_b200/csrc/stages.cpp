@@ -6,6 +6,7 @@
 // ALGORITHMIC work to the pass total and, on sampled passes, bracket it with CUDA
 // events on its own stream (live roofline numbers, nova_kernel_stats).
 #include <algorithm>
+#include <cstdlib>
 
 #include "engine.h"
 
@@ -85,7 +86,20 @@ static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, 
   const double bytes = (double)N * K * 2 + (double)B * K * (X_lo ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms, aux, Wb, X_lo));
+  // which linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 1 o, 2 gate|up, 3 down,
+  // 4 lm_head); the choice depends on the op only, never on the partition (bitwise co-execution)
+  // Default gate|up + lm_head (scripts/gpu_r2_u3.sh, decode iterations on 24..148-SM partitions: 2B
+  // 3.25 -> 3.12 ms on 24 SMs, 1.79 -> 1.71 on 64, level on the full GPU; down / o on tcgen05 win
+  // on <= 48-SM slices but lose 10-25% on larger grids, which decode also runs on).
+  static const int umask = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 20;
+  const int op_bit = epi == EPI_BF16_SILUMUL ? 4 : epi == EPI_F32_ARGMAX ? 16 : (K > N ? 8 : 2);
+  if (g_dec_umma && (umask & op_bit) && Wb && gemv_umma_supported(N, K, epi) && (epi != EPI_F32_ARGMAX || X_lo)) {
+    // tcgen05 consumer (gemv_umma.cu): the same contract, the ring stage released by the MMA commit
+    CUDA_TRY(gemv_umma(X, ldx, Wb, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms,
+                       aux ? aux->keys : nullptr, X_lo));
+  } else {
+    CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms, aux, Wb, X_lo));
+  }
   E->ktimer[1].end(i, cls, bytes, s);
   return cudaSuccess;
 }

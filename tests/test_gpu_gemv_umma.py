@@ -1,0 +1,105 @@
+"""Decode GEMV on tcgen05 (csrc/gemv_umma.cu) through the C ABI (include/nova_ops.h
+nova_op_gemv_umma) vs the oracle's ops (oracle/vlm.py linear / rms_norm / silu / argmax_lowest):
+
+* f32-store epilogue within 1e-4 (rel-inf) of the fp64 oracle linear on the same bf16 inputs, at
+  the 2B / 7B decode shapes and a tiny one (split and unsplit K plans);
+* bitwise invariance to the SM budget (the partition) -- whole-block and split units alike -- and
+  to the batch composition (row 0 alone == row 0 of a batch of 16);
+* SiLU(gate) * up over the interleaved gate|up rows, residual add, and the hi/lo lm_head with
+  the fused greedy argmax (exact token, keys left zero).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import vlm as V
+from tests.gpu_util import bf16_dev, bf16_host, rand_bf16, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2509_21301_b200 import ops as O
+
+
+def _blocked(W, N, K):
+    dW = bf16_dev(W)
+    Wb = torch.empty_like(dW)
+    O.nova_op_block_weights(dW, Wb, N, K)
+    return Wb
+
+
+@pytest.mark.parametrize("N,K", [(17920, 1536), (1536, 8960), (2048, 1536), (37888, 3584), (3584, 18944),
+                                 (256, 128), (768, 128)])
+def test_umma_gemv_matches_oracle_and_is_grid_and_batch_invariant(N, K):
+    rng = np.random.default_rng(3 * N + K)
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    X = rand_bf16(rng, (16, K))
+    Wb = _blocked(W, N, K)
+    dX = bf16_dev(X)
+    ref = V.linear(X.astype(np.float64), W.astype(np.float64))
+    Y16 = None
+    for B in (16, 1, 9):
+        Y0 = torch.empty(B, N, dtype=torch.float32, device="cuda")
+        O.nova_op_gemv_umma(dX[:B], Wb, Y0, None, N, K, B, O.EPI_F32_STORE)
+        torch.cuda.synchronize()
+        assert rel_inf(Y0.cpu().numpy(), ref[:B]) <= 1e-4, B
+        if Y16 is None:
+            Y16 = Y0
+        else:
+            assert torch.equal(Y0[0], Y16[0]), B          # batch invariance of row 0
+        for ctas in (148, 40, 24, 8):                       # whole-block units first on small grids
+            Y1 = torch.empty_like(Y0)
+            O.nova_op_gemv_umma(dX[:B], Wb, Y1, None, N, K, B, O.EPI_F32_STORE, max_ctas=ctas)
+            torch.cuda.synchronize()
+            assert torch.equal(Y0, Y1), (B, ctas)
+
+
+def test_umma_gemv_silu_and_residual_epilogues():
+    rng = np.random.default_rng(11)
+    F, D, B = 8960, 1536, 5
+    G = rand_bf16(rng, (F, D), D ** -0.5)
+    U = rand_bf16(rng, (F, D), D ** -0.5)
+    Wgu = np.empty((2 * F, D), dtype=np.float32)         # interleave 16 gate | 16 up rows (engine layout)
+    for i in range(F // 16):
+        Wgu[32 * i:32 * i + 16] = G[16 * i:16 * i + 16]
+        Wgu[32 * i + 16:32 * i + 32] = U[16 * i:16 * i + 16]
+    X = rand_bf16(rng, (B, D))
+    Wb = _blocked(Wgu, 2 * F, D)
+    act = torch.empty(B, F, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_gemv_umma(bf16_dev(X), Wb, act, None, 2 * F, D, B, O.EPI_BF16_SILUMUL, max_ctas=32)
+    torch.cuda.synchronize()
+    x64 = X.astype(np.float64)
+    ref = V.silu(V.linear(x64, G.astype(np.float64))) * V.linear(x64, U.astype(np.float64))
+    assert rel_inf(bf16_host(act), ref) <= 8e-3
+    # residual: Y += X W^T (f32)
+    Wd = rand_bf16(rng, (D, F), F ** -0.5)
+    Xa = rand_bf16(rng, (B, F))
+    base = rng.standard_normal((B, D)).astype(np.float32)
+    Y = torch.from_numpy(base.copy()).cuda()
+    O.nova_op_gemv_umma(bf16_dev(Xa), _blocked(Wd, D, F), Y, None, D, F, B, O.EPI_F32_RESID, max_ctas=24)
+    torch.cuda.synchronize()
+    ref2 = base.astype(np.float64) + V.linear(Xa.astype(np.float64), Wd.astype(np.float64))
+    assert rel_inf(Y.cpu().numpy(), ref2) <= 1e-4
+
+
+def test_umma_lm_head_hi_lo_argmax():
+    rng = np.random.default_rng(78)
+    V_, D, B = 151936, 1536, 3
+    W = rand_bf16(rng, (V_, D), 2 * D ** -0.5)
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    gam = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (D,), 0.1) + 1.0))
+    Xh = (rng.standard_normal((B, D)) * 2).astype(np.float32)
+    Wb = _blocked(W, V_, D)
+    hl = torch.empty(2 * B, D, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_rmsnorm(torch.from_numpy(Xh).cuda(), bf16_dev(gam), hl, B, D, 1e-6, y_mode=2)
+    keys = torch.zeros(B, dtype=torch.int64, device="cuda")
+    L = torch.empty(B, V_, dtype=torch.float32, device="cuda")
+    O.nova_op_gemv_umma(hl[:B], Wb, L, None, V_, D, B, O.EPI_F32_ARGMAX, X_lo=hl[B:], keys=keys, max_ctas=32)
+    tok = torch.empty(B, dtype=torch.int32, device="cuda")
+    O.nova_op_argmax_finalize(keys, B, tok)
+    torch.cuda.synchronize()
+    lg = L.cpu().numpy()
+    ref = V.linear(V.rms_norm(Xh.astype(np.float64), gam, 1e-6), W.astype(np.float64))
+    assert rel_inf(lg, ref) <= 1e-4
+    assert tok.cpu().numpy().tolist() == [V.argmax_lowest(lg[b]) for b in range(B)]
+    assert int(keys.abs().sum().item()) == 0
