@@ -34,10 +34,13 @@ for name, mode, kw in [("serial", E.SERIAL, {}), ("static16", E.STATIC, dict(sm_
     eng.finalize()
     eng.set_partition(mode, **kw)
     rids = [eng.submit(req.pixels, req.prompt_ids, req.gen_len) for _ in range(2)]
-    done = 0
-    while done < 2:
-        done = eng.step(2000).finished
-    toks = {r: [t for _, t in sorted((i, t) for q, i, t, _, _ in eng.poll_tokens() if q == r)] for r in rids}
+    got = []
+    for _ in range(2000):
+        eng.step(2000)
+        got += eng.poll_tokens()
+        if sum(1 for x in got if x[0] in rids) >= 2 * req.gen_len:
+            break
+    toks = {r: [t for _, t in sorted((i, t) for q, i, t, _, _ in got if q == r)] for r in rids}
     lg = np.stack([eng.debug_logits(rids[0], k) for k in range(req.gen_len)])
     out[name] = {"tokens": toks[rids[0]], "tokens2": toks[rids[1]], "logits": lg.tobytes().hex(),
                  "err": float(np.abs(lg - ref["logits"]).max())}
