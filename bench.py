@@ -553,7 +553,10 @@ def main():
                 # the paper's baselines: prefill-first with decode threshold 5, and
                 # co-running stages with no SM partition (both streams see every SM)
                 ("pf_limit_5", dict(mode=E.PF_LIMIT, pf_threshold=5, b_max=16)),
-                ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16))]
+                ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16)),
+                # the paper's chunked-prefill baseline: hybrid prefill-chunk + decode batches,
+                # token budget 128 (the paper's best)
+                ("chunk_128", dict(mode=E.CHUNK, chunk_budget=128, b_max=16))]
         if plan.get("points"):   # Pareto point for the estimated arrival rate
             pols.append(("frontier", dict(mode=E.FRONTIER, b_max=16)))
         if kind == "poisson":    # cfg 2: the static SM-split sweep

@@ -131,9 +131,16 @@ nova_status nova_submit(nova_engine* e, const nova_request* r, uint64_t* req_id)
  *   rule, each co-run pass takes the Pareto point (nova_set_frontier) with the lowest Eq. 1
  *   E2E among those whose Eq. 4 throughput covers the estimated arrival rate (the last
  *   `window` arrivals); if none does, the highest-throughput point (P:356 -- the frontier is
- *   the paper's justification for Eq. 5). */
+ *   the paper's justification for Eq. 5).
+ * CHUNK: the paper's chunked-prefill baseline "Chunk" (Sarathi-style hybrid batching,
+ *   token budget chunk_budget, the paper's best 128): one pass at a time on all SMs; an LLM step
+ *   is a HYBRID iteration = the next min(remaining, chunk_budget - B) prefill tokens of the
+ *   request in chunked prefill + the current decode batch (B requests) in one batch; vision
+ *   encode cannot join the batch (separate weights) and runs as its own pass, alternating
+ *   with LLM steps (R26).  The prefill token (index 0) is emitted by the last chunk. */
 enum { NOVA_MODE_SERIAL = 0, NOVA_MODE_STATIC = 1, NOVA_MODE_ADAPTIVE = 2, NOVA_MODE_PF_LIMIT = 3,
-       NOVA_MODE_MULTI_STREAM = 4, NOVA_MODE_FRONTIER = 5 };
+       NOVA_MODE_MULTI_STREAM = 4, NOVA_MODE_FRONTIER = 5, NOVA_MODE_CHUNK = 6 };
+#define NOVA_CHUNK_MAX 256  /* largest chunk_budget (hybrid workspace rows = NOVA_CHUNK_MAX + 16) */
 enum { NOVA_CTX_DV = 0, NOVA_CTX_DP = 1, NOVA_CTX_SOLO = 2 };
 typedef struct {
   int32_t mode;                        /* NOVA_MODE_*                                           */
@@ -145,6 +152,8 @@ typedef struct {
   int32_t sm_dv_floor;                 /* ADAPTIVE / FRONTIER: decode SMs never below this while
                                           co-running with vision (offload-aware, see
                                           nova_offload_floor); 0 = none                       */
+  int32_t chunk_budget;                /* CHUNK: tokens per hybrid iteration (<= 0: 128;
+                                          <= NOVA_CHUNK_MAX)                                  */
 } nova_partition_policy;
 /* Takes effect at each role's next forward pass.  `applied` (may be NULL)
  * receives the values rounded down to the granularity.  NOVA_E_PARTITION if a
@@ -191,8 +200,11 @@ nova_status nova_request_stats(nova_engine* e, uint64_t req_id, nova_req_stats* 
 nova_status nova_release_request(nova_engine* e, uint64_t req_id);
 
 /* Decision log of Algorithm 1 (for replay against the oracle). */
-enum { NOVA_DEC_VISION = 0, NOVA_DEC_PREFILL = 1, NOVA_DEC_DECODE = 2, NOVA_DEC_FINISH = 3 };
-enum { NOVA_EV_VISION_DONE = 0, NOVA_EV_PREFILL_DONE = 1, NOVA_EV_DECODE_DONE = 2, NOVA_EV_ARRIVAL = 3 };
+/* NOVA_DEC_HYBRID (CHUNK mode): ids[0] = the request in chunked prefill, ids[1..] = the decode
+ * batch; s_dec = the chunk's prefill token count (the pass itself runs on all SMs). */
+enum { NOVA_DEC_VISION = 0, NOVA_DEC_PREFILL = 1, NOVA_DEC_DECODE = 2, NOVA_DEC_FINISH = 3, NOVA_DEC_HYBRID = 4 };
+enum { NOVA_EV_VISION_DONE = 0, NOVA_EV_PREFILL_DONE = 1, NOVA_EV_DECODE_DONE = 2, NOVA_EV_ARRIVAL = 3,
+       NOVA_EV_HYBRID_DONE = 4 };
 typedef struct {
   int64_t t_ns;
   int32_t tick;      /* tick sequence number                                     */

@@ -31,22 +31,31 @@ Readings (R13-R17):
   * FRONTIER: co-run like ADAPTIVE, but the decode split of a
     co-run pass is the Pareto point picked for the arrival rate estimated over the
     last lam_window arrivals (planner.frontier_pick), instead of Eq. 5.
+  * CHUNK (the paper's chunked-prefill baseline: "splits a LLM prefill request into
+    several chunks and batches these chunks with LLM decode requests", token budget 128).
+    Reading (R26): one pass at a time on all SMs; an LLM step is a HYBRID pass
+    = the next min(remaining, budget - B) prefill tokens of the request in chunked prefill
+    (FIFO from the prefill queue) + the decode batch (B requests); with no prefill in progress
+    a plain decode pass.  Vision encode cannot join a batch (separate weights): it runs
+    as its own pass, alternating with LLM steps when both are ready, and only while no encoded
+    request waits for its first chunk.  The last chunk emits the prefill token.
 The same state machine drives `simulate` (virtual time, durations from curves),
 which checks the worked example of SURVEY.md §8(c) c6 by hand values.
 """
 from __future__ import annotations
 
+import math
 from collections import deque
 from dataclasses import dataclass, field
 
 from .planner import adaptive_sm, arrival_rate, frontier_pick
 
-SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, FRONTIER = 0, 1, 2, 3, 4, 5
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, FRONTIER, CHUNK = 0, 1, 2, 3, 4, 5, 6
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 # event kinds (order = tie-break class: completions first)
-EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
+EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL, EV_HYBRID_DONE = 0, 1, 2, 3, 4
 # decision kinds
-D_VISION, D_PREFILL, D_DECODE, D_FINISH = 0, 1, 2, 3
+D_VISION, D_PREFILL, D_DECODE, D_FINISH, D_HYBRID = 0, 1, 2, 3, 4
 
 
 @dataclass
@@ -66,6 +75,7 @@ class Policy:
     frontier: list = field(default_factory=list)   # FRONTIER: (s_v, s_p, e2e, thr) Pareto points
     lam_window: int = 16        # FRONTIER: arrivals in the rate estimate
     sm_dv_floor: int = 0        # offload-aware floor of the decode split while vision co-runs (f3)
+    chunk_budget: int = 128     # CHUNK: tokens per hybrid pass
 
 
 @dataclass
@@ -74,6 +84,9 @@ class Req:
     gen_len: int
     emitted: int = 0
     join_seq: int = -1
+    S: int = 1                  # LLM prefill tokens (n_v + prompt); CHUNK mode
+    pre_done: int = 0           # CHUNK: prefill tokens of finished hybrid passes
+    chunk_n: int = 0            # CHUNK: tokens of the hybrid pass in flight
 
 
 class Alg1:
@@ -91,6 +104,7 @@ class Alg1:
         self.join_counter = 0
         self.last_pass = None               # SERIAL alternation
         self.arr_t: deque[int] = deque(maxlen=max(2, policy.lam_window))   # FRONTIER rate estimate
+        self.chunk_req: int | None = None   # CHUNK: the request in chunked prefill
         self.log: list[tuple] = []
 
     # -- Eq. 5 / static split for a co-run context
@@ -110,7 +124,7 @@ class Alg1:
 
     def n_pend(self) -> int:
         return (len(self.q_v) + (self.vision_running is not None) + len(self.prefill_wait)
-                + (self.prefill_running is not None))
+                + (self.prefill_running is not None) + (self.chunk_req is not None))
 
     def front_running(self) -> bool:
         return self.vision_running is not None or self.prefill_running is not None
@@ -134,8 +148,8 @@ class Alg1:
         else:
             self._decode_ready(rid)
 
-    def add_request(self, rid: int, gen_len: int):
-        self.reqs[rid] = Req(rid, gen_len)
+    def add_request(self, rid: int, gen_len: int, S: int = 1):
+        self.reqs[rid] = Req(rid, gen_len, S=S)
 
     def tick(self, events: list[tuple]) -> list[tuple]:
         """events: (kind, key, payload[, t_ns]) -- payload rid (or list of rids for DECODE_DONE);
@@ -160,8 +174,20 @@ class Alg1:
                 self.last_pass = "decode"
                 for rid in payload:
                     self._emit(rid, out)
+            elif kind == EV_HYBRID_DONE:      # payload[0]: the chunked prefill, payload[1:]: decode rows
+                self.decode_running = None
+                self.last_pass = "decode"
+                r = self.reqs[payload[0]]
+                r.pre_done += r.chunk_n
+                if r.pre_done >= r.S:
+                    self.chunk_req = None
+                    self._emit(payload[0], out)
+                for rid in payload[1:]:
+                    self._emit(rid, out)
         npend = self.n_pend()
-        if self.p.mode == SERIAL:
+        if self.p.mode == CHUNK:
+            self._dispatch_chunk(out)
+        elif self.p.mode == SERIAL:
             self._dispatch_serial(out)
         elif self.p.mode == PF_LIMIT:
             self._dispatch_pf_limit(out)
@@ -215,6 +241,31 @@ class Alg1:
         elif front_ready:
             self._dispatch_front(out, lambda c: (CTX_SOLO, 0))
 
+    def _dispatch_chunk(self, out):
+        if self.vision_running is not None or self.decode_running is not None:
+            return
+        llm_ready = self.chunk_req is not None or bool(self.prefill_wait) or bool(self.q_d)
+        vis_ready = bool(self.q_v) and not self.prefill_wait
+        if vis_ready and (not llm_ready or self.last_pass == "decode"):
+            rid = self.q_v.popleft()
+            self.vision_running = rid
+            out.append((D_VISION, (rid,), CTX_SOLO, 0))
+            return
+        if not llm_ready:
+            return
+        if self.chunk_req is None and self.prefill_wait:
+            self.chunk_req = self.prefill_wait.popleft()
+        batch = self.q_d[: self.p.b_max]
+        self.q_d = self.q_d[self.p.b_max:]
+        if self.chunk_req is not None:
+            r = self.reqs[self.chunk_req]
+            r.chunk_n = min(r.S - r.pre_done, max(1, self.p.chunk_budget - len(batch)))
+            self.decode_running = [self.chunk_req] + batch
+            out.append((D_HYBRID, (self.chunk_req,) + tuple(batch), CTX_SOLO, r.chunk_n))
+        else:
+            self.decode_running = batch
+            out.append((D_DECODE, tuple(batch), CTX_SOLO, self.p.total_sms))
+
     def _dispatch_serial(self, out):
         if self.busy():
             return
@@ -252,13 +303,14 @@ class SimRequest:
     gen_len: int
     vis_scale: float = 1.0
     pre_scale: float = 1.0
+    S: int = 1                  # LLM prefill tokens (CHUNK mode)
 
 
 def simulate(policy: Policy, curves: SimCurves, requests: list[SimRequest]):
     """Run Alg. 1 in virtual integer-ns time.  Returns (decision log, token times per rid)."""
     alg = Alg1(policy)
     for r in requests:
-        alg.add_request(r.rid, r.gen_len)
+        alg.add_request(r.rid, r.gen_len, r.S)
     byid = {r.rid: r for r in requests}
     arrivals = sorted(requests, key=lambda r: (r.arrival_ns, r.rid))
     ai = 0
@@ -285,6 +337,12 @@ def simulate(policy: Policy, curves: SimCurves, requests: list[SimRequest]):
             elif kind == EV_DECODE_DONE:
                 for rid in payload:
                     tokens[rid].append(t)
+            elif kind == EV_HYBRID_DONE:
+                r0 = alg.reqs[payload[0]]
+                if r0.pre_done + r0.chunk_n >= r0.S:     # the last chunk emits the prefill token
+                    tokens[payload[0]].append(t)
+                for rid in payload[1:]:
+                    tokens[rid].append(t)
         for kind, rids, ctx, s in alg.tick(evs):
             if kind == D_FINISH:
                 done += 1
@@ -297,6 +355,12 @@ def simulate(policy: Policy, curves: SimCurves, requests: list[SimRequest]):
                 base = curves.t_p_solo if ctx == CTX_SOLO else curves.t_p[curves.idx(s)]
                 dur = int(round(base * byid[rids[0]].pre_scale))
                 pending.append((t + dur, EV_PREFILL_DONE, rids[0], rids[0]))
+            elif kind == D_HYBRID:   # the chunk's share of the solo prefill + the decode batch
+                nb = len(rids) - 1
+                dd = curves.t_d_solo * (1.0 + curves.beta * (nb - 1)) if nb > 0 else 0.0
+                r0 = byid[rids[0]]
+                dur = int(math.floor(curves.t_p_solo * r0.pre_scale * s / r0.S + dd + 0.5))  # llround (x > 0)
+                pending.append((t + dur, EV_HYBRID_DONE, min(rids), list(rids)))
             else:
                 if ctx == CTX_SOLO:
                     base = curves.t_d_solo

@@ -33,7 +33,7 @@ class Request(C.Structure):
 class PartitionPolicy(C.Structure):
     _fields_ = [("mode", I32), ("sm_decode_dv", I32), ("sm_decode_dp", I32), ("sm_op_dv", I32),
                 ("sm_op_dp", I32), ("sm_min", I32), ("alpha_dv", F32), ("alpha_dp", F32), ("b_max", I32),
-                ("pf_threshold", I32), ("sm_dv_floor", I32)]
+                ("pf_threshold", I32), ("sm_dv_floor", I32), ("chunk_budget", I32)]
 
 
 class StepInfo(C.Structure):

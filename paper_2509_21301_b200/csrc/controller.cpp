@@ -59,7 +59,8 @@ int Alg1::split(int ctx, int n_pend) const {
 }
 
 int Alg1::n_pend() const {
-  return (int)q_v.size() + (vision_running ? 1 : 0) + (int)prefill_wait.size() + (prefill_running ? 1 : 0);
+  return (int)q_v.size() + (vision_running ? 1 : 0) + (int)prefill_wait.size() + (prefill_running ? 1 : 0) +
+         (chunk_req ? 1 : 0);
 }
 
 void Alg1::decode_ready(Request* r) {
@@ -107,6 +108,47 @@ void Alg1::dispatch_decode(std::vector<Decision>& out, int ctx, int s) {
   out.push_back(Decision{NOVA_DEC_DECODE, ctx, s, batch});
 }
 
+// CHUNK (the paper's chunked-prefill baseline; R26): one pass at a time on all SMs.
+// An LLM step is a hybrid iteration: the next min(remaining, budget - B) prefill tokens of the
+// request in chunked prefill (FIFO from the prefill queue) batched with the decode batch (B
+// requests, join order, <= B_max); without a prefill in progress it is a plain decode iteration.
+// Vision encode runs as its own pass (separate weights), alternating with LLM steps when
+// both are ready, and only while no finished encode waits for its first chunk (one E_vis staging).
+void Alg1::dispatch_chunk(std::vector<Decision>& out) {
+  if (vision_running || decode_busy) return;
+  const bool llm_ready = chunk_req || !prefill_wait.empty() || !q_d.empty();
+  const bool vis_ready = !q_v.empty() && prefill_wait.empty();
+  if (vis_ready && (!llm_ready || last_pass == 1)) {
+    Request* r = q_v.front();
+    q_v.pop_front();
+    vision_running = r;
+    out.push_back(Decision{NOVA_DEC_VISION, NOVA_CTX_SOLO, 0, {r}});
+    return;
+  }
+  if (!llm_ready) return;
+  if (!chunk_req && !prefill_wait.empty()) {
+    chunk_req = prefill_wait.front();
+    prefill_wait.pop_front();
+  }
+  const int bmax = std::max(1, pol.b_max);
+  const int n = std::min<int>((int)q_d.size(), bmax);
+  std::vector<Request*> batch(q_d.begin(), q_d.begin() + n);
+  q_d.erase(q_d.begin(), q_d.begin() + n);
+  decode_busy = true;
+  if (chunk_req) {
+    const int budget = pol.chunk_budget > 0 ? pol.chunk_budget : 128;
+    chunk_req->chunk_c0 = chunk_req->pre_done;
+    chunk_req->chunk_n = std::min(chunk_req->S() - chunk_req->pre_done, std::max(1, budget - n));
+    std::vector<Request*> rs{chunk_req};
+    rs.insert(rs.end(), batch.begin(), batch.end());
+    decode_running = rs;
+    out.push_back(Decision{NOVA_DEC_HYBRID, NOVA_CTX_SOLO, chunk_req->chunk_n, rs});
+  } else {
+    decode_running = batch;
+    out.push_back(Decision{NOVA_DEC_DECODE, NOVA_CTX_SOLO, total_sms, batch});
+  }
+}
+
 std::vector<Decision> Alg1::tick(std::vector<Event>& evs) {
   // completions before arrivals, then by request id (R13)
   std::stable_sort(evs.begin(), evs.end(), [](const Event& a, const Event& b) {
@@ -139,10 +181,25 @@ std::vector<Decision> Alg1::tick(std::vector<Event>& evs) {
         last_pass = 1;
         for (Request* r : e.reqs) emit(r, out);
         break;
+      case NOVA_EV_HYBRID_DONE: {  // reqs[0]: the chunked prefill (token 0 after its last chunk)
+        decode_running.clear();
+        decode_busy = false;
+        last_pass = 1;
+        Request* p = e.reqs[0];
+        p->pre_done += p->chunk_n;
+        if (p->pre_done >= p->S()) {
+          chunk_req = nullptr;
+          emit(p, out);
+        }
+        for (size_t i = 1; i < e.reqs.size(); ++i) emit(e.reqs[i], out);
+        break;
+      }
     }
   }
   const int npend = n_pend();
-  if (pol.mode == NOVA_MODE_SERIAL) {
+  if (pol.mode == NOVA_MODE_CHUNK) {
+    dispatch_chunk(out);
+  } else if (pol.mode == NOVA_MODE_SERIAL) {
     if (!front_running() && !decode_busy) {
       const bool front_ready = !prefill_wait.empty() || !q_v.empty();
       const bool dec_ready = !q_d.empty();

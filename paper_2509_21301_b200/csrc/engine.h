@@ -61,6 +61,8 @@ struct Request {
   int emitted = 0;
   int64_t join_seq = -1;
   float sim_vs = 1.f, sim_ps = 1.f;
+  int pre_done = 0;                 // CHUNK: prefill tokens processed by finished hybrid passes
+  int chunk_c0 = 0, chunk_n = 0;    // CHUNK: the chunk of the hybrid pass in flight
   std::vector<int> pages;
   std::vector<int> forced;          // teacher forcing
   std::vector<int> tokens;          // emitted tokens
@@ -89,6 +91,7 @@ struct Alg1 {
   std::deque<Request*> q_v, prefill_wait;
   Request* vision_running = nullptr;
   Request* prefill_running = nullptr;
+  Request* chunk_req = nullptr;  // CHUNK: the request in chunked prefill (its chunks ride on LLM steps)
   std::vector<Request*> decode_running;
   bool decode_busy = false;
   std::vector<Request*> q_d;
@@ -110,6 +113,7 @@ struct Alg1 {
   void decode_ready(Request* r);
   void dispatch_front(std::vector<Decision>& out, bool corun, int npend, bool has_decode);
   void dispatch_decode(std::vector<Decision>& out, int ctx, int s);
+  void dispatch_chunk(std::vector<Decision>& out);
 };
 
 // ------------------------------------------------------------------ partition family
@@ -228,6 +232,16 @@ class Engine {
     int* h_forced;
     float* h_logits;
   } dw{};
+  struct HybWS {  // CHUNK mode: hybrid iterations (prefill chunk rows, then decode rows)
+    float *pre, *hid, *xf, *logits;   // pre: the chunked request's input rows [S_max][D] (E_vis | prompt embeds)
+    bf16 *xb, *qkv, *attn, *act;
+    DecodeRow *rows, *lm_rows;        // per hybrid row (attention / RoPE) and per lm_head row
+    int *pos3, *tok;
+    unsigned long long* keys;
+    DecodeRow *h_rows, *h_lm_rows;    // pinned
+    int *h_pos3, *h_tok, *h_forced;   // pinned
+    float* h_logits;                  // pinned [17][V]
+  } hw{};
   Partition part;
   DecFusedState* dfs = nullptr;     // fused decode kernel state (null: per-op decode path)
   unsigned long long dec_bar_base = 0;  // grid-barrier counter value at the next fused launch
@@ -311,6 +325,9 @@ class Engine {
   // decode SMs of a pass: the whole GPU when SOLO, else the partition's s_dec
   int dec_sms(int ctx, int s_dec) const { return (ctx == NOVA_CTX_SOLO || s_dec <= 0 || s_dec >= part.total) ? part.total : s_dec; }
   cudaError_t run_decode(const std::vector<Request*>& rows, const std::vector<int>& forced, cudaStream_t s, int sms);
+  // CHUNK mode: one hybrid iteration -- reqs[0]'s chunk [chunk_c0, chunk_c0 + chunk_n) of prefill rows
+  // and reqs[1..] as decode rows in one batch; writes hw.h_tok (prefill token first if last chunk)
+  cudaError_t run_hybrid(const std::vector<Request*>& reqs, const std::vector<int>& forced, cudaStream_t s, int sms);
   cudaStream_t stream_for(int role, int ctx, int s_dec);
   int s_max_of_public() const;
   nova_status time_pass(int stage, int s, int gh, int gw, int n_prompt, int B, int ctx, int corun, int iters,

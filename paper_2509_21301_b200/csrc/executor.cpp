@@ -179,6 +179,10 @@ void Worker::run() {
     } else if (c.kind == NOVA_DEC_PREFILL) {
       e = eng->run_prefill(c.reqs[0], s, eng->front_sms(c.s_dec));
       done.kind = NOVA_EV_PREFILL_DONE;
+    } else if (c.kind == NOVA_DEC_HYBRID) {
+      e = eng->run_hybrid(c.reqs, c.forced_tok, s, eng->part.total);
+      done.kind = NOVA_EV_HYBRID_DONE;
+      for (Request* r : c.reqs) done.key = std::min<uint64_t>(done.key, r->id);
     } else {
       e = eng->run_decode(c.reqs, c.forced_tok, s, eng->dec_sms(c.ctx, c.s_dec));
       done.kind = NOVA_EV_DECODE_DONE;
@@ -195,7 +199,9 @@ void Worker::run() {
       float ms = 0;
       cudaEventElapsedTime(&ms, p0, p1);
       const int cls = c.kind == NOVA_DEC_VISION ? NOVA_K_VIT_PASS
-                                                : (c.kind == NOVA_DEC_PREFILL ? NOVA_K_PRE_PASS : NOVA_K_DEC_PASS);
+                                                : ((c.kind == NOVA_DEC_PREFILL || c.kind == NOVA_DEC_HYBRID)
+                                                       ? NOVA_K_PRE_PASS
+                                                       : NOVA_K_DEC_PASS);
       {
         std::lock_guard<std::mutex> g(eng->kmu);
         eng->kstats[cls].ms += ms;
@@ -217,6 +223,13 @@ void Worker::run() {
           done.tokens.push_back(eng->dw.h_tok[b]);
           if (eng->cfg.debug_keep_logits)
             c.reqs[b]->logits.emplace_back(eng->dw.h_logits + b * V, eng->dw.h_logits + (b + 1) * V);
+        }
+      } else if (c.kind == NOVA_DEC_HYBRID) {  // hw.h_tok[0]: the prefill token (last chunk); [1..]: decode rows
+        for (size_t b = 0; b < c.reqs.size(); ++b) {
+          done.tokens.push_back(eng->hw.h_tok[b]);
+          const bool emits = b > 0 || c.reqs[0]->chunk_c0 + c.reqs[0]->chunk_n >= c.reqs[0]->S();
+          if (eng->cfg.debug_keep_logits && emits)
+            c.reqs[b]->logits.emplace_back(eng->hw.h_logits + b * V, eng->hw.h_logits + (b + 1) * V);
         }
       }
     }
@@ -242,7 +255,7 @@ nova_status Engine::create(const nova_model_config* m, const nova_engine_config*
   sim = c->backend == NOVA_BACKEND_SIM;
   if (cfg.max_decode_batch <= 0 || cfg.max_decode_batch > 16) return fail(NOVA_E_INVAL, "max_decode_batch in 1..16");
   if (cfg.max_requests <= 0) return fail(NOVA_E_INVAL, "max_requests must be > 0");
-  alg.pol = nova_partition_policy{NOVA_MODE_ADAPTIVE, 72, 72, 48, 48, 16, 8.f, 8.f, cfg.max_decode_batch, 5, 0};
+  alg.pol = nova_partition_policy{NOVA_MODE_ADAPTIVE, 72, 72, 48, 48, 16, 8.f, 8.f, cfg.max_decode_batch, 5, 0, 128};
   free_slots.clear();
   for (int i = cfg.max_requests - 1; i >= 0; --i) free_slots.push_back(i);
   if (sim) {
@@ -273,7 +286,11 @@ nova_status Engine::create(const nova_model_config* m, const nova_engine_config*
   if (cudaHostAlloc(&fw.h_pos3, 3 * S * sizeof(int), 0) || cudaHostAlloc(&fw.h_tok, 64, 0) ||
       cudaHostAlloc(&fw.h_logits, V * 4, 0) || cudaHostAlloc(&dw.h_rows, B * sizeof(DecodeRow), 0) ||
       cudaHostAlloc(&dw.h_tok, B * 4, 0) || cudaHostAlloc(&dw.h_forced, B * 4, 0) ||
-      cudaHostAlloc(&dw.h_logits, B * V * 4, 0))
+      cudaHostAlloc(&dw.h_logits, B * V * 4, 0) ||
+      cudaHostAlloc(&hw.h_rows, (NOVA_CHUNK_MAX + 16) * sizeof(DecodeRow), 0) ||
+      cudaHostAlloc(&hw.h_lm_rows, 17 * sizeof(DecodeRow), 0) || cudaHostAlloc(&hw.h_pos3, 3 * NOVA_CHUNK_MAX * 4, 0) ||
+      cudaHostAlloc(&hw.h_tok, 17 * 4, 0) || cudaHostAlloc(&hw.h_forced, 16 * 4, 0) ||
+      cudaHostAlloc(&hw.h_logits, 17 * V * 4, 0))
     return fail(NOVA_E_NOMEM, "pinned host buffers");
   free_pages.clear();
   for (int i = cfg.kv_pages - 1; i >= 0; --i) free_pages.push_back(i);
@@ -356,6 +373,7 @@ nova_status Engine::finalize() {
     }
   }
   cudaMemset(fw.keys, 0, 16 * 8);
+  cudaMemset(hw.keys, 0, 17 * 8);
   ktimer[0].init(512);
   ktimer[1].init(512);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(NOVA_E_CUDA, "finalize sync");
@@ -393,8 +411,12 @@ void Engine::shutdown() {
   }
   if (!sim) {
     for (void* p : {(void*)host_vit, (void*)fw.h_pos3, (void*)fw.h_tok, (void*)fw.h_logits, (void*)dw.h_rows,
-                    (void*)dw.h_tok, (void*)dw.h_forced, (void*)dw.h_logits})
+                    (void*)dw.h_tok, (void*)dw.h_forced, (void*)dw.h_logits, (void*)hw.h_rows, (void*)hw.h_lm_rows,
+                    (void*)hw.h_pos3, (void*)hw.h_tok, (void*)hw.h_forced, (void*)hw.h_logits})
       if (p) cudaFreeHost(p);
+    hw.h_rows = hw.h_lm_rows = nullptr;
+    hw.h_pos3 = hw.h_tok = hw.h_forced = nullptr;
+    hw.h_logits = nullptr;
     host_vit = nullptr;
     fw.h_pos3 = fw.h_tok = nullptr;
     fw.h_logits = nullptr;
@@ -548,6 +570,8 @@ void Engine::dispatch(const Decision& d) {
   } else if (d.kind == NOVA_DEC_PREFILL) {
     d.reqs[0]->st.pre_start = now;
     d.reqs[0]->st.split_at_pre = d.s_dec;
+  } else if (d.kind == NOVA_DEC_HYBRID && d.reqs[0]->chunk_c0 == 0) {
+    d.reqs[0]->st.pre_start = now;
   }
   if (sim) {
     Event ev;
@@ -561,6 +585,14 @@ void Engine::dispatch(const Decision& d) {
       ev.kind = NOVA_EV_PREFILL_DONE;
       dur = (int64_t)llround((d.ctx == NOVA_CTX_SOLO ? sc.t_p_solo : curve_at(sc_s, sc_tp, d.s_dec)) * d.reqs[0]->sim_ps);
       ev.tokens.push_back(-1);
+    } else if (d.kind == NOVA_DEC_HYBRID) {  // chunk share of the solo prefill + the decode batch
+      ev.kind = NOVA_EV_HYBRID_DONE;
+      for (Request* r : d.reqs) ev.key = std::min<uint64_t>(ev.key, r->id);
+      Request* p = d.reqs[0];
+      const double nb = (double)d.reqs.size() - 1;
+      const double dd = nb > 0 ? (double)sc.t_d_solo * (1.0 + sc.beta * (nb - 1)) : 0.0;
+      dur = (int64_t)llround((double)sc.t_p_solo * p->sim_ps * p->chunk_n / p->S() + dd);
+      ev.tokens.assign(d.reqs.size(), -1);
     } else {
       ev.kind = NOVA_EV_DECODE_DONE;
       for (Request* r : d.reqs) ev.key = std::min<uint64_t>(ev.key, r->id);
@@ -578,9 +610,9 @@ void Engine::dispatch(const Decision& d) {
   c.ctx = d.ctx;
   c.s_dec = d.s_dec;
   c.reqs = d.reqs;
-  if (d.kind == NOVA_DEC_DECODE) {
+  if (d.kind == NOVA_DEC_DECODE || d.kind == NOVA_DEC_HYBRID) {
     c.forced_tok.assign(d.reqs.size(), -1);
-    for (size_t b = 0; b < d.reqs.size(); ++b) {
+    for (size_t b = d.kind == NOVA_DEC_HYBRID ? 1 : 0; b < d.reqs.size(); ++b) {
       Request* r = d.reqs[b];
       const int k = r->emitted;  // feeding token k-1
       if ((int)r->forced.size() >= k && k >= 1) c.forced_tok[b] = r->forced[k - 1];
@@ -660,11 +692,13 @@ nova_status Engine::step(int64_t max_wait_us, nova_step_info* out) {
     log_event(e);
     if (e.kind == NOVA_EV_VISION_DONE) {
       e.reqs[0]->st.vis_end = e.t;
-    } else if (e.kind == NOVA_EV_PREFILL_DONE || e.kind == NOVA_EV_DECODE_DONE) {
+    } else if (e.kind == NOVA_EV_PREFILL_DONE || e.kind == NOVA_EV_DECODE_DONE || e.kind == NOVA_EV_HYBRID_DONE) {
       for (size_t b = 0; b < e.reqs.size(); ++b) {
         Request* r = e.reqs[b];
         const int idx = r->emitted;  // index of this token
-        if (e.kind == NOVA_EV_PREFILL_DONE) {
+        const bool first = e.kind == NOVA_EV_PREFILL_DONE || (e.kind == NOVA_EV_HYBRID_DONE && b == 0);
+        if (e.kind == NOVA_EV_HYBRID_DONE && b == 0 && r->pre_done + r->chunk_n < r->S()) continue;  // mid-prefill chunk
+        if (first) {
           r->st.pre_end = e.t;
           r->st.first_tok = e.t;
         }

@@ -161,6 +161,24 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   w.rows = (DecodeRow*)take(B * sizeof(DecodeRow));
   w.tok = (int*)take(B * 4);
   w.keys = (unsigned long long*)take(B * 8);
+  // CHUNK mode (hybrid iterations): up to NOVA_CHUNK_MAX prefill rows + 16 decode rows
+  Engine::HybWS h{};
+  {
+    const size_t MH = NOVA_CHUNK_MAX + 16;
+    h.pre = (float*)take(S * D * 4);
+    h.hid = (float*)take(MH * D * 4);
+    h.xf = (float*)take(17 * D * 4);
+    h.logits = (float*)take(17 * V * 4);
+    h.xb = (bf16*)take(MH * std::max(std::max(D, F), Hhd) * 2);
+    h.qkv = (bf16*)take(MH * d.llm_qkv_n * 2);
+    h.attn = (bf16*)take(MH * Hhd * 2);
+    h.act = (bf16*)take(MH * F * 2);
+    h.rows = (DecodeRow*)take(MH * sizeof(DecodeRow));
+    h.lm_rows = (DecodeRow*)take(17 * sizeof(DecodeRow));
+    h.pos3 = (int*)take(3 * NOVA_CHUNK_MAX * 4);
+    h.tok = (int*)take(17 * 4);
+    h.keys = (unsigned long long*)take(17 * 8);
+  }
   const size_t pix = (size_t)m.in_ch * N * m.patch * m.patch;
   bf16* d_pix = (bf16*)take(n_slots * pix * 2);
   int* d_prompt = (int*)take((size_t)n_slots * c.max_prompt * 4);
@@ -169,6 +187,9 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   if (e) {
     e->fw = f;
     e->dw = w;
+    e->hw.pre = h.pre, e->hw.hid = h.hid, e->hw.xf = h.xf, e->hw.logits = h.logits, e->hw.xb = h.xb;
+    e->hw.qkv = h.qkv, e->hw.attn = h.attn, e->hw.act = h.act, e->hw.rows = h.rows, e->hw.lm_rows = h.lm_rows;
+    e->hw.pos3 = h.pos3, e->hw.tok = h.tok, e->hw.keys = h.keys;
     e->d_pix = d_pix;
     e->d_prompt = d_prompt;
     e->d_bt = d_bt;

@@ -122,7 +122,10 @@ nova_status nova_set_frontier(nova_engine* e, const nova_plan_point* pts, int32_
 nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, nova_partition_policy* applied) {
   if (!e || !p) return NOVA_E_INVAL;
   Engine& E = e->e;
-  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_FRONTIER) return E.fail(NOVA_E_INVAL, "mode");
+  if (p->mode < NOVA_MODE_SERIAL || p->mode > NOVA_MODE_CHUNK) return E.fail(NOVA_E_INVAL, "mode");
+  if (p->mode != NOVA_MODE_CHUNK && E.alg.chunk_req)
+    return E.fail(NOVA_E_STATE, "a chunked prefill is in progress: leave CHUNK mode once it is done");
+  if (p->chunk_budget > NOVA_CHUNK_MAX) return E.fail(NOVA_E_INVAL, "chunk_budget > NOVA_CHUNK_MAX");
   if (p->mode == NOVA_MODE_FRONTIER && E.alg.frontier.empty())
     return E.fail(NOVA_E_STATE, "FRONTIER mode needs nova_set_frontier first");
   const int g = E.alg.granularity, mx = E.alg.max_split;
@@ -135,6 +138,7 @@ nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, n
   q.sm_min = rnd(q.sm_min);
   if (q.b_max <= 0 || q.b_max > E.cfg.max_decode_batch) q.b_max = E.cfg.max_decode_batch;
   if (q.pf_threshold <= 0) q.pf_threshold = 5;
+  if (q.chunk_budget <= 0) q.chunk_budget = 128;
   q.sm_dv_floor = q.sm_dv_floor <= 0 ? 0 : std::min(rnd(q.sm_dv_floor), mx);
   if (q.mode == NOVA_MODE_STATIC && (q.sm_decode_dv < g || q.sm_decode_dp < g || q.sm_decode_dv > mx ||
                                      q.sm_decode_dp > mx))

@@ -379,4 +379,108 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
   return cudaSuccess;
 }
 
+// ---------------------------------------------------------------- CHUNK: hybrid iteration (f1)
+// The paper's chunked-prefill baseline (R26): one batch of M = C + B rows --
+// rows [0, C) are prefill rows [c0, c0 + C) of reqs[0] (its E_vis | prompt embeds, staged at the
+// first chunk), rows [C, M) the decode rows of reqs[1..].  Every linear is one tcgen05 GEMM over
+// the M rows; RoPE / KV append per row (M-RoPE positions for the chunk, 1D for generated tokens);
+// attention is the paged decode kernel with one query row per token: a chunk row at cache index j
+// attends to keys [0, j] (the prefix of earlier chunks + the causal part of its own chunk, both
+// already in the pages).  lm_head on the last chunk row (token 0, once the prefill completes) and
+// on the decode rows.
+cudaError_t Engine::run_hybrid(const std::vector<Request*>& rq, const std::vector<int>& forced, cudaStream_t s,
+                               int sms) {
+  const auto& m = dims.m;
+  const int D = m.llm_dim, H = m.llm_heads, KV = m.llm_kv_heads, hd = m.head_dim, F = m.llm_ffn, V = m.vocab;
+  const int ldq = dims.llm_qkv_n;
+  Request* P = rq[0];
+  const int c0 = P->chunk_c0, C = P->chunk_n, B = (int)rq.size() - 1, M = C + B;
+  const int nv = P->n_v(), S = P->S();
+  const bool last = c0 + C >= S;
+  if (C < 1 || C > NOVA_CHUNK_MAX || B > 16) return cudaErrorInvalidValue;
+  pass_work[1] = 0;
+  bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
+  if (c0 == 0) {  // stage the request's input rows: E_vis (vision merger output) | prompt embeddings
+    CUDA_TRY(cudaMemcpyAsync(hw.pre, fw.hid, (size_t)nv * D * 4, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(embed(W.embed, D, d_prompt + (size_t)P->slot * cfg.max_prompt, nullptr, nullptr, hw.pre + (size_t)nv * D,
+                   D, P->n_prompt, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(hw.hid, hw.pre + (size_t)c0 * D, (size_t)C * D * 4, cudaMemcpyDeviceToDevice, s));
+  // chunk rows: M-RoPE positions (HF get_rope_index, image first) and cache index c0 + r
+  const int lw = P->gw / m.merge, st = std::max(P->gh / m.merge, lw);
+  int max_ctx = 0;
+  for (int r = 0; r < C; ++r) {
+    const int j = c0 + r;
+    if (j < nv) {
+      hw.h_pos3[r] = 0;
+      hw.h_pos3[C + r] = j / lw;
+      hw.h_pos3[2 * C + r] = j % lw;
+    } else {
+      hw.h_pos3[r] = hw.h_pos3[C + r] = hw.h_pos3[2 * C + r] = st + (j - nv);
+    }
+    hw.h_rows[r] = DecodeRow{P->slot, j, hw.h_pos3[2 * C + r], 0};
+    max_ctx = std::max(max_ctx, j);
+  }
+  for (int b = 0; b < B; ++b) {  // decode rows (as run_decode): feed token emitted - 1
+    Request* r = rq[1 + b];
+    const int e = r->emitted;
+    const int stb = std::max(r->gh / m.merge, r->gw / m.merge);
+    hw.h_rows[C + b] = DecodeRow{r->slot, r->S() + e - 1, stb + r->n_prompt - 1 + e, 0};
+    max_ctx = std::max(max_ctx, hw.h_rows[C + b].ctx);
+  }
+  int n_lm = 0;  // lm_head rows: [0] the chunk's last row (if it completes the prefill), [1..B] decode rows
+  hw.h_lm_rows[0] = DecodeRow{P->slot, S - 1, 0, 0};
+  for (int b = 0; b < B; ++b) hw.h_lm_rows[1 + b] = hw.h_rows[C + b];
+  CUDA_TRY(cudaMemcpyAsync(hw.rows, hw.h_rows, M * sizeof(DecodeRow), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(hw.lm_rows, hw.h_lm_rows, (B + 1) * sizeof(DecodeRow), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(hw.pos3, hw.h_pos3, 3 * C * sizeof(int), cudaMemcpyHostToDevice, s));
+  for (int b = 0; b < B; ++b)
+    if (forced[1 + b] >= 0) {
+      hw.h_forced[b] = forced[1 + b];
+      CUDA_TRY(cudaMemcpyAsync(d_last + rq[1 + b]->slot, hw.h_forced + b, 4, cudaMemcpyHostToDevice, s));
+    }
+  if (B > 0) CUDA_TRY(embed(W.embed, D, nullptr, hw.rows + C, d_last, hw.hid + (size_t)C * D, D, B, s));
+  for (int l = 0; l < m.llm_layers; ++l) {
+    const LlmLayerW& L = W.llm[l];
+    CUDA_TRY(rmsnorm(hw.hid, D, L.ln1, hw.xb, 0, D, M, D, m.rms_eps, s));
+    CUDA_TRY(t_gemm(this, 1, NOVA_K_LLM_GEMM, hw.xb, D, L.qkv_w, D, hw.qkv, ldq, L.qkv_b, M, ldq, D, EPI_BF16, sms, s));
+    CUDA_TRY(llm_rope_kv(hw.qkv, ldq, C, H, KV, hd, m.llm_theta, m.mrope_section[0], m.mrope_section[1], hw.pos3, C,
+                         nullptr, P->slot, c0, pool, l, cfg.kv_pages, d_bt, max_pages_per_req, s));
+    if (B > 0)
+      CUDA_TRY(llm_rope_kv(hw.qkv + (size_t)C * ldq, ldq, B, H, KV, hd, m.llm_theta, m.mrope_section[0],
+                           m.mrope_section[1], nullptr, 0, hw.rows + C, -1, 0, pool, l, cfg.kv_pages, d_bt,
+                           max_pages_per_req, s));
+    CUDA_TRY(decode_attn(hw.qkv, ldq, hw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
+                         hw.rows, M, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
+    CUDA_TRY(t_gemm(this, 1, NOVA_K_LLM_GEMM, hw.attn, H * hd, L.o_w, H * hd, hw.hid, D, nullptr, M, D, H * hd,
+                    EPI_F32_RESID, sms, s));
+    CUDA_TRY(rmsnorm(hw.hid, D, L.ln2, hw.xb, 0, D, M, D, m.rms_eps, s));
+    CUDA_TRY(t_gemm(this, 1, NOVA_K_LLM_GEMM, hw.xb, D, L.gu_w, D, hw.act, F, nullptr, M, 2 * F, D, EPI_BF16_SILUMUL,
+                    sms, s));
+    CUDA_TRY(t_gemm(this, 1, NOVA_K_LLM_GEMM, hw.act, F, L.down_w, F, hw.hid, D, nullptr, M, D, F, EPI_F32_RESID, sms,
+                    s));
+  }
+  // final RMSNorm (f32) -> lm_head -> greedy argmax; the prefill row and the decode rows are two
+  // GEMV launches (each <= 16 rows)
+  GemvAux la;
+  if (last) {
+    CUDA_TRY(rmsnorm(hw.hid + (size_t)(C - 1) * D, D, W.final_norm, hw.xf, 1, D, 1, D, m.rms_eps, s));
+    la.keys = hw.keys;
+    CUDA_TRY(gemv_ex(hw.xf, 1, D, W.lm_head, V, D, hw.logits, V, nullptr, 1, EPI_F32_ARGMAX, la, s));
+  }
+  if (B > 0) {
+    CUDA_TRY(rmsnorm(hw.hid + (size_t)C * D, D, W.final_norm, hw.xf + D, 1, D, B, D, m.rms_eps, s));
+    la.keys = hw.keys + 1;
+    CUDA_TRY(gemv_ex(hw.xf + D, 1, D, W.lm_head, V, D, hw.logits + V, V, nullptr, B, EPI_F32_ARGMAX, la, s));
+  }
+  n_lm = B + 1;
+  const int lm0 = last ? 0 : 1;
+  if (n_lm - lm0 > 0)
+    CUDA_TRY(argmax_finalize(hw.keys + lm0, n_lm - lm0, hw.tok + lm0, hw.lm_rows + lm0, d_last, -1, s));
+  CUDA_TRY(cudaMemcpyAsync(hw.h_tok, hw.tok, (size_t)n_lm * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (cfg.debug_keep_logits)
+    CUDA_TRY(cudaMemcpyAsync(hw.h_logits, hw.logits, (size_t)n_lm * V * 4, cudaMemcpyDeviceToHost, s));
+  return cudaSuccess;
+}
+
 }  // namespace nova

@@ -15,7 +15,7 @@ import numpy as np
 from . import _abi as A
 from ._lib import lib
 
-SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, FRONTIER = 0, 1, 2, 3, 4, 5
+SERIAL, STATIC, ADAPTIVE, PF_LIMIT, MULTI_STREAM, FRONTIER, CHUNK = 0, 1, 2, 3, 4, 5, 6
 CTX_DV, CTX_DP, CTX_SOLO = 0, 1, 2
 DEC_VISION, DEC_PREFILL, DEC_DECODE, DEC_FINISH = 0, 1, 2, 3
 EV_VISION_DONE, EV_PREFILL_DONE, EV_DECODE_DONE, EV_ARRIVAL = 0, 1, 2, 3
@@ -143,9 +143,10 @@ class Engine:
         return t.value, g.value, n.value
 
     def set_partition(self, mode=ADAPTIVE, sm_decode_dv=72, sm_decode_dp=72, sm_op_dv=48, sm_op_dp=48, sm_min=16,
-                      alpha_dv=8.0, alpha_dp=8.0, b_max=0, pf_threshold=5, sm_dv_floor=0) -> A.PartitionPolicy:
+                      alpha_dv=8.0, alpha_dp=8.0, b_max=0, pf_threshold=5, sm_dv_floor=0,
+                      chunk_budget=128) -> A.PartitionPolicy:
         p = A.PartitionPolicy(mode, sm_decode_dv, sm_decode_dp, sm_op_dv, sm_op_dp, sm_min, alpha_dv, alpha_dp, b_max,
-                              pf_threshold, sm_dv_floor)
+                              pf_threshold, sm_dv_floor, chunk_budget)
         out = A.PartitionPolicy()
         self._check(self.lib.nova_set_partition(self.h, C.byref(p), C.byref(out)), "nova_set_partition")
         return out

@@ -67,7 +67,9 @@ def main():
             continue
         pols.append((f"adaptive_smin{smin}", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=smin,
                                                   alpha_dv=(sv - smin) / 3.0, alpha_dp=(sp - smin) / 3.0, b_max=16)))
-    base = {"serial": dict(mode=E.SERIAL, b_max=16), "multi_stream": dict(mode=E.MULTI_STREAM, b_max=16)}
+    base = {"serial": dict(mode=E.SERIAL, b_max=16), "multi_stream": dict(mode=E.MULTI_STREAM, b_max=16),
+            "chunk_128": dict(mode=E.CHUNK, chunk_budget=128, b_max=16),
+            "pf_limit_5": dict(mode=E.PF_LIMIT, pf_threshold=5, b_max=16)}
     pols += [(n, base[n]) for n in a.policies.split(",") if n in base]
     for rho in a.rho:
         trs = [(BN.make_trace(SHAPE, a.requests, rho, t_front, 61 + k) if a.trace == 'mmpp' else poisson_trace(a.requests, rho / t_front_p, 21 + k)) for k in range(a.seeds)]

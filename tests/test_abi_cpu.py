@@ -111,7 +111,10 @@ def _replay(log, reqs, pol):
     """Feed the engine's logged events, tick by tick, to the oracle Alg. 1 and compare decisions."""
     alg = OS.Alg1(pol)
     for rid, g in reqs.items():
-        alg.add_request(rid, g)
+        if isinstance(g, tuple):   # (gen_len, S): CHUNK mode needs the prefill length
+            alg.add_request(rid, g[0], g[1])
+        else:
+            alg.add_request(rid, g)
     ticks = {}
     for rec in log:
         ticks.setdefault(rec[0], []).append(rec)
@@ -120,7 +123,7 @@ def _replay(log, reqs, pol):
         evs, decs = [], []
         for tick, is_ev, kind, ctx, s, ids, tns in ticks[t]:
             if is_ev:
-                payload = list(ids) if kind == OS.EV_DECODE_DONE else ids[0]
+                payload = list(ids) if kind in (OS.EV_DECODE_DONE, OS.EV_HYBRID_DONE) else ids[0]
                 evs.append((kind, min(ids), payload, tns))
             else:
                 decs.append((kind, tuple(ids), ctx, s))
@@ -168,6 +171,61 @@ def test_sim_decision_log_replays_on_oracle(E, mode, seed):
     assert len(fin) == len(gens) and n > 3 * len(gens)
     toks = e.poll_tokens(100000)
     assert len(toks) == sum(gens.values())
+
+
+@pytest.mark.parametrize("budget,seed", [(128, 1), (48, 2), (512 // 4, 3)])
+def test_sim_chunk_mode_replays_on_oracle(E, budget, seed):
+    """CHUNK (the paper's chunked-prefill baseline, R26): the C++ controller's decision
+    log (hybrid passes with their chunk sizes) replays on the oracle state machine, every prefill
+    token count is covered exactly by its chunks, and all tokens are emitted."""
+    rnd = random.Random(seed)
+    e = _sim_engine(E, E.CHUNK, [8, 16], [9 * MS] * 2, [3 * MS] * 2, [MS] * 2, [MS] * 2, (9 * MS, 3 * MS, int(0.7 * MS)),
+                    beta=0.03, b_max=8, chunk_budget=budget)
+    t, gens = 0, {}
+    for i in range(40):
+        t += int(rnd.expovariate(1 / 20.0) * MS) if rnd.random() < 0.8 else 0
+        g = rnd.randint(1, 10)
+        grid = rnd.choice([(8, 12), (52, 94), (4, 6)])
+        npr = rnd.randint(1, 30)
+        rid = e.submit(None, [1] * npr, g, t, grid=grid)
+        gens[rid] = (g, (grid[0] // 2) * (grid[1] // 2) + npr)
+    while e.step().events:
+        pass
+    log = e.decision_log()
+    n = _replay(log, gens, OS.Policy(mode=OS.CHUNK, total_sms=148, granularity=8, b_max=8, chunk_budget=budget))
+    hyb = [r for r in log if not r[1] and r[2] == OS.D_HYBRID]
+    covered = {}
+    for r in hyb:
+        covered[r[5][0]] = covered.get(r[5][0], 0) + r[4]
+        assert 1 <= r[4] <= budget and len(r[5]) - 1 <= 8
+        assert r[4] <= max(1, budget - (len(r[5]) - 1))
+    assert covered == {rid: gs[1] for rid, gs in gens.items()}
+    assert n > len(gens)
+    toks = e.poll_tokens(100000)
+    assert len(toks) == sum(g for g, _ in gens.values())
+    assert sorted(i for rid, i, *_ in toks if rid == min(gens)) == list(range(gens[min(gens)][0]))
+
+
+def test_sim_chunk_matches_oracle_simulation_times(E):
+    """CHUNK through the C++ Sim backend and oracle.scheduler.simulate: identical token times."""
+    pol = dict(b_max=4, chunk_budget=64)
+    e = _sim_engine(E, E.CHUNK, [8], [9 * MS], [3 * MS], [MS], [MS], (9 * MS, 3 * MS, MS), beta=0.05, **pol)
+    rnd = random.Random(9)
+    reqs, t = [], 0
+    for i in range(25):
+        t += int(rnd.expovariate(1 / 9.0) * MS)
+        g = rnd.randint(1, 8)
+        grid = rnd.choice([(8, 12), (16, 20)])
+        rid = e.submit(None, [3, 4, 5], g, t, grid=grid)
+        reqs.append(OS.SimRequest(rid, t, g, 1.0, 1.0, S=(grid[0] // 2) * (grid[1] // 2) + 3))
+    while e.step().events:
+        pass
+    got = {}
+    for rid, idx, tok, tt, fl in e.poll_tokens(10000):
+        got.setdefault(rid, []).append(tt)
+    _, want = OS.simulate(OS.Policy(mode=OS.CHUNK, **pol), OS.SimCurves([8], [9 * MS], [3 * MS], [MS], [MS], 9 * MS,
+                                                                        3 * MS, MS, beta=0.05), reqs)
+    assert got == want
 
 
 def test_sim_matches_oracle_simulation_times(E):

@@ -150,3 +150,42 @@ def test_full_width_reduced_depth_parity(base):
         if srt[-1] - srt[-2] > 0.1:
             assert tk[k] == int(np.argmax(ref["logits"][k]))
     e.close()
+
+
+@pytest.mark.parametrize("budget", [5, 128])
+def test_chunked_prefill_mode_matches_oracle(tiny_setup, budget):
+    """CHUNK (the paper's chunked-prefill baseline; R26): hybrid passes that batch
+    prefill chunks with decode rows give the oracle's tokens and logits (<= 3e-2).  budget 5: the
+    12-token tiny prefill takes 3-12 chunks, several of them sharing a batch with decode rows."""
+    from paper_2509_21301_b200 import engine as E
+    bits, req, ref = tiny_setup
+    e = _engine(TINY, bits)
+    e.set_partition(E.CHUNK, chunk_budget=budget, b_max=4)
+    outs = _run(e, [req] * 4)
+    for tk, lg in outs:
+        assert tk == ref["tokens"].tolist()
+        assert np.abs(lg - ref["logits"]).max() <= 3e-2
+    log = e.decision_log()
+    hyb = [r for r in log if not r[1] and r[2] == 4]   # NOVA_DEC_HYBRID
+    assert hyb and sum(r[4] for r in hyb) == 4 * 12     # every prefill token in exactly one chunk
+    if budget == 5:
+        assert any(len(r[5]) > 1 for r in hyb)           # some chunk shared a batch with decode rows
+    e.close()
+
+
+def test_chunked_prefill_full_width_reduced_depth():
+    """CHUNK at 2B width, BASELINE image size (S = 1286 -> 11 chunks of <= 128 tokens), depth 2+2:
+    the chunked prefill's token-0 logits and the decode logits match the oracle (teacher-forced)."""
+    from paper_2509_21301_b200 import engine as E
+    s = reduced_depth(Q2B, 2, 2)
+    bits = gen_weights(s, 1)
+    req = make_request(s, (52, 94), 64, 4, 1)
+    e = _engine(s, bits, max_requests=2, kv_pages=64, max_patches=4888, max_prompt=64, max_gen=8)
+    e.set_partition(E.CHUNK, chunk_budget=128)
+    (tk, lg), = _run(e, [req], timeout_s=300)
+    ref = V.generate(V.OracleWeights(bits, np.float32), req.pixels, req.prompt_ids, req.gen_len, s,
+                     force_tokens=tk)
+    assert np.abs(lg - ref["logits"]).max() <= 5e-2 * max(1.0, np.abs(ref["logits"]).max() / 10)
+    hyb = [r for r in e.decision_log() if not r[1] and r[2] == 4]
+    assert len(hyb) == 11 and sum(r[4] for r in hyb) == 1286
+    e.close()
