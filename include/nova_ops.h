@@ -102,6 +102,14 @@ int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void*
                         int H, int KV, int hd, const int32_t* block_tables, int max_pages, const nova_decode_row* rows,
                         int B, int max_ctx, float* ws, int32_t* tickets, void* stream);
 
+/* Chunked-prefill attention (the paper's Chunk baseline; CHUNK mode): C query rows of one
+ * request -- q at qkv rows [0, C) (heads 0..H-1, fused q|k|v layout, row stride ld) with cache
+ * indices c0 .. c0 + C - 1 -- attend to that request's paged cache (block_table_row: its block
+ * table, device; K/V of all C rows already appended), key j visible to row r iff j <= c0 + r;
+ * GQA (query head h reads KV head h / (H / KV)), scale hd^-1/2.  out [C][H hd] bf16 (ldo). */
+int nova_op_chunk_attn(const void* qkv, int ld, void* out, int ldo, int C, int c0, int H, int KV, int hd,
+                       const void* kv_pool, int layer, int n_pages, const int32_t* block_table_row, void* stream);
+
 /* Fused decode linear (a7; "kernel fusion ... RoPE and RMSNorm"):
  * Y = epilogue(Xin . W^T + bias) for B <= 16 rows, where Xin is, by x_mode:
  *   0: X bf16;  1: X f32 (hi/lo bf16 split, exact to ~2^-16);

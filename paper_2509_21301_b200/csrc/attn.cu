@@ -196,6 +196,165 @@ cudaError_t fa_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int H,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- chunked-prefill attention
+// CHUNK mode (the paper's chunked-prefill baseline): the C query rows of one prefill chunk
+// (cache indices c0 .. c0 + C - 1 of request `slot`, already appended) attend to every cached key
+// j <= their own index -- the prefix of earlier chunks and the causal part of the chunk -- read
+// straight from the paged pool: a 64-key tile is one KV page (bt[slot][tile]).  Same online-softmax
+// structure as flash_attn_kernel (64 query rows x one query head per CTA, mma.sync m16n8k16).
+template <int HD>
+__global__ void __launch_bounds__(128) chunk_attn_kernel(const bf16* __restrict__ qkv, int ld, bf16* __restrict__ out,
+                                                         int ldo, int C, int c0, int H, int KV,
+                                                         const bf16* __restrict__ pool, int layer, int n_pages,
+                                                         const int* __restrict__ btr, float scale_log2) {
+  using Cf = FaCfg<HD>;
+  constexpr int HDP = Cf::HDP, BKV = Cf::BKV;
+  constexpr int KT = HD / 16, DT = HD / 8, CH = HD / 8;
+  extern __shared__ __align__(16) uint8_t fa_smem[];
+  bf16* sQ = reinterpret_cast<bf16*>(fa_smem);
+  bf16* sK = sQ + Cf::BQ * HDP;
+  bf16* sV = sK + 2 * BKV * HDP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int qt = blockIdx.x, h = blockIdx.y;
+  const int kvh = h / (H / KV);
+  const int q0 = qt * Cf::BQ;
+  const bf16* qbase = qkv + (size_t)h * HD;
+  // launched with programmatic dependent launch: q and this chunk's K/V are written by the
+  // preceding RoPE / KV-append kernel
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int i = tid; i < Cf::BQ * CH; i += 128) {
+    const int r = i / CH, cc = i % CH;
+    const int row = q0 + r;
+    cp_async16(sQ + r * HDP + cc * 8, qbase + (size_t)(row < C ? row : 0) * ld + cc * 8, row < C);
+  }
+  const int Lk = c0 + min(C, q0 + Cf::BQ);  // keys this tile of queries can see
+  const size_t page_elems = (size_t)2 * KV * 64 * HD;
+  auto load_kv = [&](int tile, int buf) {
+    const bf16* kb = pool + ((size_t)layer * n_pages + btr[tile]) * page_elems + (size_t)kvh * 64 * HD;
+    const bf16* vb = kb + (size_t)KV * 64 * HD;
+    const int k0 = tile * BKV;
+    for (int i = tid; i < BKV * CH; i += 128) {
+      const int r = i / CH, cc = i % CH;
+      const bool ok = k0 + r < Lk;
+      cp_async16(sK + (buf * BKV + r) * HDP + cc * 8, kb + (size_t)(ok ? r : 0) * HD + cc * 8, ok);
+      cp_async16(sV + (buf * BKV + r) * HDP + cc * 8, vb + (size_t)(ok ? r : 0) * HD + cc * 8, ok);
+    }
+  };
+  const int n_tiles = (Lk + BKV - 1) / BKV;
+  load_kv(0, 0);
+  cp_async_commit();
+  float o[DT][4];
+#pragma unroll
+  for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-1e30f, -1e30f}, l_r[2] = {0.f, 0.f};
+  uint32_t qa[KT][4];
+  const int row_a = q0 + warp * 16 + g, row_b = row_a + 8;  // chunk rows; cache index c0 + row
+  for (int t = 0; t < n_tiles; ++t) {
+    if (t + 1 < n_tiles) load_kv(t + 1, (t + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk)
+        ldmatrix_x4(qa[kk], smem_u32(sQ + (warp * 16 + (lane & 15)) * HDP + kk * 16 + (lane >> 4) * 8));
+    }
+    const bf16* kt = sK + (t & 1) * BKV * HDP;
+    const bf16* vt = sV + (t & 1) * BKV * HDP;
+    float s[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk) {
+        uint32_t b[2];
+        ldmatrix_x2(b, smem_u32(kt + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
+        mma_bf16_16816(s[nt], qa[kk], b);
+      }
+    }
+    const int k0 = t * BKV;
+    float mx[2] = {-1e30f, -1e30f};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int key = k0 + nt * 8 + 2 * c + (j & 1);
+        const int row = (j < 2) ? row_a : row_b;
+        const float v = (key <= c0 + row && key < Lk) ? s[nt][j] * scale_log2 : -1e30f;
+        s[nt][j] = v;
+        mx[j >> 1] = fmaxf(mx[j >> 1], v);
+      }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(m_r[r], mx[r]);
+      corr[r] = exp2f(m_r[r] - mn);
+      m_r[r] = mn;
+    }
+    float ls[2] = {0.f, 0.f};
+    uint32_t pa[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] - m_r[0]), p1 = exp2f(s[nt][1] - m_r[0]);
+      const float p2 = exp2f(s[nt][2] - m_r[1]), p3 = exp2f(s[nt][3] - m_r[1]);
+      ls[0] += p0 + p1;
+      ls[1] += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) l_r[r] = l_r[r] * corr[r] + ls[r];
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      o[dt][0] *= corr[0];
+      o[dt][1] *= corr[0];
+      o[dt][2] *= corr[1];
+      o[dt][3] *= corr[1];
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        uint32_t b[2];
+        ldmatrix_x2_trans(b, smem_u32(vt + (kk * 16 + (lane & 15)) * HDP + dt * 8));
+        mma_bf16_16816(o[dt], pa[kk], b);
+      }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
+  }
+  const float inv_a = 1.f / l_r[0], inv_b = 1.f / l_r[1];
+#pragma unroll
+  for (int dt = 0; dt < DT; ++dt) {
+    const int col = h * HD + dt * 8 + 2 * c;
+    if (row_a < C)
+      *reinterpret_cast<uint32_t*>(out + (size_t)row_a * ldo + col) = pack_bf16(o[dt][0] * inv_a, o[dt][1] * inv_a);
+    if (row_b < C)
+      *reinterpret_cast<uint32_t*>(out + (size_t)row_b * ldo + col) = pack_bf16(o[dt][2] * inv_b, o[dt][3] * inv_b);
+  }
+}
+
+template <int HD>
+cudaError_t ca_launch(const bf16* qkv, int ld, bf16* out, int ldo, int C, int c0, int H, int KV, const bf16* pool,
+                      int layer, int n_pages, const int* btr, cudaStream_t s) {
+  const float sl2 = LOG2E / sqrtf((float)HD);
+  const int smem = FaCfg<HD>::SMEM;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(chunk_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  return launch_k(chunk_attn_kernel<HD>, dim3((C + 63) / 64, H), dim3(128), smem, s, true, qkv, ld, out, ldo, C, c0, H,
+                  KV, pool, layer, n_pages, btr, sl2);
+}
+
 // ---------------------------------------------------------------- decode attention
 constexpr int DCHUNK = 256;
 constexpr int MAXG = 8;  // max GQA group size
@@ -727,6 +886,18 @@ cudaError_t decode_attn(const bf16* qkv, int ld, bf16* out, int ldo, const bf16*
     case 64: return da_launch<64>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
     case 128:
       return da_launch<128>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t chunk_attn(const bf16* qkv, int ld, bf16* out, int ldo, int C, int c0, int H, int KV, int hd,
+                       const bf16* kv_pool, int layer, int n_pages, const int* block_table_row, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  if (H % KV || ld % 8) return cudaErrorInvalidValue;
+  switch (hd) {
+    case 32: return ca_launch<32>(qkv, ld, out, ldo, C, c0, H, KV, kv_pool, layer, n_pages, block_table_row, s);
+    case 64: return ca_launch<64>(qkv, ld, out, ldo, C, c0, H, KV, kv_pool, layer, n_pages, block_table_row, s);
+    case 128: return ca_launch<128>(qkv, ld, out, ldo, C, c0, H, KV, kv_pool, layer, n_pages, block_table_row, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -193,6 +193,12 @@ cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf
                         int H, int KV, int hd, const int* block_tables, int max_pages, const DecodeRow* rows, int B,
                         int max_ctx, float* ws, int* tickets, cudaStream_t s);
 
+// Chunked-prefill attention (CHUNK mode): C query rows (cache indices c0 .. c0 + C - 1 of one
+// request, K/V already appended) attend causally to the request's paged cache; block_table_row =
+// that request's block table (device).  out rows [0, C) (ldo).
+cudaError_t chunk_attn(const bf16* qkv, int ld, bf16* out, int ldo, int C, int c0, int H, int KV, int hd,
+                       const bf16* kv_pool, int layer, int n_pages, const int* block_table_row, cudaStream_t s);
+
 cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf16* y, int ldy, int M, int d,
                       float eps, cudaStream_t s);
 // y_f32: 0 bf16 rows, 1 f32 rows, 2 bf16 hi rows at y and bf16 lo rows at y + M * ldy

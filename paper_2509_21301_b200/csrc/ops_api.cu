@@ -87,6 +87,11 @@ int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_bl
                       tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo));
 }
 int nova_op_gemv_umma_splits(int N, int K, int epi) { return gemv_umma_plan(N, K, epi).P; }
+int nova_op_chunk_attn(const void* qkv, int ld, void* out, int ldo, int C, int c0, int H, int KV, int hd,
+                       const void* kv_pool, int layer, int n_pages, const int32_t* block_table_row, void* stream) {
+  return st(chunk_attn((const bf16*)qkv, ld, (bf16*)out, ldo, C, c0, H, KV, hd, (const bf16*)kv_pool, layer, n_pages,
+                       block_table_row, S(stream)));
+}
 int nova_op_argmax_finalize(uint64_t* keys, int n, int32_t* out_tok, const nova_decode_row* rows, int32_t* last_tok,
                             int single_slot, void* stream) {
   return st(argmax_finalize((unsigned long long*)keys, n, out_tok, (const DecodeRow*)rows, last_tok, single_slot,

@@ -386,7 +386,8 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
 // the M rows; RoPE / KV append per row (M-RoPE positions for the chunk, 1D for generated tokens);
 // attention is the paged decode kernel with one query row per token: a chunk row at cache index j
 // attends to keys [0, j] (the prefix of earlier chunks + the causal part of its own chunk, both
-// already in the pages).  lm_head on the last chunk row (token 0, once the prefill completes) and
+// already in the pages) -- chunk_attn for the chunk rows (one pass over the prefix per 64-row query
+// tile), the paged decode kernel for the decode rows.  lm_head on the last chunk row (token 0, once the prefill completes) and
 // on the decode rows.
 cudaError_t Engine::run_hybrid(const std::vector<Request*>& rq, const std::vector<int>& forced, cudaStream_t s,
                                int sms) {
@@ -450,8 +451,12 @@ cudaError_t Engine::run_hybrid(const std::vector<Request*>& rq, const std::vecto
       CUDA_TRY(llm_rope_kv(hw.qkv + (size_t)C * ldq, ldq, B, H, KV, hd, m.llm_theta, m.mrope_section[0],
                            m.mrope_section[1], nullptr, 0, hw.rows + C, -1, 0, pool, l, cfg.kv_pages, d_bt,
                            max_pages_per_req, s));
-    CUDA_TRY(decode_attn(hw.qkv, ldq, hw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
-                         hw.rows, M, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
+    CUDA_TRY(chunk_attn(hw.qkv, ldq, hw.attn, H * hd, C, c0, H, KV, hd, pool, l, cfg.kv_pages,
+                        d_bt + (size_t)P->slot * max_pages_per_req, s));
+    if (B > 0)
+      CUDA_TRY(decode_attn(hw.qkv + (size_t)C * ldq, ldq, hw.attn + (size_t)C * H * hd, H * hd, pool, l, cfg.kv_pages,
+                           H, KV, hd, d_bt, max_pages_per_req, hw.rows + C, B, max_ctx, dw.attn_ws, dw.tickets + 4096,
+                           s));
     CUDA_TRY(t_gemm(this, 1, NOVA_K_LLM_GEMM, hw.attn, H * hd, L.o_w, H * hd, hw.hid, D, nullptr, M, D, H * hd,
                     EPI_F32_RESID, sms, s));
     CUDA_TRY(rmsnorm(hw.hid, D, L.ln2, hw.xb, 0, D, M, D, m.rms_eps, s));

@@ -157,3 +157,8 @@ def nova_op_gemv_umma(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_ct
 
 def nova_op_gemv_umma_splits(N: int, K: int, epi: int) -> int:
     return lib().nova_op_gemv_umma_splits(N, K, epi)
+
+
+def nova_op_chunk_attn(qkv, out, C, c0, H, KV, hd, kv_pool, layer, n_pages, block_table_row, stream=None):
+    check(lib().nova_op_chunk_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), C, c0, H, KV, hd, _p(kv_pool), layer,
+                                   n_pages, _p(block_table_row), _s(stream)), "chunk_attn")
