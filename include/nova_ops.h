@@ -102,6 +102,17 @@ int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void*
                         int H, int KV, int hd, const int32_t* block_tables, int max_pages, const nova_decode_row* rows,
                         int B, int max_ctx, float* ws, int32_t* tickets, void* stream);
 
+/* Persistent paged decode attention (decode_attn_p.cu): same contract as nova_op_decode_attn
+ * (rows[b] = {slot, ctx, pos, pad}: query b attends keys 0..ctx of its slot's pages; GQA), work
+ * units (request, KV head, 128-key chunk) on a grid of 3 CTAs per SM of the partition (max_ctas =
+ * SM budget, 0 = whole GPU); ws >= B * KV * mch * (32 + (H / KV) hd) floats with mch >=
+ * ceil((max_ctx + 1) / 128) (<= 64), tickets >= B * KV ints (zero on entry, left zero).  Results
+ * are bitwise independent of max_ctas and of the other rows of the batch. */
+int nova_op_decode_attn_p(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
+                          int H, int KV, int hd, const int32_t* block_tables, int max_pages,
+                          const nova_decode_row* rows, int B, int max_ctx, float* ws, int32_t* tickets, int mch,
+                          int max_ctas, void* stream);
+
 /* Chunked-prefill attention (the paper's Chunk baseline; CHUNK mode): C query rows of one
  * request -- q at qkv rows [0, C) (heads 0..H-1, fused q|k|v layout, row stride ld) with cache
  * indices c0 .. c0 + C - 1 -- attend to that request's paged cache (block_table_row: its block

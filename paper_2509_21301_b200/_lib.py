@@ -34,6 +34,7 @@ OPS_SIGNATURES = {
     "nova_op_gemv_umma": [P, P, I, P, I, I, P, I, P, I, I, P, P, P, I, P],
     "nova_op_gemv_umma_splits": [I, I, I],
     "nova_op_chunk_attn": [P, I, P, I, I, I, I, I, I, P, I, I, P, P],
+    "nova_op_decode_attn_p": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P, I, I, P],
     "nova_op_layernorm": [P, I, P, P, P, I, I, I, F, P],
     "nova_op_rmsnorm": [P, I, P, P, I, I, I, I, F, P],
     "nova_op_patchify": [P, I, I, I, I, I, I, P, P],

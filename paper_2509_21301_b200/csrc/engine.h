@@ -330,6 +330,8 @@ class Engine {
   cudaError_t run_hybrid(const std::vector<Request*>& reqs, const std::vector<int>& forced, cudaStream_t s, int sms);
   cudaStream_t stream_for(int role, int ctx, int s_dec);
   int s_max_of_public() const;
+  // 128-key chunk capacity of dw.attn_ws per (request, KV head) (decode_attn_p, fused decode)
+  int attn_mch() const { return (s_max_of_public() + cfg.max_gen + 1 + 127) / 128; }
   nova_status time_pass(int stage, int s, int gh, int gw, int n_prompt, int B, int ctx, int corun, int iters,
                         double* out);
 };

@@ -193,6 +193,17 @@ cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf
                         int H, int KV, int hd, const int* block_tables, int max_pages, const DecodeRow* rows, int B,
                         int max_ctx, float* ws, int* tickets, cudaStream_t s);
 
+// Persistent paged decode attention (decode_attn_p.cu): units (request, KV head, 128-key chunk)
+// on a grid of 3 CTAs per SM of the partition (sms; 0 = whole GPU), chunk partials in ws
+// (B * KV * mch * (32 + (H / KV) hd) floats, mch >= ceil((max_ctx + 1) / 128), <= 64) merged in
+// chunk order by the CTA that completes a (request, KV head) (tickets: B * KV ints, zero, left
+// zero).  Bitwise independent of sms.  B <= 16, H / KV <= 16.
+extern int g_dec_attn_p;  // env NOVA_DEC_ATTN_P=1: the decode path uses decode_attn_p (default 0, measured no faster)
+int decode_attn_p_chunk();
+cudaError_t decode_attn_p(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
+                          int KV, int hd, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx,
+                          float* ws, int* tickets, int mch, int sms, cudaStream_t s);
+
 // Chunked-prefill attention (CHUNK mode): C query rows (cache indices c0 .. c0 + C - 1 of one
 // request, K/V already appended) attend causally to the request's paged cache; block_table_row =
 // that request's block table (device).  out rows [0, C) (ldo).

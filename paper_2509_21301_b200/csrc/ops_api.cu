@@ -87,6 +87,12 @@ int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_bl
                       tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo));
 }
 int nova_op_gemv_umma_splits(int N, int K, int epi) { return gemv_umma_plan(N, K, epi).P; }
+int nova_op_decode_attn_p(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
+                          int H, int KV, int hd, const int32_t* bt, int max_pages, const nova_decode_row* rows, int B,
+                          int max_ctx, float* ws, int32_t* tickets, int mch, int max_ctas, void* stream) {
+  return st(decode_attn_p((const bf16*)qkv, ld, (bf16*)out, ldo, (const bf16*)kv_pool, layer, n_pages, H, KV, hd, bt,
+                          max_pages, (const DecodeRow*)rows, B, max_ctx, ws, tickets, mch, max_ctas, S(stream)));
+}
 int nova_op_chunk_attn(const void* qkv, int ld, void* out, int ldo, int C, int c0, int H, int KV, int hd,
                        const void* kv_pool, int layer, int n_pages, const int32_t* block_table_row, void* stream) {
   return st(chunk_attn((const bf16*)qkv, ld, (bf16*)out, ldo, C, c0, H, KV, hd, (const bf16*)kv_pool, layer, n_pages,

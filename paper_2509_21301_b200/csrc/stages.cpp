@@ -263,7 +263,7 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
     fr.aws = dw.attn_ws, fr.atk = dw.tickets + 4096, fr.bar = dw.bar, fr.bar_base = dec_bar_base;
     fr.pool = pool, fr.n_pages = cfg.kv_pages, fr.max_pages = max_pages_per_req, fr.bt = d_bt, fr.rows = dw.rows;
     fr.last_tok = d_last, fr.tok_out = dw.tok, fr.store_logits = cfg.debug_keep_logits;
-    fr.mch = (s_max_of_public() + cfg.max_gen + 1 + decode_fused_phase_chunk() - 1) / decode_fused_phase_chunk();
+    fr.mch = attn_mch();
     // debug bisection (env NOVA_DEC_FUSED_STOP = k): the fused kernel runs phases < k (0 embed,
     // 1 + 5 l + {0 qkv, 1 attention, 2 o, 3 gate|up, 4 down}, 5 L + 1 lm_head), the per-op path
     // finishes the iteration from there (k = 1 + 5 l + {0, 2, 3, 4} or 5 L + 1)
@@ -327,8 +327,13 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
     {
       pass_work[1] += kv_bytes_layer;
       const int i = ktimer[1].begin(s);
-      CUDA_TRY(decode_attn(dw.qkv, ldq, dw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
-                           dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
+      if (g_dec_attn_p)  // persistent, sized to the partition (decode_attn_p.cu)
+        CUDA_TRY(decode_attn_p(dw.qkv, ldq, dw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt,
+                               max_pages_per_req, dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, attn_mch(), sms,
+                               s));
+      else
+        CUDA_TRY(decode_attn(dw.qkv, ldq, dw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
+                             dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
       ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
     }
   resume:
@@ -454,9 +459,9 @@ cudaError_t Engine::run_hybrid(const std::vector<Request*>& rq, const std::vecto
     CUDA_TRY(chunk_attn(hw.qkv, ldq, hw.attn, H * hd, C, c0, H, KV, hd, pool, l, cfg.kv_pages,
                         d_bt + (size_t)P->slot * max_pages_per_req, s));
     if (B > 0)
-      CUDA_TRY(decode_attn(hw.qkv + (size_t)C * ldq, ldq, hw.attn + (size_t)C * H * hd, H * hd, pool, l, cfg.kv_pages,
-                           H, KV, hd, d_bt, max_pages_per_req, hw.rows + C, B, max_ctx, dw.attn_ws, dw.tickets + 4096,
-                           s));
+      CUDA_TRY(decode_attn_p(hw.qkv + (size_t)C * ldq, ldq, hw.attn + (size_t)C * H * hd, H * hd, pool, l,
+                             cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req, hw.rows + C, B, max_ctx, dw.attn_ws,
+                             dw.tickets + 4096, attn_mch(), sms, s));
     CUDA_TRY(t_gemm(this, 1, NOVA_K_LLM_GEMM, hw.attn, H * hd, L.o_w, H * hd, hw.hid, D, nullptr, M, D, H * hd,
                     EPI_F32_RESID, sms, s));
     CUDA_TRY(rmsnorm(hw.hid, D, L.ln2, hw.xb, 0, D, M, D, m.rms_eps, s));

@@ -162,3 +162,10 @@ def nova_op_gemv_umma_splits(N: int, K: int, epi: int) -> int:
 def nova_op_chunk_attn(qkv, out, C, c0, H, KV, hd, kv_pool, layer, n_pages, block_table_row, stream=None):
     check(lib().nova_op_chunk_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), C, c0, H, KV, hd, _p(kv_pool), layer,
                                    n_pages, _p(block_table_row), _s(stream)), "chunk_attn")
+
+
+def nova_op_decode_attn_p(qkv, out, kv_pool, layer, n_pages, H, KV, hd, block_tables, rows, B, max_ctx, ws, tickets,
+                          mch, max_ctas=0, stream=None):
+    check(lib().nova_op_decode_attn_p(_p(qkv), qkv.stride(0), _p(out), out.stride(0), _p(kv_pool), layer, n_pages, H,
+                                      KV, hd, _p(block_tables), block_tables.shape[1], _p(rows), B, max_ctx, _p(ws),
+                                      _p(tickets), mch, max_ctas, _s(stream)), "decode_attn_p")

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r2v2_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2v2_pytest.log
+timeout 120 python __graft_entry__.py smoke 2>&1 | tail -1
+timeout 1800 python bench.py > gpurun_out/r2v2_bench.json 2> gpurun_out/r2v2_bench.err; echo "bench rc=$?"
+tail -2 gpurun_out/r2v2_bench.err
