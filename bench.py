@@ -556,7 +556,9 @@ def main():
                 ("multi_stream", dict(mode=E.MULTI_STREAM, b_max=16)),
                 # the paper's chunked-prefill baseline: hybrid prefill-chunk + decode batches,
                 # token budget 128 (the paper's best)
-                ("chunk_128", dict(mode=E.CHUNK, chunk_budget=128, b_max=16))]
+                ("chunk_128", dict(mode=E.CHUNK, chunk_budget=128, b_max=16)),
+                # the same adaptive policy, front passes repartitioned every 8 layers
+                ("adaptive_regroup8", dict(policy, front_regroup=8))]
         if plan.get("points"):   # Pareto point for the estimated arrival rate
             pols.append(("frontier", dict(mode=E.FRONTIER, b_max=16)))
         if kind == "poisson":    # cfg 2: the static SM-split sweep

@@ -154,6 +154,12 @@ typedef struct {
                                           nova_offload_floor); 0 = none                       */
   int32_t chunk_budget;                /* CHUNK: tokens per hybrid iteration (<= 0: 128;
                                           <= NOVA_CHUNK_MAX)                                  */
+  int32_t front_regroup;               /* STATIC / ADAPTIVE / FRONTIER: every
+                                          front_regroup layers a running vision / prefill pass
+                                          re-reads the split Eq. 5 (or the static / frontier rule)
+                                          gives now and moves to that split's front partition
+                                          (all SMs once no decode work is left); 0 = the paper's
+                                          per-pass granularity                        */
 } nova_partition_policy;
 /* Takes effect at each role's next forward pass.  `applied` (may be NULL)
  * receives the values rounded down to the granularity.  NOVA_E_PARTITION if a
@@ -231,6 +237,10 @@ nova_status nova_debug_logits(nova_engine* e, uint64_t req_id, int32_t index, fl
 /* Teacher forcing: decode step k (k >= 1) consumes tokens[k-1] instead of the argmax
  * of step k-1.  Must be called right after nova_submit. */
 nova_status nova_debug_force_tokens(nova_engine* e, uint64_t req_id, const int32_t* tokens, int32_t n);
+
+/* Front passes moved to another partition at a layer-group boundary so far (front_regroup, f4);
+ * -1 for a NULL engine. */
+int64_t nova_front_switches(nova_engine* e);
 
 /* Copy an internal decode workspace buffer to host memory (parity debugging; synchronizes the
  * device).  name: "dec_hid" (f32 [max_decode_batch][llm_dim]), "dec_xg" / "dec_xlo" (bf16

@@ -33,7 +33,8 @@ class Request(C.Structure):
 class PartitionPolicy(C.Structure):
     _fields_ = [("mode", I32), ("sm_decode_dv", I32), ("sm_decode_dp", I32), ("sm_op_dv", I32),
                 ("sm_op_dp", I32), ("sm_min", I32), ("alpha_dv", F32), ("alpha_dp", F32), ("b_max", I32),
-                ("pf_threshold", I32), ("sm_dv_floor", I32), ("chunk_budget", I32)]
+                ("pf_threshold", I32), ("sm_dv_floor", I32), ("chunk_budget", I32),
+                ("front_regroup", I32)]
 
 
 class StepInfo(C.Structure):
@@ -93,6 +94,7 @@ ENGINE_SIGNATURES = {
     "nova_release_request": (R, [E, U64]),
     "nova_debug_logits": (R, [E, U64, I32, C.POINTER(F32), I32]),
     "nova_debug_read_buffer": (R, [E, C.c_char_p, C.c_void_p, U64]),
+    "nova_front_switches": (I64, [E]),
     "nova_debug_force_tokens": (R, [E, U64, C.POINTER(I32), I32]),
     "nova_time_pass": (R, [E, I32, I32, I32, I32, I32, I32, I32, I32, I32, C.POINTER(F64)]),
     "nova_plan": (R, [C.POINTER(Curves), F64, F64, C.POINTER(PlanPoint), I32, C.POINTER(I32), C.POINTER(PlanPoint),

@@ -250,6 +250,13 @@ class Engine {
   KStat kstats[NOVA_K_COUNT];
   std::mutex kmu;
   int64_t pass_count[2] = {0, 0};
+  // §8(f) f4: front passes repartitioned every regroup_layers layers (0 = per pass) toward
+  // front_hint = the decode split the policy gives now for the front's context (0 = no decode work:
+  // all SMs to the front; -1 = none), published by step()
+  std::atomic<int> regroup_layers{0};
+  std::atomic<int> front_hint{-1};
+  std::atomic<long long> front_switches{0};
+  cudaEvent_t regroup_ev = nullptr;
   int sample_every = 0;              // 0 = kernel timing off; n = time every n-th pass of a role
   double pass_work[2] = {0, 0};      // algorithmic work of the last pass issued by each role
 
@@ -320,8 +327,14 @@ class Engine {
 
   // stage programs (model.cpp); return cudaError
   int front_sms(int s_dec) const { return s_dec <= 0 ? part.total : part.total - s_dec; }
-  cudaError_t run_encode(Request* r, cudaStream_t s, int sms);
-  cudaError_t run_prefill(Request* r, cudaStream_t s, int sms);
+  struct FrontRG {  // live repartition of one front pass (f4)
+    int s_dec;       // decode split the pass's partition leaves out (0 = all SMs)
+    int group;       // layers per group
+  };
+  // every stage program may move `s` / `sms` to another front partition when rg != null
+  cudaError_t run_encode(Request* r, cudaStream_t& s, int sms, FrontRG* rg = nullptr);
+  cudaError_t run_prefill(Request* r, cudaStream_t& s, int sms, FrontRG* rg = nullptr);
+  cudaError_t front_regroup(FrontRG* rg, cudaStream_t& s, int& sms);
   // decode SMs of a pass: the whole GPU when SOLO, else the partition's s_dec
   int dec_sms(int ctx, int s_dec) const { return (ctx == NOVA_CTX_SOLO || s_dec <= 0 || s_dec >= part.total) ? part.total : s_dec; }
   cudaError_t run_decode(const std::vector<Request*>& rows, const std::vector<int>& forced, cudaStream_t s, int sms);

@@ -173,11 +173,13 @@ void Worker::run() {
     Event done;
     done.reqs = c.reqs;
     done.key = c.reqs.empty() ? 0 : c.reqs[0]->id;
+    Engine::FrontRG rg{c.s_dec, eng->regroup_layers.load()};
+    Engine::FrontRG* rgp = (role == 0 && rg.group > 0) ? &rg : nullptr;
     if (c.kind == NOVA_DEC_VISION) {
-      e = eng->run_encode(c.reqs[0], s, eng->front_sms(c.s_dec));
+      e = eng->run_encode(c.reqs[0], s, eng->front_sms(c.s_dec), rgp);  // may move s (f4)
       done.kind = NOVA_EV_VISION_DONE;
     } else if (c.kind == NOVA_DEC_PREFILL) {
-      e = eng->run_prefill(c.reqs[0], s, eng->front_sms(c.s_dec));
+      e = eng->run_prefill(c.reqs[0], s, eng->front_sms(c.s_dec), rgp);
       done.kind = NOVA_EV_PREFILL_DONE;
     } else if (c.kind == NOVA_DEC_HYBRID) {
       e = eng->run_hybrid(c.reqs, c.forced_tok, s, eng->part.total);
@@ -315,6 +317,7 @@ nova_status Engine::finalize() {
   if (cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&upload_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(NOVA_E_CUDA, "streams");
+  if (cudaEventCreateWithFlags(&regroup_ev, cudaEventDisableTiming) != cudaSuccess) return fail(NOVA_E_CUDA, "events");
   ev_upload.assign(n_slots_total, nullptr);
   for (auto& ev : ev_upload)
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(NOVA_E_CUDA, "events");
@@ -400,6 +403,8 @@ void Engine::shutdown() {
     dfs = nullptr;
     part.destroy();
     for (auto ev : ev_upload) cudaEventDestroy(ev);
+    if (regroup_ev) cudaEventDestroy(regroup_ev);
+    regroup_ev = nullptr;
     for (auto ev : ev_loaded) cudaEventDestroy(ev);
     for (auto ev : ev_free) cudaEventDestroy(ev);
     if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -723,6 +728,14 @@ nova_status Engine::step(int64_t max_wait_us, nova_step_info* out) {
       last_info.context = d.ctx;
       last_info.decode_batch = (int)d.reqs.size();
     }
+  }
+  if (regroup_layers.load(std::memory_order_relaxed) > 0) {  // f4: the split the policy gives now
+    int hint = -1;
+    if (alg.vision_running || alg.prefill_running) {
+      const int ctx = alg.vision_running ? NOVA_CTX_DV : NOVA_CTX_DP;
+      hint = (alg.decode_busy || !alg.q_d.empty()) ? alg.split(ctx, alg.n_pend()) : 0;
+    }
+    front_hint.store(hint, std::memory_order_relaxed);
   }
   tick_no++;
   last_info.events = (int)evs.size();

@@ -139,6 +139,8 @@ nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, n
   if (q.b_max <= 0 || q.b_max > E.cfg.max_decode_batch) q.b_max = E.cfg.max_decode_batch;
   if (q.pf_threshold <= 0) q.pf_threshold = 5;
   if (q.chunk_budget <= 0) q.chunk_budget = 128;
+  if (q.front_regroup < 0) q.front_regroup = 0;
+  if (q.mode != NOVA_MODE_STATIC && q.mode != NOVA_MODE_ADAPTIVE && q.mode != NOVA_MODE_FRONTIER) q.front_regroup = 0;
   q.sm_dv_floor = q.sm_dv_floor <= 0 ? 0 : std::min(rnd(q.sm_dv_floor), mx);
   if (q.mode == NOVA_MODE_STATIC && (q.sm_decode_dv < g || q.sm_decode_dp < g || q.sm_decode_dv > mx ||
                                      q.sm_decode_dp > mx))
@@ -147,6 +149,7 @@ nova_status nova_set_partition(nova_engine* e, const nova_partition_policy* p, n
                                        q.sm_op_dv > mx || q.sm_op_dp > mx || q.alpha_dv < 0 || q.alpha_dp < 0))
     return E.fail(NOVA_E_PARTITION, "adaptive budgets outside [granularity, max split]");
   E.alg.pol = q;
+  E.regroup_layers.store(q.front_regroup);
   if (applied) *applied = q;
   return NOVA_OK;
 }
@@ -218,6 +221,8 @@ nova_status nova_debug_logits(nova_engine* e, uint64_t id, int32_t index, float*
   std::memcpy(out, L[index].data(), (size_t)vocab * 4);
   return NOVA_OK;
 }
+
+int64_t nova_front_switches(nova_engine* e) { return e ? (int64_t)e->e.front_switches.load() : -1; }
 
 nova_status nova_debug_read_buffer(nova_engine* e, const char* name, void* out, uint64_t bytes) {
   if (!e || !name || !out) return NOVA_E_INVAL;

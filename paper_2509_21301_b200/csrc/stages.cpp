@@ -105,7 +105,23 @@ static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, 
 }
 
 // ---------------------------------------------------------------- vision encode (a5)
-cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
+// §8(f) f4: at a layer-group boundary, move the rest of the front pass to the partition the policy
+// gives now (the paper fixes it per pass): the stream switch is an event edge, so kernel order
+// and results are unchanged (every kernel is partition-invariant).
+cudaError_t Engine::front_regroup(FrontRG* rg, cudaStream_t& s, int& sms) {
+  const int want = front_hint.load(std::memory_order_relaxed);
+  if (want < 0 || want == rg->s_dec) return cudaSuccess;
+  CUDA_TRY(cudaEventRecord(regroup_ev, s));
+  cudaStream_t ns = stream_for(0, NOVA_CTX_DV, want);
+  CUDA_TRY(cudaStreamWaitEvent(ns, regroup_ev, 0));
+  s = ns;
+  sms = front_sms(want);
+  rg->s_dec = want;
+  front_switches.fetch_add(1, std::memory_order_relaxed);
+  return cudaSuccess;
+}
+
+cudaError_t Engine::run_encode(Request* r, cudaStream_t& s, int sms, FrontRG* rg) {
   const auto& m = dims.m;
   const int gh = r->gh, gw = r->gw, N = gh * gw, Dv = m.vit_dim, hd = dims.vit_hd;
   const int H = gh * m.patch, Wd = gw * m.patch;
@@ -116,6 +132,7 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
                   Dv, dims.patch_dim, EPI_F32_STORE, sms, s));
   const int L = m.vit_depth;
   for (int l = 0; l < L; ++l) {
+    if (rg && l > 0 && l % rg->group == 0) CUDA_TRY(front_regroup(rg, s, sms));
     bf16* blk;
     int k = 0;
     if (vit_K > 0) {  // Eq. 7 ring: the slot that received logical layer l
@@ -166,7 +183,7 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t s, int sms) {
 }
 
 // ---------------------------------------------------------------- LLM prefill (a6)
-cudaError_t Engine::run_prefill(Request* r, cudaStream_t s, int sms) {
+cudaError_t Engine::run_prefill(Request* r, cudaStream_t& s, int sms, FrontRG* rg) {
   const auto& m = dims.m;
   const int D = m.llm_dim, H = m.llm_heads, KV = m.llm_kv_heads, hd = m.head_dim, F = m.llm_ffn;
   const int nv = r->n_v(), S = r->S(), ldq = dims.llm_qkv_n;
@@ -187,6 +204,7 @@ cudaError_t Engine::run_prefill(Request* r, cudaStream_t s, int sms) {
                  D, r->n_prompt, s));
   bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
   for (int l = 0; l < m.llm_layers; ++l) {
+    if (rg && l > 0 && l % rg->group == 0) CUDA_TRY(front_regroup(rg, s, sms));
     const LlmLayerW& L = W.llm[l];
     CUDA_TRY(rmsnorm(fw.hid, D, L.ln1, fw.xb, 0, D, S, D, m.rms_eps, s));
     CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.xb, D, L.qkv_w, D, fw.qkv, ldq, L.qkv_b, S, ldq, D, EPI_BF16, sms, s));

@@ -144,9 +144,9 @@ class Engine:
 
     def set_partition(self, mode=ADAPTIVE, sm_decode_dv=72, sm_decode_dp=72, sm_op_dv=48, sm_op_dp=48, sm_min=16,
                       alpha_dv=8.0, alpha_dp=8.0, b_max=0, pf_threshold=5, sm_dv_floor=0,
-                      chunk_budget=128) -> A.PartitionPolicy:
+                      chunk_budget=128, front_regroup=0) -> A.PartitionPolicy:
         p = A.PartitionPolicy(mode, sm_decode_dv, sm_decode_dp, sm_op_dv, sm_op_dp, sm_min, alpha_dv, alpha_dp, b_max,
-                              pf_threshold, sm_dv_floor, chunk_budget)
+                              pf_threshold, sm_dv_floor, chunk_budget, front_regroup)
         out = A.PartitionPolicy()
         self._check(self.lib.nova_set_partition(self.h, C.byref(p), C.byref(out)), "nova_set_partition")
         return out

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--trace", default="mmpp", choices=["mmpp", "poisson"],
                     help="mmpp: cfg 3 bursty mix; poisson: cfg 2 (52x94 screenshots, prompt 64, gen 48)")
     ap.add_argument("--static", type=int, nargs="*", default=[], help="static decode splits (both contexts)")
+    ap.add_argument("--regroup", type=int, nargs="*", default=[],
+                    help="adaptive_plan with front passes repartitioned every N layers (SURVEY §8(f) f4)")
     a = ap.parse_args()
     import torch
     from synth import Q7B, Q2B
@@ -67,6 +69,7 @@ def main():
             continue
         pols.append((f"adaptive_smin{smin}", dict(mode=E.ADAPTIVE, sm_op_dv=sv, sm_op_dp=sp, sm_min=smin,
                                                   alpha_dv=(sv - smin) / 3.0, alpha_dp=(sp - smin) / 3.0, b_max=16)))
+    pols += [(f"adaptive_regroup{n}", dict(pols[0][1], front_regroup=n)) for n in a.regroup]
     base = {"serial": dict(mode=E.SERIAL, b_max=16), "multi_stream": dict(mode=E.MULTI_STREAM, b_max=16),
             "chunk_128": dict(mode=E.CHUNK, chunk_budget=128, b_max=16),
             "pf_limit_5": dict(mode=E.PF_LIMIT, pf_threshold=5, b_max=16)}
@@ -77,6 +80,7 @@ def main():
             eng.set_partition(**pol)
             rs = []
             t_pol = time.time()
+            sw0 = eng.lib.nova_front_switches(eng.h)
             for k, tr in enumerate(trs):
                 inputs = BN.make_inputs(SHAPE, tr, 400 + k, 0, True)
                 r = BN.replay(eng, inputs)
@@ -85,6 +89,7 @@ def main():
             print(json.dumps({"rho": rho, "policy": name,
                               **{k: round(statistics.mean(x[k] for x in rs), 2) for k in rs[0]},
                               "per_seed_max": [round(x["max"], 1) for x in rs],
+                              "front_switches": eng.lib.nova_front_switches(eng.h) - sw0,
                               "wall_s": round(time.time() - t_pol, 1)}), flush=True)
     eng.close()
     torch.cuda.synchronize()

@@ -3,8 +3,8 @@ oracle on the same generated weights and inputs (SURVEY.md §8(c) c1', c6).
 
 - cfg 1 tiny VLM: greedy tokens identical, logits max-abs <= 3e-2 (BASELINE).
 - co-execution == serial: tokens and f32 logits bitwise identical across SERIAL,
-  STATIC splits, ADAPTIVE, the frontier-lookup controller and the paper's PF-Limit /
-  Multi-Stream baselines on a
+  STATIC splits, ADAPTIVE (also with front passes repartitioned every layer, §8(f) f4), the
+  frontier-lookup controller and the paper's PF-Limit / Multi-Stream baselines on a
   20-request trace (BASELINE).
 - offload: K = 2, 3, 4 physical ViT layers give bitwise the all-resident outputs over several
   vision passes, with a depth (7) that no K divides (the ring's slots rotate across passes).
@@ -96,6 +96,8 @@ def test_coexec_bitwise_equals_serial(tiny_setup):
                       ("static56", dict(mode=E.STATIC, sm_decode_dv=56, sm_decode_dp=104)),
                       ("adaptive", dict(mode=E.ADAPTIVE, sm_op_dv=48, sm_op_dp=40, sm_min=8, alpha_dv=13.0,
                                         alpha_dp=10.0, b_max=5)),
+                      ("adaptive_regroup", dict(mode=E.ADAPTIVE, sm_op_dv=48, sm_op_dp=40, sm_min=8, alpha_dv=13.0,
+                                                alpha_dp=10.0, b_max=5, front_regroup=1)),   # f4: per layer
                       ("pf_limit", dict(mode=E.PF_LIMIT, pf_threshold=3)),
                       ("multi_stream", dict(mode=E.MULTI_STREAM)),
                       ("frontier", dict(mode=E.FRONTIER))]:
