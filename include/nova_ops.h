@@ -165,7 +165,10 @@ int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_
  * (nova_op_gemv_umma_splits).  max_ctas = SM budget of the partition (0 = whole GPU). */
 int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
                       const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
-                      void* stream);
+                      const float* norm_hid, float norm_eps, void* stream);
+/* norm_hid != NULL (epi NOVA_EPI_BF16_SILUMUL only): RMSNorm folded after the GEMV (DESIGN R25) -- X
+ * holds x~ = bf16(h * gamma) and every output row b is scaled by rsqrt(mean_k h[b][k]^2 + norm_eps),
+ * h = norm_hid [B][K] f32, before SiLU(gate) * up. */
 int nova_op_gemv_umma_splits(int N, int K, int epi);
 
 /* keys[r] (from NOVA_EPI_F32_ARGMAX) -> out_tok[r]; also last_tok[rows[r].slot] (rows != NULL)

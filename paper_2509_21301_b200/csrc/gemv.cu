@@ -319,7 +319,10 @@ __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const void* __restrict
           if constexpr (EPI == EPI_BF16) {
             reinterpret_cast<bf16*>(Y)[(size_t)b * ldy + n] = __float2bfloat16_rn(v);
           } else if constexpr (EPI == EPI_F32_RESID) {
-            reinterpret_cast<float*>(Y)[(size_t)b * ldy + n] += v;
+            float* yp = reinterpret_cast<float*>(Y) + (size_t)b * ldy + n;
+            const float h = *yp + v;
+            *yp = h;
+            if (aux.nxout) aux.nxout[(size_t)b * aux.ldnx + n] = __float2bfloat16_rn(h * __bfloat162float(aux.ngamma[n]));
           } else {
             reinterpret_cast<float*>(Y)[(size_t)b * ldy + n] = v;
           }

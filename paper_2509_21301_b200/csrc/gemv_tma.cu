@@ -391,7 +391,11 @@ __global__ void __launch_bounds__(32 * (1 + PCfg<RB, XHL>::NWC), GEMV_CPS) gemv_
           if constexpr (EPI == EPI_BF16) {
             reinterpret_cast<bf16*>(a.Y)[(size_t)b * a.ldy + n] = __float2bfloat16_rn(v);
           } else if constexpr (EPI == EPI_F32_RESID) {
-            reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + n] += v;
+            float* yp = reinterpret_cast<float*>(a.Y) + (size_t)b * a.ldy + n;
+            const float h = *yp + v;
+            *yp = h;
+            if (a.aux.nxout)
+              a.aux.nxout[(size_t)b * a.aux.ldnx + n] = __float2bfloat16_rn(h * __bfloat162float(a.aux.ngamma[n]));
           } else {
             reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + n] = v;
           }

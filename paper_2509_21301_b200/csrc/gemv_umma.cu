@@ -73,6 +73,8 @@ struct UArgs {
   int* tickets;      // [N / 128] (zero on entry, left zero)
   int N, K, B, ldy, ks, P, blocks;
   unsigned long long* keys;  // EPI_F32_ARGMAX
+  const float* nhid;         // RMSNorm folded (R25): residual rows [B][K] (null = off)
+  float neps;
 };
 
 // unit i of this CTA: whole-block rounds first (split partials summed in registers), then split units
@@ -105,6 +107,8 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  float* s_inv = reinterpret_cast<float*>(s_last + 3);  // [16] RMSNorm row scales (16-byte aligned)
+  float* s_red = s_inv + 16;                             // [4][16] warp partials
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
@@ -220,6 +224,26 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
     pdl_wait();  // epilogues read / write activations of the previous kernels
     const int quarter = warp & 3, et = threadIdx.x - 64;  // et: epilogue thread 0..127
     const int r = quarter * 32 + lane;                     // row within the block
+    if (a.nhid) {
+      // RMSNorm row scales (R25), while the first MMAs run: thread et sums float4 chunks et, et + 128,
+      // ... in order, xor butterfly per warp, warps combined ((w0 + w1) + w2) + w3 -- one fixed order
+      const int nch = a.K / 4, ew = et >> 5;
+      for (int b = 0; b < a.B; ++b) {
+        const float4* hr = reinterpret_cast<const float4*>(a.nhid + (size_t)b * a.K);
+        float sq = 0.f;
+        for (int q = et; q < nch; q += 128) {
+          const float4 h4 = __ldcg(hr + q);
+          sq += (h4.x * h4.x + h4.y * h4.y) + (h4.z * h4.z + h4.w * h4.w);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) s_red[ew * 16 + b] = sq;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et < a.B)
+        s_inv[et] = rsqrtf((((s_red[et] + s_red[16 + et]) + s_red[32 + et]) + s_red[48 + et]) / (float)a.K + a.neps);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
     int acc = 0;
     uint32_t aphase = 0;
     float sum[16];
@@ -268,6 +292,10 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
       }
       // ---- epilogues (row n, batch columns b < B)
       if constexpr (EPI == EPI_BF16_SILUMUL) {
+        if (a.nhid) {
+#pragma unroll
+          for (int b = 0; b < 16; ++b) v[b] *= b < a.B ? s_inv[b] : 0.f;
+        }
         // rows interleave 16 gate | 16 up: lane l < 16 (gate) pairs with lane l + 16 (up)
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
@@ -392,7 +420,7 @@ bool gemv_umma_supported(int N, int K, int epi) {
 
 cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int K, void* Y, int ldy, const bf16* bias,
                       int B, int epi, float* ws, int* tickets, cudaStream_t s, int sms, unsigned long long* keys,
-                      const bf16* X_lo) {
+                      const bf16* X_lo, const float* norm_hid, float norm_eps) {
   if (B <= 0) return cudaSuccess;
   if (B > 16 || !gemv_umma_supported(N, K, epi) || ldx % 8 || !W_blocked) return cudaErrorInvalidValue;
   if (epi == EPI_F32_ARGMAX && (!keys || !X_lo)) return cudaErrorInvalidValue;
@@ -405,7 +433,8 @@ cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int 
   } else {
     mx2 = mx;
   }
-  UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks, pl.P, N / RB, keys};
+  if (norm_hid && (epi != EPI_BF16_SILUMUL || K % 4)) return cudaErrorInvalidValue;
+  UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks, pl.P, N / RB, keys, norm_hid, norm_eps};
   if (X_lo) {
     if (epi == EPI_F32_ARGMAX) return ulaunch<EPI_F32_ARGMAX, 1>(mx, mx2, a, sms, s);
     if (epi == EPI_F32_STORE) return ulaunch<EPI_F32_STORE, 1>(mx, mx2, a, sms, s);

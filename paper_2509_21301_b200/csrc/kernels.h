@@ -92,9 +92,11 @@ extern bool g_use_tma_gemv;
 extern int g_dec_umma;  // env NOVA_DEC_UMMA (default 1): decode linears on gemv_umma where supported
 GemvTmaPlan gemv_umma_plan(int N, int K, int epi);
 bool gemv_umma_supported(int N, int K, int epi);
+// norm_hid != null (EPI_BF16_SILUMUL): X is x~ = bf16(h * gamma) and every output row b is scaled by
+// rsqrt(mean_k h[b][k]^2 + eps) after the GEMV (h = norm_hid rows, ld D) -- RMSNorm folded (R25).
 cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int K, void* Y, int ldy, const bf16* bias,
                       int B, int epi, float* ws, int* tickets, cudaStream_t s, int sms, unsigned long long* keys,
-                      const bf16* X_lo);
+                      const bf16* X_lo, const float* norm_hid = nullptr, float norm_eps = 0.f);
 extern int g_dec_tma_mask;  // decode linears on the persistent TMA GEMV: bit 0 qkv, 1 o, 2 gate|up, 3 down, 4 lm_head
 
 // Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).
@@ -129,6 +131,11 @@ struct GemvAux {
   const int* bt = nullptr;
   int max_pages = 0;
   unsigned long long* keys = nullptr;  // EPI_F32_ARGMAX: [B] packed (ordered logit, ~index), zero on entry
+  // EPI_F32_RESID, next-norm prep (DESIGN R25): also write nxout[b][n] = bf16(Y_new[b][n] * ngamma[n])
+  // -- the next linear contracts W . x~ and applies the RMSNorm row scale after the GEMV
+  const bf16* ngamma = nullptr;
+  bf16* nxout = nullptr;
+  int ldnx = 0;
 };
 // x modes: 0 bf16, 1 f32 (hi/lo split), 2 f32 residual + RMSNorm on load -> bf16, 3 same -> hi/lo
 cudaError_t gemv_ex(const void* X, int xmode, int ldx, const bf16* W, int N, int K, void* Y, int ldy,

@@ -82,9 +82,9 @@ int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_
 }
 int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
                       const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
-                      void* stream) {
+                      const float* norm_hid, float norm_eps, void* stream) {
   return st(gemv_umma((const bf16*)X, ldx, (const bf16*)W_blocked, N, K, Y, ldy, (const bf16*)bias, B, epi, ws,
-                      tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo));
+                      tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo, norm_hid, norm_eps));
 }
 int nova_op_gemv_umma_splits(int N, int K, int epi) { return gemv_umma_plan(N, K, epi).P; }
 int nova_op_decode_attn_p(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,

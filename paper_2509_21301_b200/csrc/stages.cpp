@@ -12,6 +12,9 @@
 
 namespace nova {
 
+// env NOVA_FOLD_NORM=0 keeps the standalone RMSNorm kernel before gate|up (A/B switch)
+static const int g_fold_norm = getenv("NOVA_FOLD_NORM") ? atoi(getenv("NOVA_FOLD_NORM")) : 1;
+
 #define CUDA_TRY(x)                   \
   do {                                \
     cudaError_t _e = (x);             \
@@ -77,27 +80,33 @@ static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xmode, int ldx,
   return cudaSuccess;
 }
 
+// Which decode linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 1 o, 2 gate|up,
+// 3 down, 4 lm_head); the choice depends on the op only, never on the partition (co-execution is
+// bitwise == serial).  Default gate|up + lm_head (scripts/gpu_r2_u3.sh, decode iterations on
+// 24..148-SM partitions: 2B 3.25 -> 3.12 ms on 24 SMs, 1.79 -> 1.71 on 64, level on the full GPU;
+// down / o on tcgen05 win on <= 48-SM slices but lose 10-25% on larger grids).
+static int umma_mask() {
+  static const int m = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 20;
+  return g_dec_umma ? m : 0;
+}
+
 // TMA-streamed decode linear (bf16 x): gate|up, where it streams at ~99% of HBM (scripts/kbench.py)
 static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, const bf16* Wb, int N, int K, void* Y,
                               int ldy, const bf16* bias, int B, int epi, int sms, const GemvAux* aux, cudaStream_t s,
-                              const bf16* X_lo = nullptr, int cls = NOVA_K_DEC_GEMV) {
+                              const bf16* X_lo = nullptr, int cls = NOVA_K_DEC_GEMV, const float* norm_hid = nullptr,
+                              float norm_eps = 0.f) {
   const int nout = epi == EPI_BF16_SILUMUL ? N / 2 : N;
   const int ysz = epi == EPI_F32_RESID ? 8 : ((epi == EPI_F32_STORE || epi == EPI_F32_ARGMAX) ? 4 : 2);
   const double bytes = (double)N * K * 2 + (double)B * K * (X_lo ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  // which linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 1 o, 2 gate|up, 3 down,
-  // 4 lm_head); the choice depends on the op only, never on the partition (bitwise co-execution)
-  // Default gate|up + lm_head (scripts/gpu_r2_u3.sh, decode iterations on 24..148-SM partitions: 2B
-  // 3.25 -> 3.12 ms on 24 SMs, 1.79 -> 1.71 on 64, level on the full GPU; down / o on tcgen05 win
-  // on <= 48-SM slices but lose 10-25% on larger grids, which decode also runs on).
-  static const int umask = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 20;
   const int op_bit = epi == EPI_BF16_SILUMUL ? 4 : epi == EPI_F32_ARGMAX ? 16 : (K > N ? 8 : 2);
-  if (g_dec_umma && (umask & op_bit) && Wb && gemv_umma_supported(N, K, epi) && (epi != EPI_F32_ARGMAX || X_lo)) {
+  if ((umma_mask() & op_bit) && Wb && gemv_umma_supported(N, K, epi) && (epi != EPI_F32_ARGMAX || X_lo)) {
     // tcgen05 consumer (gemv_umma.cu): the same contract, the ring stage released by the MMA commit
     CUDA_TRY(gemv_umma(X, ldx, Wb, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms,
-                       aux ? aux->keys : nullptr, X_lo));
+                       aux ? aux->keys : nullptr, X_lo, norm_hid, norm_eps));
   } else {
+    if (norm_hid) return cudaErrorInvalidValue;  // the folded RMSNorm needs the tcgen05 GEMV
     CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms, aux, Wb, X_lo));
   }
   E->ktimer[1].end(i, cls, bytes, s);
@@ -355,19 +364,25 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
       ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
     }
   resume:
+    // RMSNorm(ln2) folded (R25) when gate|up runs on gemv_umma and o on the mma.sync GEMVs: the o-proj
+    // residual epilogue writes x~ = bf16(h * ln2) into dw.xb, gate|up scales rows by rsqrt(mean h^2 + eps)
+    const bool fold = (tm & 4) && (umma_mask() & 4) && !(umma_mask() & 2) && sub == 0 &&
+                      gemv_umma_supported(2 * F, D, EPI_BF16_SILUMUL) && g_fold_norm;
     if (sub <= 2) {
+    GemvAux oa;
+    if (fold) oa.ngamma = L.ln2, oa.nxout = dw.xb, oa.ldnx = D;
     if (tm & 2)
       CUDA_TRY(t_gemv_tma(this, dw.attn, H * hd, L.o_w, L.o_wb, D, H * hd, dw.hid, D, nullptr, B, EPI_F32_RESID, sms,
-                          nullptr, s));
+                          &oa, s));
     else
       CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.attn, 0, H * hd, L.o_w, D, H * hd, dw.hid, D, nullptr, B,
-                      EPI_F32_RESID, plain, s));
+                      EPI_F32_RESID, oa, s));
     }
     if (sub <= 3) {
     if (tm & 4) {
-      CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
+      if (!fold) CUDA_TRY(rmsnorm(dw.hid, D, L.ln2, dw.xb, 0, D, B, D, m.rms_eps, s));
       CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.gu_w, L.gu_wb, 2 * F, D, dw.act, F, nullptr, B, EPI_BF16_SILUMUL, sms,
-                          nullptr, s));
+                          nullptr, s, nullptr, NOVA_K_DEC_GEMV, fold ? dw.hid : nullptr, m.rms_eps));
     } else {
       GemvAux na;
       na.gamma = L.ln2;

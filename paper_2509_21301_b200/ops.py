@@ -145,14 +145,15 @@ def nova_op_gemv_stream(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_
 
 
 def nova_op_gemv_umma(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_ctas=0, ldx=None, ldy=None,
-                      stream=None):
+                      norm_hid=None, norm_eps=0.0, stream=None):
     dev = X.device
     if dev not in _ws_cache:
         _ws_cache[dev] = (torch.empty(16 * 16 * 160000, dtype=torch.float32, device=dev),
                           torch.zeros(8192, dtype=torch.int32, device=dev))
     ws, tk = _ws_cache[dev]
     check(lib().nova_op_gemv_umma(_p(X), _p(X_lo), ldx or X.stride(0), _p(Wb), N, K, _p(Y), ldy or Y.stride(0),
-                                  _p(bias), B, epi, _p(ws), _p(tk), _p(keys), max_ctas, _s(stream)), "gemv_umma")
+                                  _p(bias), B, epi, _p(ws), _p(tk), _p(keys), max_ctas, _p(norm_hid), float(norm_eps),
+                                  _s(stream)), "gemv_umma")
 
 
 def nova_op_gemv_umma_splits(N: int, K: int, epi: int) -> int:

@@ -103,3 +103,34 @@ def test_umma_lm_head_hi_lo_argmax():
     assert rel_inf(lg, ref) <= 1e-4
     assert tok.cpu().numpy().tolist() == [V.argmax_lowest(lg[b]) for b in range(B)]
     assert int(keys.abs().sum().item()) == 0
+
+
+@pytest.mark.parametrize("F,D,B", [(8960, 1536, 2), (8960, 1536, 16), (192, 128, 3)])
+def test_umma_gate_up_with_folded_rmsnorm(F, D, B):
+    """DESIGN R25: x~ = bf16(h * gamma) through the GEMV, rows scaled by rsqrt(mean h^2 + eps) after it
+    == RMSNorm(h) then gate|up (oracle rms_norm / linear / silu), bf16 rel-inf <= 8e-3; and bitwise
+    invariant to the SM budget."""
+    rng = np.random.default_rng(F + B)
+    G = rand_bf16(rng, (F, D), D ** -0.5)
+    U = rand_bf16(rng, (F, D), D ** -0.5)
+    Wgu = np.empty((2 * F, D), dtype=np.float32)
+    for i in range(F // 16):
+        Wgu[32 * i:32 * i + 16] = G[16 * i:16 * i + 16]
+        Wgu[32 * i + 16:32 * i + 32] = U[16 * i:16 * i + 16]
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    gam = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (D,), 0.1) + 1.0))
+    h = (rng.standard_normal((B, D)) * 3).astype(np.float32)
+    xt = bf16_bits_to_f32(f32_to_bf16_bits(h * gam))                      # x~ = bf16(h * gamma)
+    Wb = _blocked(Wgu, 2 * F, D)
+    dh, dx = torch.from_numpy(h).cuda(), bf16_dev(xt)
+    outs = []
+    for ctas in (0, 24):
+        act = torch.empty(B, F, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_gemv_umma(dx, Wb, act, None, 2 * F, D, B, O.EPI_BF16_SILUMUL, max_ctas=ctas, norm_hid=dh,
+                            norm_eps=1e-6)
+        torch.cuda.synchronize()
+        outs.append(act)
+    assert torch.equal(outs[0], outs[1])
+    xn = V.rms_norm(h.astype(np.float64), gam, 1e-6)
+    ref = V.silu(V.linear(xn, G.astype(np.float64))) * V.linear(xn, U.astype(np.float64))
+    assert rel_inf(bf16_host(outs[0]), ref) <= 8e-3
