@@ -279,12 +279,12 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
         __threadfence();
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
-          float q8[8];
+          float q8[16];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) q8[q] = (b < a.B && q < a.P) ? __ldcg(&a.ws[((size_t)q * a.B + b) * a.N + n]) : 0.f;
+          for (int q = 0; q < 16; ++q) q8[q] = (b < a.B && q < a.P) ? __ldcg(&a.ws[((size_t)q * a.B + b) * a.N + n]) : 0.f;
           float s = 0.f;
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < 16; ++q)
             if (q < a.P) s += q8[q];
           v[b] = s;
         }
@@ -398,8 +398,9 @@ GemvTmaPlan gemv_umma_plan(int N, int K, int epi) {
   const int blocks = N / RB;
   static const int target = getenv("NOVA_UMMA_UNITS") ? atoi(getenv("NOVA_UMMA_UNITS")) : 128;
   int bestP = 1;
+  static const int maxp = getenv("NOVA_UMMA_MAXP") ? atoi(getenv("NOVA_UMMA_MAXP")) : 8;
   if (epi != EPI_F32_ARGMAX) {
-    for (int P = 1; P <= 8; ++P) {
+    for (int P = 1; P <= maxp; ++P) {
       const int ks = ((K + P - 1) / P + KC - 1) / KC * KC;
       if ((K + ks - 1) / ks != P || (P > 1 && ks < 256)) continue;
       bestP = P;
