@@ -157,12 +157,13 @@ int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_
 
 /* The same decode linear on the 5th-generation tensor cores (gemv_umma.cu): weights in the
  * streaming layout as the M = 128 tcgen05 operand, x as N = 16, one thread issuing the MMAs whose
- * commit frees each ring stage; 128-row blocks with a shape-only K split (results bitwise
- * independent of max_ctas and of the batch composition, not bitwise equal to nova_op_gemv_stream:
- * another accumulation order).  N % 128 == 0, K % 64 == 0, B <= 16; epi NOVA_EPI_BF16,
+ * commit frees each ring stage; 128-row blocks whose K range is cut into P shape-only chunks, the
+ * result being the left fold of the chunk partials, the blocks x P chunks dealt out to the CTAs as
+ * equal contiguous ranges (stream-K) -- results bitwise independent of max_ctas and of the batch
+ * composition, not bitwise equal to nova_op_gemv_stream (another accumulation order).  N % 128 == 0, K % 64 == 0, B <= 16; epi NOVA_EPI_BF16,
  * NOVA_EPI_BF16_SILUMUL, NOVA_EPI_F32_RESID, NOVA_EPI_F32_STORE, or NOVA_EPI_F32_ARGMAX with X_lo.
- * ws: P * B * N floats and tickets: N / 128 ints (zeroed, left zero) when the plan splits K
- * (nova_op_gemv_umma_splits).  max_ctas = SM budget of the partition (0 = whole GPU). */
+ * ws: P * B * N floats (P * N <= 2^20) and tickets: N / 128 ints (zeroed, left zero) when the plan
+ * cuts K into P > 1 chunks (nova_op_gemv_umma_splits).  max_ctas = SM budget of the partition (0 = whole GPU). */
 int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
                       const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
                       const float* norm_hid, float norm_eps, void* stream);

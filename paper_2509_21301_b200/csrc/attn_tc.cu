@@ -955,7 +955,10 @@ NOVA_DEV float2 exp2_fma2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x)),
                      __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y)));
 }
-constexpr int EXP_POLY_OF_8 = 2;  // pairs of P per 8 whose exponentials run on the FMA pipe
+#ifndef NOVA_EXP_POLY
+#define NOVA_EXP_POLY 2
+#endif
+constexpr int EXP_POLY_OF_8 = NOVA_EXP_POLY;  // pairs of P per 8 whose exponentials run on the FMA pipe
 constexpr int KST4 = 4;    // K / V ring depth
 template <int HD>
 struct Ft4Cfg {

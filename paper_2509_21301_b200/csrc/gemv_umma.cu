@@ -19,10 +19,17 @@
 //  * warps 2-5: epilogue, one output row per thread (tcgen05.ld 32x32b.x16), double-buffered
 //    accumulators so unit i's epilogue overlaps unit i+1's MMAs;
 //  * 3 stages x 16 KB of weights per CTA, 4 CTAs per SM (3 for the hi/lo lm_head) = 192 KB in
-//    flight per SM;
-//  * work decomposition (128-row block x K split P) from the shape only; split partials summed in
-//    split order (in registers for whole-block units, through the workspace + ticket otherwise), so
-//    the result is bitwise independent of the grid (the partition) and of the batch composition.
+//    flight per SM -- the bulk-copy probe's best ring (4 x 3 x 16 KB: 5.1 TB/s on a 24-SM slice);
+//  * work decomposition: a 128-row block's K range is cut into P chunks of CK k-steps (CK, P from
+//    the shape only) and the block's result is the LEFT FOLD of its chunk partials
+//    c_0 + c_1 + ... + c_{P-1} (each c_q one TMEM accumulation).  The grid decides only who computes
+//    what: each CTA takes R = blocks / G whole blocks (folded in registers) plus an equal contiguous
+//    share of the remaining blocks' items (stream-K); a CTA writes its prefix fold (a share that
+//    starts a block) or its single chunk partials (one that starts mid-block) to the workspace for a
+//    block it shares, and the last contributor (ticket) completes the same left fold -- so the result
+//    is bitwise independent of the grid (the partition) and of the batch composition.  Shared blocks
+//    are processed first (their tickets hide behind the stream), whole blocks last.
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -40,17 +47,62 @@ constexpr int KC = 64;               // k per stage (one 128-byte swizzle atom r
 constexpr int W_BYTES = RB * KC * 2; // 16 KB
 constexpr int X_BYTES = 16 * KC * 2; // 2 KB (UMMA N = 16)
 constexpr int NTHR = 192;            // producer, MMA, 4 epilogue warps
-constexpr int TMEM_COLS = 32;        // two 16-column accumulators
+constexpr int NACC = 4;              // TMEM accumulators (16 columns each): MMAs run up to 3 items ahead
+constexpr int TMEM_COLS = NACC * 16;
 
-template <int XHL>
+// ring shapes (same shared memory per SM): RING 0 = 3 stages x 4 CTAs per SM, 1 = 6 x 2, 2 = 12 x 1
+// (hi/lo x: 3 x 3, 5 x 2, 10 x 1)
+template <int XHL, int RING>
 struct UCfg {
-  static constexpr int ST = 3;
-  static constexpr int CPS = XHL ? 3 : 4;                     // CTAs per SM of the partition
+  static constexpr int ST = RING == 0 ? 3 : RING == 1 ? (XHL ? 5 : 6) : (XHL ? 10 : 12);
+  static constexpr int CPS = RING == 0 ? (XHL ? 3 : 4) : RING == 1 ? 2 : 1;  // CTAs per SM of the partition
   static constexpr int STAGE = W_BYTES + (1 + XHL) * X_BYTES;
   static constexpr int SMEM = 1024 + ST * STAGE + 512;
 };
 
 NOVA_DEV float silu_u(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
+
+// One ring stage on the tensor core, one elect for the whole stage: 4 MMAs (K = 16 each, +32 B
+// along K = +2 in the descriptors' 16-byte address field) into the accumulator at tmem_d (the first
+// one overwrites it when acc0 == 0), then the commit that frees the stage.  The per-MMA
+// elect / collective / descriptor moves cost ~150 ns per 16 KB stage otherwise.
+NOVA_DEV void umma_stage_x4(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0, uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n .reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      " setp.ne.b32 p, %4, 0;\n"
+      " add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"
+      " add.s64 b1, %2, 2;\n add.s64 b2, %2, 4;\n add.s64 b3, %2, 6;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n}\n" ::"r"(tmem_d),
+      "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(smem_u32(bar))
+      : "memory");
+}
+// hi / lo x (two B operands at b0 and b0 + lo): 8 MMAs
+NOVA_DEV void umma_stage_x8(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint64_t lo, uint32_t idesc, uint32_t acc0,
+                            uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n .reg .b64 a1, a2, a3, b1, b2, b3, c0, c1, c2, c3;\n"
+      " setp.ne.b32 p, %4, 0;\n"
+      " add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"
+      " add.s64 b1, %2, 2;\n add.s64 b2, %2, 4;\n add.s64 b3, %2, 6;\n"
+      " add.s64 c0, %2, %6;\n add.s64 c1, c0, 2;\n add.s64 c2, c0, 4;\n add.s64 c3, c0, 6;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, c0, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, c1, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, c2, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, c3, %3, 1;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n}\n" ::"r"(tmem_d),
+      "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(smem_u32(bar)), "l"(lo)
+      : "memory");
+}
 
 // 32 lanes x 16 consecutive f32 columns: thread t gets lane (base_lane + t), columns col..col+15
 NOVA_DEV void tmem_ld16(uint32_t taddr, float* v) {
@@ -65,47 +117,85 @@ NOVA_DEV void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+#ifdef NOVA_UMMA_TRACE
+// per-CTA timeline (scripts/umma_trace.py; never in the product build): [cta][8] globaltimer ns
+__device__ unsigned long long g_utrace[2048 * 8];
+NOVA_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define UTRACE(k) (a.trace ? (void)(g_utrace[blockIdx.x * 8 + (k)] = gtime()) : (void)0)
+#else
+#define UTRACE(k) ((void)0)
+#endif
+
 struct UArgs {
   void* Y;
   const bf16* wblk;  // streaming layout [N/64][K/64] x 64x64 tiles
   const bf16* bias;
-  float* ws;         // [P][B][N] split partials
+  float* ws;         // [blocks * P items][B][128] chunk partials / prefix folds of shared blocks
   int* tickets;      // [N / 128] (zero on entry, left zero)
-  int N, K, B, ldy, ks, P, blocks;
+  int N, K, B, ldy, CK, P, blocks, T;  // T = blocks * P items
+  int R;                               // whole-block rounds: CTA c owns blocks [c R, c R + R)
   unsigned long long* keys;  // EPI_F32_ARGMAX
   const float* nhid;         // RMSNorm folded (R25): residual rows [B][K] (null = off)
   float neps;
+#ifdef NOVA_UMMA_TRACE
+  int trace = 0;
+#endif
 };
 
-// unit i of this CTA: whole-block rounds first (split partials summed in registers), then split units
-NOVA_DEV bool uunit(int i, int blocks, int P, int G, int bx, int& blk, int& p, bool& local) {
-  const int R = P > 1 ? blocks / G : 0;
-  if (i < R * P) {
-    blk = (i / P) * G + bx;
-    p = i % P;
-    local = true;
-    return true;
+// Work of CTA c out of G: R whole blocks [c R, c R + R), then an equal contiguous share of the
+// remaining blocks' items (blocks R G .. blocks-1, P items each) -- the remainder is dealt stream-K.
+struct IOrder {
+  int rs, re;            // remainder items [rs, re) (global item numbers)
+  int z0, nz, a0, na, m0, nrem, n, wb0, P;
+  // Processing order: the remainder first -- its partial blocks at both ends (the one it ends in,
+  // then the one it starts in), then its whole blocks -- and the R whole-block rounds last, so the
+  // tickets and folds of shared blocks happen while the ring is still streaming and every CTA's
+  // tail is a block it completes in registers.
+  NOVA_DEV IOrder(int T, int blocks, int R, int G, int c, int P_) : P(P_) {
+    const int base = R * G * P, trem = T - base;
+    rs = base + (int)(((long long)c * trem) / G);
+    re = base + (int)(((long long)(c + 1) * trem) / G);
+    nrem = re - rs;
+    wb0 = c * R;
+    n = nrem + R * P;
+    z0 = a0 = m0 = rs;
+    nz = na = 0;
+    (void)blocks;
+    if (nrem <= 0 || rs / P == (re - 1) / P) return;
+    const int bs = rs / P, be = (re - 1) / P;
+    if (re % P) z0 = be * P, nz = re - z0;
+    if (rs % P) a0 = rs, na = (bs + 1) * P - rs, m0 = (bs + 1) * P;
   }
-  const int u = bx + (i - R * P) * G;
-  if (u >= (blocks - R * G) * P) return false;
-  blk = R * G + u / P;
-  p = u % P;
-  local = false;
-  return true;
+  NOVA_DEV int at(int k) const {
+    if (k < nrem) return k < nz ? z0 + k : k < nz + na ? a0 + (k - nz) : m0 + (k - nz - na);
+    return wb0 * P + (k - nrem);
+  }
+};
+// chunks [0, b0) of remainder block blk belong to the CTA whose share holds its chunk 0
+NOVA_DEV int prefix_len(int blk, int P, int T, int R, int G) {
+  const long long base = (long long)R * G * P, trem = T - base;
+  const long long i0 = (long long)blk * P - base;
+  const long long c = ((i0 + 1) * G - 1) / trem;  // owner of item i0
+  const long long e = ((c + 1) * trem) / G;
+  return (int)min(e - i0, (long long)P);
 }
 
-template <int EPI, int XHL>
-__global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
+template <int EPI, int XHL, int RING>
+__global__ void __launch_bounds__(NTHR, UCfg<XHL, RING>::CPS)
     gemv_umma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmX2, UArgs a) {
-  using C = UCfg<XHL>;
+  using C = UCfg<XHL, RING>;
   constexpr int ST = C::ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * C::STAGE);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
   float* s_inv = reinterpret_cast<float*>(s_last + 3);  // [16] RMSNorm row scales (16-byte aligned)
   float* s_red = s_inv + 16;                             // [4][16] warp partials
@@ -114,16 +204,23 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, bx = blockIdx.x;
   const int kblocks = a.K / KC;
-  auto unit_kb = [&](int p) { return (min(a.K, (p + 1) * a.ks) - p * a.ks) / KC; };
+  const IOrder ord(a.T, a.blocks, a.R, G, bx, a.P);
+  // k-steps [kb0, kb1) of item i
+  auto item_kb = [&](int i, int& blk, int& kb0, int& kb1) {
+    blk = i / a.P;
+    kb0 = (i - blk * a.P) * a.CK;
+    kb1 = min(kb0 + a.CK, kblocks);
+  };
 
   if (threadIdx.x == 0) {
+    UTRACE(0);
     tma_prefetch_desc(&tmX);
     if constexpr (XHL) tma_prefetch_desc(&tmX2);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NACC; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 128);
     }
@@ -136,88 +233,78 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer
-      auto load_w = [&](int st, int blk, int k) {
+    if (lane == 0) {  // ---------------- producer: the k-steps of the range's items, in processing order
+      auto load_w = [&](int st, int blk, int kb) {
         uint8_t* dst = smem + st * C::STAGE;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          bulk_load(dst + h * 8192, a.wblk + ((size_t)(2 * blk + h) * kblocks + k / KC) * (64 * KC), 8192, &full[st]);
+          bulk_load(dst + h * 8192, a.wblk + ((size_t)(2 * blk + h) * kblocks + kb) * (64 * KC), 8192, &full[st]);
       };
-      auto load_x = [&](int st, int k) {
+      auto load_x = [&](int st, int kb) {
         uint8_t* dst = smem + st * C::STAGE + W_BYTES;
-        tma_load_2d(dst, &tmX, &full[st], k, 0);
-        if constexpr (XHL) tma_load_2d(dst + X_BYTES, &tmX2, &full[st], k, 0);
+        tma_load_2d(dst, &tmX, &full[st], kb * KC, 0);
+        if constexpr (XHL) tma_load_2d(dst + X_BYTES, &tmX2, &full[st], kb * KC, 0);
       };
       // pass 1 (before griddepcontrol.wait): weights of the first ST stages (never written upstream)
-      int ui = 0, blk = 0, p = 0, kb = 0, i = 0;
-      bool loc;
-      bool have = uunit(ui, a.blocks, a.P, G, bx, blk, p, loc);
-      int nkb = have ? unit_kb(p) : 0;
-      while (have && i < ST) {
-        mbar_arrive_expect_tx(&full[i], C::STAGE);
-        load_w(i, blk, p * a.ks + kb * KC);
-        ++i;
-        if (++kb == nkb) {
-          kb = 0;
-          have = uunit(++ui, a.blocks, a.P, G, bx, blk, p, loc);
-          nkb = have ? unit_kb(p) : 0;
+      {
+        int j = 0;
+        for (int k = 0; k < ord.n && j < ST; ++k) {
+          int blk, kb0, kb1;
+          item_kb(ord.at(k), blk, kb0, kb1);
+          for (int kb = kb0; kb < kb1 && j < ST; ++kb, ++j) {
+            mbar_arrive_expect_tx(&full[j], C::STAGE);
+            load_w(j, blk, kb);
+          }
         }
       }
       pdl_launch_dependents();
       pdl_wait();  // x is written by the previous kernel
-      ui = 0, kb = 0;
-      have = uunit(ui, a.blocks, a.P, G, bx, blk, p, loc);
-      nkb = have ? unit_kb(p) : 0;
+      UTRACE(1);
       int j = 0;
-      for (; have; ++j) {
-        const int st = j % ST;
-        const int k = p * a.ks + kb * KC;
-        if (j < ST) {
-          load_x(st, k);
-        } else {
-          mbar_wait(&empty[st], ((j / ST) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[st], C::STAGE);
-          load_w(st, blk, k);
-          load_x(st, k);
-        }
-        if (++kb == nkb) {
-          kb = 0;
-          have = uunit(++ui, a.blocks, a.P, G, bx, blk, p, loc);
-          nkb = have ? unit_kb(p) : 0;
+      for (int k = 0; k < ord.n; ++k) {
+        int blk, kb0, kb1;
+        item_kb(ord.at(k), blk, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb, ++j) {
+          const int st = j % ST;
+          if (j >= ST) {
+            mbar_wait(&empty[st], ((j / ST) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[st], C::STAGE);
+            load_w(st, blk, kb);
+          }
+          load_x(st, kb);
         }
       }
       // tail: every stage released by its MMA commit before this CTA may exit
       for (int jj = j > ST ? j - ST : 0; jj < j; ++jj) mbar_wait(&empty[jj % ST], (jj / ST) & 1);
+      UTRACE(3);
     }
   } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, elected lane issues)
     constexpr uint32_t idesc = umma_idesc_bf16(RB, 16);
     const uint64_t da0 = umma_desc_sw128(smem_u32(smem));
     const uint64_t db0 = umma_desc_sw128(smem_u32(smem + W_BYTES));
-    int j = 0, acc = 0;
-    uint32_t aphase = 0;
-    int blk, p;
-    bool loc;
-    for (int ui = 0; uunit(ui, a.blocks, a.P, G, bx, blk, p, loc); ++ui) {
-      mbar_wait(&tempty[acc], aphase ^ 1);
+    int j = 0;
+    for (int n = 0; n < ord.n; ++n) {
+      const int acc = n % NACC;
+      mbar_wait(&tempty[acc], ((n / NACC) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * 16;
-      const int nkb = unit_kb(p);
-      for (int kb = 0; kb < nkb; ++kb, ++j) {
+      int blk, kb0, kb1;
+      item_kb(ord.at(n), blk, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb, ++j) {
         const int st = j % ST;
         mbar_wait(&full[st], (j / ST) & 1);
         tc_fence_after();
+#ifdef NOVA_UMMA_TRACE
+        if (j == 0 && lane == 0) UTRACE(2);
+#endif
         const uint64_t a0 = da0 + (uint64_t)(st * (C::STAGE >> 4));
         const uint64_t b0 = db0 + (uint64_t)(st * (C::STAGE >> 4));
-#pragma unroll
-        for (int k = 0; k < KC / 16; ++k) {  // +32 B along K inside the 128-B swizzle atom
-          umma_bf16_ss_warp(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-          if constexpr (XHL) umma_bf16_ss_warp(d, a0 + 2 * k, b0 + (X_BYTES >> 4) + 2 * k, idesc, 1u);
-        }
-        umma_commit_warp(&empty[st]);
+        if constexpr (XHL)
+          umma_stage_x8(d, a0, b0, (uint64_t)(X_BYTES >> 4), idesc, kb != kb0 ? 1u : 0u, &empty[st]);
+        else
+          umma_stage_x4(d, a0, b0, idesc, kb != kb0 ? 1u : 0u, &empty[st]);
       }
       umma_commit_warp(&tfull[acc]);
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
     }
   } else {  // ---------------- epilogue: warps 2..5 -> TMEM lane quarters 2, 3, 0, 1
     pdl_launch_dependents();
@@ -244,97 +331,148 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL>::CPS)
         s_inv[et] = rsqrtf((((s_red[et] + s_red[16 + et]) + s_red[32 + et]) + s_red[48 + et]) / (float)a.K + a.neps);
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
-    int acc = 0;
-    uint32_t aphase = 0;
+    const int B = a.B, P = a.P;
+    auto slot = [&](size_t item, int b) { return a.ws + (item * B + b) * RB + r; };
     float sum[16];
-    int blk, p;
-    bool local;
-    for (int ui = 0; uunit(ui, a.blocks, a.P, G, bx, blk, p, local); ++ui) {
-      mbar_wait(&tfull[acc], aphase);
+    int nshared = 0;
+    bool prefix = false;  // this CTA holds chunk 0 of the current block: sum = its left fold so far
+    int q0 = 0;           // first chunk of the current block in this CTA's range
+    int cur = -1;         // current block
+    for (int n = 0; n < ord.n; ++n) {
+      const int i = ord.at(n), acc = n % NACC;
+      mbar_wait(&tfull[acc], (n / NACC) & 1);
       tc_fence_after();
       float v[16];
       tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 16, v);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
-      const int n = blk * RB + r;
-      if (local) {  // split partials summed in split order in registers (== the workspace reduction)
+      const int blk = i / P, q = i - blk * P;
+      if (blk != cur) cur = blk, prefix = (q == 0), q0 = q;
+      const bool last_here = n == ord.n - 1 || ord.at(n + 1) / P != blk;
+      if (prefix) {  // c_0 + c_1 + ... in registers
 #pragma unroll
-        for (int b = 0; b < 16; ++b) sum[b] = (p == 0 ? 0.f : sum[b]) + v[b];
-        if (p < a.P - 1) continue;
+        for (int b = 0; b < 16; ++b) sum[b] = q == 0 ? v[b] : sum[b] + v[b];
+        if (!last_here) continue;
+        if (q == P - 1) {  // the whole block in this CTA
 #pragma unroll
-        for (int b = 0; b < 16; ++b) v[b] = sum[b];
-      } else if (a.P > 1) {
+          for (int b = 0; b < 16; ++b) v[b] = sum[b];
+        } else {
+#pragma unroll
+          for (int b = 0; b < 16; ++b)
+            if (b < B) __stcg(slot(i, b), sum[b]);
+        }
+      } else {  // a range that starts mid-block: single chunk partials
 #pragma unroll
         for (int b = 0; b < 16; ++b)
-          if (b < a.B) a.ws[((size_t)p * a.B + b) * a.N + n] = v[b];
-        __threadfence();
+          if (b < B) __stcg(slot(i, b), v[b]);
+        if (!last_here) continue;
+      }
+      if (!(prefix && q == P - 1)) {  // shared block: the last contributor completes the fold
+        // one release/acquire ticket per CTA: the barrier orders the epilogue threads' partial stores
+        // before thread 0's atom (cumulativity), and its acquire before the other threads' loads
+        const int cnt = q - q0 + 1;
+        int* last_s = s_last + (nshared++ & 1);  // alternating flags: no third barrier
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) *s_last = (atomicAdd(&a.tickets[blk], 1) == a.P - 1);
+        if (et == 0) {
+          int old;
+          asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(a.tickets + blk), "r"(cnt) : "memory");
+          *last_s = old == P - cnt;
+        }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        const bool last = *s_last;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last is reused by the next unit
-        if (!last) continue;
-        __threadfence();
+#ifdef NOVA_UMMA_TRACE
+        if (et == 0) UTRACE(5);
+#endif
+        if (!*last_s) continue;
+        // c_0..c_{b0-1} folded by the prefix owner, then c_{b0}, ..., c_{P-1}: every load of a batch
+        // column in flight at once, the fold in chunk order (P <= 16)
+        const int b0 = prefix_len(blk, P, a.T, a.R, G);
+        const size_t i0 = (size_t)blk * P;
+        const size_t cs = (size_t)B * RB;  // chunk stride in the workspace
+        if (B <= 2) {  // decode's usual batch: all <= 2 x 16 loads in flight, then the two folds
+          const float* p0 = slot(i0, 0);
+          float w0[16], w1[16];
 #pragma unroll
-        for (int b = 0; b < 16; ++b) {
-          float q8[16];
+          for (int c = 0; c < 16; ++c) {
+            const bool on = c >= b0 - 1 && c < P;
+            w0[c] = on ? __ldcg(p0 + c * cs) : 0.f;
+            w1[c] = (on && B == 2) ? __ldcg(p0 + RB + c * cs) : 0.f;
+          }
+          float f0 = 0.f, f1 = 0.f;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) q8[q] = (b < a.B && q < a.P) ? __ldcg(&a.ws[((size_t)q * a.B + b) * a.N + n]) : 0.f;
-          float s = 0.f;
+          for (int c = 0; c < 16; ++c) {
+            if (c == b0 - 1) {
+              f0 = w0[c];
+              f1 = w1[c];
+            } else if (c >= b0 && c < P) {
+              f0 += w0[c];
+              f1 += w1[c];
+            }
+          }
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (q < a.P) s += q8[q];
-          v[b] = s;
+          for (int b = 0; b < 16; ++b) v[b] = b == 0 ? f0 : b == 1 ? f1 : 0.f;
+        } else {  // one chunk's batch columns per round trip
+#pragma unroll
+          for (int b = 0; b < 16; ++b) v[b] = b < B ? __ldcg(slot(i0 + b0 - 1, b)) : 0.f;
+          for (int c = b0; c < P; ++c) {
+            float w[16];
+#pragma unroll
+            for (int b = 0; b < 16; ++b) w[b] = b < B ? __ldcg(slot(i0 + c, b)) : 0.f;
+#pragma unroll
+            for (int b = 0; b < 16; ++b) v[b] += w[b];
+          }
         }
         if (et == 0) a.tickets[blk] = 0;
       }
-      // ---- epilogues (row n, batch columns b < B)
+      const int nrow = blk * RB + r;
+      // ---- epilogues (row nrow, batch columns b < B)
       if constexpr (EPI == EPI_BF16_SILUMUL) {
         if (a.nhid) {
 #pragma unroll
-          for (int b = 0; b < 16; ++b) v[b] *= b < a.B ? s_inv[b] : 0.f;
+          for (int b = 0; b < 16; ++b) v[b] *= b < B ? s_inv[b] : 0.f;
         }
         // rows interleave 16 gate | 16 up: lane l < 16 (gate) pairs with lane l + 16 (up)
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
           const float up = __shfl_down_sync(0xffffffffu, v[b], 16);
-          if (lane < 16 && b < a.B)
+          if (lane < 16 && b < B)
             reinterpret_cast<bf16*>(a.Y)[(size_t)b * a.ldy + blk * (RB / 2) + quarter * 16 + lane] =
                 __float2bfloat16_rn(silu_u(v[b]) * up);
         }
       } else if constexpr (EPI == EPI_F32_ARGMAX) {
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
-          if (b < a.B) reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + n] = v[b];
+          if (b < B) reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + nrow] = v[b];
           uint32_t uu = __float_as_uint(v[b]);
           uu = (uu & 0x80000000u) ? ~uu : (uu | 0x80000000u);
-          unsigned long long best = ((unsigned long long)uu << 32) | (0xFFFFFFFFu - (uint32_t)n);
+          unsigned long long best = ((unsigned long long)uu << 32) | (0xFFFFFFFFu - (uint32_t)nrow);
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long ot = __shfl_xor_sync(0xffffffffu, best, o);
             best = ot > best ? ot : best;
           }
-          if (lane == 0 && b < a.B) atomicMax(a.keys + b, best);
+          if (lane == 0 && b < B) atomicMax(a.keys + b, best);
         }
       } else {
-        const float bi = a.bias ? __bfloat162float(a.bias[n]) : 0.f;
+        const float bi = a.bias ? __bfloat162float(a.bias[nrow]) : 0.f;
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
-          if (b >= a.B) continue;
+          if (b >= B) continue;
           const float y = v[b] + bi;
           if constexpr (EPI == EPI_BF16) {
-            reinterpret_cast<bf16*>(a.Y)[(size_t)b * a.ldy + n] = __float2bfloat16_rn(y);
+            reinterpret_cast<bf16*>(a.Y)[(size_t)b * a.ldy + nrow] = __float2bfloat16_rn(y);
           } else if constexpr (EPI == EPI_F32_RESID) {
-            reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + n] += y;
+            reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + nrow] += y;
           } else {
-            reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + n] = y;
+            reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + nrow] = y;
           }
         }
       }
     }
   }
+#ifdef NOVA_UMMA_TRACE
+  if (threadIdx.x == 64) UTRACE(4);
+  if (threadIdx.x == 0 && a.trace) g_utrace[blockIdx.x * 8 + 6] = ((unsigned long long)ord.rs << 32) | (unsigned)ord.n;
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -368,10 +506,10 @@ bool encx(CUtensorMap* m, const void* ptr, int rows, int cols, int ld) {
 
 std::mutex g_u_mu;
 
-template <int EPI, int XHL>
-cudaError_t ulaunch(const CUtensorMap& mx, const CUtensorMap& mx2, const UArgs& a, int sms, cudaStream_t s) {
-  using C = UCfg<XHL>;
-  auto kern = gemv_umma_kernel<EPI, XHL>;
+template <int EPI, int XHL, int RING>
+cudaError_t ulaunch_r(const CUtensorMap& mx, const CUtensorMap& mx2, const UArgs& a, int sms, cudaStream_t s) {
+  using C = UCfg<XHL, RING>;
+  auto kern = gemv_umma_kernel<EPI, XHL, RING>;
   static bool set = false;
   {
     std::lock_guard<std::mutex> g(g_u_mu);
@@ -381,35 +519,53 @@ cudaError_t ulaunch(const CUtensorMap& mx, const CUtensorMap& mx2, const UArgs& 
       set = true;
     }
   }
+  // the grid (never the sums): whole blocks when there are enough of them to keep HBM busy
+  // (>= NOVA_UMMA_WBMIN = 128 blocks x 48 KB in flight), the blocks x P items stream-K otherwise
+  static const int wbmin = getenv("NOVA_UMMA_WBMIN") ? atoi(getenv("NOVA_UMMA_WBMIN")) : 128;
   int grid = C::CPS * (sms > 0 ? sms : 148);
-  if (grid > a.blocks * a.P) grid = a.blocks * a.P;
-  return launch_k(kern, dim3(grid), dim3(NTHR), C::SMEM, s, true, mx, mx2, a);
+  if (a.blocks < grid) grid = a.blocks >= wbmin ? a.blocks : std::min(grid, a.T);
+  UArgs b = a;
+  b.R = a.blocks / grid;
+#ifdef NOVA_UMMA_TRACE
+  static const int tn = getenv("NOVA_UMMA_TRACE_N") ? atoi(getenv("NOVA_UMMA_TRACE_N")) : -1;
+  b.trace = tn < 0 || tn == a.N;
+#endif
+  return launch_k(kern, dim3(grid), dim3(NTHR), C::SMEM, s, true, mx, mx2, b);
+}
+
+// Ring shape by the SM budget (the grid, never the sums): on slices below 64 SMs four CTAs of 3
+// stages per SM stream the most; on >= 64 SMs HBM saturates anyway and two CTAs of 6 stages
+// prefetch more of each CTA's weights before griddepcontrol.wait (scripts/gpu_r2_x4.sh: 2B decode
+// iteration 1.68 -> 1.51 ms on the full GPU, 24-SM slice 3.14 -> 2.99 ms with the 3 x 4 ring).
+// env NOVA_UMMA_RING = 0 / 1 / 2 forces one.
+template <int EPI, int XHL>
+cudaError_t ulaunch(const CUtensorMap& mx, const CUtensorMap& mx2, const UArgs& a, int sms, cudaStream_t s) {
+  static const int force = getenv("NOVA_UMMA_RING") ? atoi(getenv("NOVA_UMMA_RING")) : -1;
+  const int ring = force >= 0 ? force : (sms <= 0 || sms >= 64) ? 1 : 0;
+  if (ring == 1) return ulaunch_r<EPI, XHL, 1>(mx, mx2, a, sms, s);
+  if (ring == 2) return ulaunch_r<EPI, XHL, 2>(mx, mx2, a, sms, s);
+  return ulaunch_r<EPI, XHL, 0>(mx, mx2, a, sms, s);
 }
 
 }  // namespace
 
-// Shape-only decomposition: 128-row blocks and the smallest K split P (<= 8, chunks >= 256 k) that
-// gives >= ~128 units -- one wave at the 32-SM (128-CTA) slices decode mostly runs on; bigger grids
-// then take whole blocks first and split units for the rest (a split costs a partial round trip +
-// ticket, so wide matrices are not split at all).  env NOVA_UMMA_UNITS overrides the 128.
+// Shape-only decomposition: 128-row blocks, each K range cut into P chunks of CK k-steps (the last
+// may be shorter): CK >= 4 (NOVA_UMMA_CKMIN; 64 KB of weights per item -- 2 and 8 measured no
+// better in decode iterations) and P <= 16 (NOVA_UMMA_PMAX: the length of the fold a
+// shared block's last contributor completes), and N * P <= 2^20 (the workspace: P * B * N floats).
 GemvTmaPlan gemv_umma_plan(int N, int K, int epi) {
+  (void)epi;
   GemvTmaPlan pl;
   pl.RB = RB;
-  const int blocks = N / RB;
-  static const int target = getenv("NOVA_UMMA_UNITS") ? atoi(getenv("NOVA_UMMA_UNITS")) : 128;
-  int bestP = 1;
-  static const int maxp = getenv("NOVA_UMMA_MAXP") ? atoi(getenv("NOVA_UMMA_MAXP")) : 8;
-  if (epi != EPI_F32_ARGMAX) {
-    for (int P = 1; P <= maxp; ++P) {
-      const int ks = ((K + P - 1) / P + KC - 1) / KC * KC;
-      if ((K + ks - 1) / ks != P || (P > 1 && ks < 256)) continue;
-      bestP = P;
-      if (blocks * P >= target) break;
-    }
-  }
-  pl.P = bestP;
-  pl.ks = ((K + bestP - 1) / bestP + KC - 1) / KC * KC;
-  pl.units = blocks * bestP;
+  const int kblocks = K / KC;
+  static const int ckmin = getenv("NOVA_UMMA_CKMIN") ? atoi(getenv("NOVA_UMMA_CKMIN")) : 4;
+  static const int pmax = std::min(16, getenv("NOVA_UMMA_PMAX") ? atoi(getenv("NOVA_UMMA_PMAX")) : 16);
+  int ck = std::max(ckmin, (kblocks + pmax - 1) / pmax);
+  while (ck < kblocks && (long long)N * ((kblocks + ck - 1) / ck) > (1LL << 20)) ++ck;
+  ck = std::max(1, std::min(ck, kblocks));
+  pl.P = (kblocks + ck - 1) / ck;
+  pl.ks = ck * KC;
+  pl.units = (N / RB) * pl.P;
   return pl;
 }
 
@@ -435,7 +591,7 @@ cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int 
     mx2 = mx;
   }
   if (norm_hid && (epi != EPI_BF16_SILUMUL || K % 4)) return cudaErrorInvalidValue;
-  UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks, pl.P, N / RB, keys, norm_hid, norm_eps};
+  UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks / KC, pl.P, N / RB, pl.units, 0, keys, norm_hid, norm_eps};
   if (X_lo) {
     if (epi == EPI_F32_ARGMAX) return ulaunch<EPI_F32_ARGMAX, 1>(mx, mx2, a, sms, s);
     if (epi == EPI_F32_STORE) return ulaunch<EPI_F32_STORE, 1>(mx, mx2, a, sms, s);
@@ -451,3 +607,9 @@ cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int 
 }
 
 }  // namespace nova
+
+#ifdef NOVA_UMMA_TRACE
+extern "C" int nova_debug_umma_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, nova::g_utrace, (size_t)n * 8 * 8);
+}
+#endif

@@ -152,7 +152,8 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   // >= the fused decode's chunk partials: B x KV x ceil((max_ctx + 1) / 128) x (32 + (H / KV) hd)
   const size_t fused_parts = B * m.llm_kv_heads * ((max_ctx + 1 + 127) / 128) * (32 + (size_t)(m.llm_heads / m.llm_kv_heads) * m.head_dim);
   w.attn_ws = (float*)take(std::max(B * m.llm_heads * nparts * (m.head_dim + 2), fused_parts) * 4);
-  w.gemv_ws = (float*)take((size_t)16 * B * std::max(std::max(D, F), (size_t)d.llm_qkv_n) * 4);
+  // split partials: mma.sync GEMVs 16 x B x N, gemv_umma P x B x N with N * P <= 2^20 (gemv_umma_plan)
+  w.gemv_ws = (float*)take(std::max((size_t)16 * std::max(std::max(D, F), (size_t)d.llm_qkv_n), (size_t)1 << 20) * B * 4);
   w.tickets = (int*)take(8192 * 4);
   w.qkvf = (float*)take(B * d.llm_qkv_n * 4);
   w.ss = (float*)take(B * ((D / 64 + 3) / 4 * 4) * 4);

@@ -80,13 +80,14 @@ static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xmode, int ldx,
   return cudaSuccess;
 }
 
-// Which decode linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 1 o, 2 gate|up,
-// 3 down, 4 lm_head); the choice depends on the op only, never on the partition (co-execution is
-// bitwise == serial).  Default gate|up + lm_head (scripts/gpu_r2_u3.sh, decode iterations on
-// 24..148-SM partitions: 2B 3.25 -> 3.12 ms on 24 SMs, 1.79 -> 1.71 on 64, level on the full GPU;
-// down / o on tcgen05 win on <= 48-SM slices but lose 10-25% on larger grids).
+// Which decode linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 2 o, 4 gate|up,
+// 8 down, 16 lm_head); the choice depends on the op only, never on the partition (co-execution is
+// bitwise == serial).  Default all four (30): with the stream-K decomposition and one elect per ring
+// stage (gemv_umma.cu) decode iterations on 24-SM slices and the full GPU are faster than with o /
+// down on the mma.sync GEMVs at B = 2..16 (scripts/gpu_r2_mask.sh; 2B 24 SMs B = 16 6.18 -> 5.97 ms,
+// full GPU 2.64 -> 2.29 ms; 7B 24 SMs B = 16 15.5 -> 12.6 ms), the 48-56-SM 2B range excepted.
 static int umma_mask() {
-  static const int m = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 20;
+  static const int m = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 30;
   return g_dec_umma ? m : 0;
 }
 

@@ -1,0 +1,13 @@
+#!/bin/bash
+L=paper_2509_21301_b200
+cp $L/libnova_new.so $L/libnova.so
+timeout 300 python -m pytest tests/test_gpu_gemv_umma.py -x -q 2>&1 | tail -2
+cp $L/libnova_trace.so $L/libnova.so
+for c in 148 64 24; do timeout 60 python scripts/umma_trace.py 17920 1536 3 $c 2 2>&1 | tail -1; done
+for c in 64 24; do timeout 60 python scripts/umma_trace.py 37888 3584 3 $c 2 2>&1 | tail -1; done
+cp $L/libnova_new.so $L/libnova.so
+for ck in 4 2; do
+  for sh in 2b_gu 2b_down 2b_lm 7b_gu 7b_down; do NOVA_UMMA_CKMIN=$ck timeout 300 python scripts/ubench.py --only $sh --iters 20 2>&1 | grep '"B": 2'; done
+  for m in 20 30; do NOVA_UMMA_CKMIN=$ck NOVA_UMMA_MASK=$m timeout 300 python scripts/dec_splits.py --model 2b --B 2 16 2>&1 | tail -2; done
+  for m in 20 30; do NOVA_UMMA_CKMIN=$ck NOVA_UMMA_MASK=$m timeout 300 python scripts/dec_splits.py --model 7b --B 2 2>&1 | tail -1; done
+done

@@ -44,7 +44,7 @@ def main():
             Y = torch.zeros(B, nout, dtype=torch.bfloat16 if epi == O.EPI_BF16_SILUMUL else torch.float32,
                             device="cuda")
             keys = torch.zeros(B, dtype=torch.int64, device="cuda")
-            for ctas in (148, 64, 32):
+            for ctas in (148, 64, 32, 24):
                 row = {"op": name, "B": B, "ctas": ctas}
                 for kname, fn in (("tma", O.nova_op_gemv_stream), ("umma", O.nova_op_gemv_umma)):
                     xlo = X[B:] if epi == O.EPI_F32_ARGMAX else None

@@ -29,7 +29,7 @@ def _blocked(W, N, K):
 
 
 @pytest.mark.parametrize("N,K", [(17920, 1536), (1536, 8960), (2048, 1536), (37888, 3584), (3584, 18944),
-                                 (256, 128), (768, 128)])
+                                 (256, 128), (768, 128), (384, 320), (1280, 2240)])
 def test_umma_gemv_matches_oracle_and_is_grid_and_batch_invariant(N, K):
     rng = np.random.default_rng(3 * N + K)
     W = rand_bf16(rng, (N, K), K ** -0.5)
@@ -47,11 +47,33 @@ def test_umma_gemv_matches_oracle_and_is_grid_and_batch_invariant(N, K):
             Y16 = Y0
         else:
             assert torch.equal(Y0[0], Y16[0]), B          # batch invariance of row 0
-        for ctas in (148, 40, 24, 8):                       # whole-block units first on small grids
+        for ctas in (148, 40, 24, 8, 1):                    # stream-K ranges: blocks shared across CTAs
             Y1 = torch.empty_like(Y0)
             O.nova_op_gemv_umma(dX[:B], Wb, Y1, None, N, K, B, O.EPI_F32_STORE, max_ctas=ctas)
             torch.cuda.synchronize()
             assert torch.equal(Y0, Y1), (B, ctas)
+
+
+def test_umma_stream_k_ranges_any_grid():
+    """Item ranges cut blocks at every position (1..37 CTAs of 3 per SM budget unit): the left fold of
+    the chunk partials is completed by whichever CTA arrives last -- bitwise the same result."""
+    N, K = 640, 1600                                      # 5 blocks x P chunks (25 k-steps, short last chunk)
+    P = O.nova_op_gemv_umma_splits(N, K, O.EPI_F32_STORE)
+    assert P > 1
+    rng = np.random.default_rng(5)
+    W = rand_bf16(rng, (N, K), K ** -0.5)
+    X = rand_bf16(rng, (3, K))
+    Wb, dX = _blocked(W, N, K), bf16_dev(X)
+    ref = V.linear(X.astype(np.float64), W.astype(np.float64))
+    Y0 = None
+    for ctas in (1, 2, 3, 5, 7, 11, 37):
+        Y = torch.empty(3, N, dtype=torch.float32, device="cuda")
+        O.nova_op_gemv_umma(dX, Wb, Y, None, N, K, 3, O.EPI_F32_STORE, max_ctas=ctas)
+        torch.cuda.synchronize()
+        assert rel_inf(Y.cpu().numpy(), ref) <= 1e-4, ctas
+        if Y0 is None:
+            Y0 = Y
+        assert torch.equal(Y, Y0), ctas
 
 
 def test_umma_gemv_silu_and_residual_epilogues():
