@@ -100,7 +100,9 @@ typedef struct {
  * ceil((max_ctx+1)/128) <= 64, H/KV <= 16.  Deterministic, batch- and grid-invariant. */
 int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int32_t* block_tables, int max_pages, const nova_decode_row* rows,
-                        int B, int max_ctx, float* ws, int32_t* tickets, void* stream);
+                        int B, int max_ctx, float* ws, int32_t* tickets, int max_ctas, void* stream);
+/* max_ctas: SM budget of the partition (0 = whole GPU); it picks the K/V ring depth (2 stages, one CTA per
+ * SM, or 1 stage, two CTAs per SM), never the result. */
 
 /* Persistent paged decode attention (decode_attn_p.cu): same contract as nova_op_decode_attn
  * (rows[b] = {slot, ctx, pos, pad}: query b attends keys 0..ctx of its slot's pages; GQA), work
@@ -166,11 +168,28 @@ int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_
  * cuts K into P > 1 chunks (nova_op_gemv_umma_splits).  max_ctas = SM budget of the partition (0 = whole GPU). */
 int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
                       const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
-                      const float* norm_hid, float norm_eps, void* stream);
+                      const float* norm_hid, float norm_eps, const void* ngamma, void* nxout, int ldnx,
+                      void* stream);
 /* norm_hid != NULL (epi NOVA_EPI_BF16_SILUMUL only): RMSNorm folded after the GEMV (DESIGN R25) -- X
  * holds x~ = bf16(h * gamma) and every output row b is scaled by rsqrt(mean_k h[b][k]^2 + norm_eps),
- * h = norm_hid [B][K] f32, before SiLU(gate) * up. */
+ * h = norm_hid [B][K] f32, before SiLU(gate) * up.
+ * nxout != NULL (epi NOVA_EPI_F32_RESID only, ngamma [N] bf16 required): the other half of that fold --
+ * after Y[b][n] += result, also nxout[b * ldnx + n] = bf16(Y[b][n] * ngamma[n]) (the next RMSNorm's
+ * x~, read by the following NOVA_EPI_BF16_SILUMUL call).  NULL = off. */
 int nova_op_gemv_umma_splits(int N, int K, int epi);
+/* Decode qkv projection on the same tcgen05 GEMV (DESIGN R25 fold + the EPI_QKV_ROPE_KV epilogue of
+ * nova_op_gemv_fused, SURVEY §8(a) a7 "QKV GEMV (+bias) + M-RoPE + KV append"): X = x~ = bf16(h * ln1)
+ * [B][K] (ldx), h = norm_hid [B][K] f32; q/k/v = rsqrt(mean_k h^2 + norm_eps) * (x~ W^T) + bias, RoPE at
+ * rows[b].pos on q and k; q heads -> Q [B][ldq] bf16 (first H * hd columns), k / v -> kv_pool at layer,
+ * page bt[rows[b].slot][rows[b].ctx / 64], cell rows[b].ctx % 64.  hd must be 128 (one 128-row block
+ * per head), N = (H + 2 KV) * hd, B <= 16; ws / tickets as nova_op_gemv_umma.  Bitwise independent of
+ * max_ctas and of the batch composition. */
+int nova_op_gemv_umma_qkv(const void* X, int ldx, const void* W_blocked, int N, int K, void* Q, int ldq,
+                          const void* bias, int B, const float* norm_hid, float norm_eps, int H, int KV, int hd,
+                          float theta, const nova_decode_row* rows, void* kv_pool, int layer, int n_pages,
+                          const int32_t* bt, int max_pages, float* ws, int32_t* tickets, int max_ctas, void* stream);
+/* y[r][c] = bf16(x[r][c] * gamma[c]) for M rows of d (the R25 fold's GEMV input). */
+int nova_op_scale_rows_bf16(const float* x, int ldx, const void* gamma, void* y, int ldy, int M, int d, void* stream);
 
 /* keys[r] (from NOVA_EPI_F32_ARGMAX) -> out_tok[r]; also last_tok[rows[r].slot] (rows != NULL)
  * or last_tok[single_slot] (>= 0); resets keys[r] to 0.  n <= 1024. */

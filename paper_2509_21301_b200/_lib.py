@@ -26,13 +26,15 @@ OPS_SIGNATURES = {
     "nova_op_gemv_tma": [P, I, P, I, I, P, I, P, I, I, P, P, I, P],
     "nova_op_flash_attn": [P, I, P, I, I, I, I, I, I, I, P],
     "nova_op_flash_attn_mma": [P, I, P, I, I, I, I, I, I, P],
-    "nova_op_decode_attn": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P, P],
+    "nova_op_decode_attn": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P, I, P],
     "nova_op_gemv_fused": [P, I, I, P, I, I, P, I, P, I, I, P, F, I, I, I, F, P, P, I, I, P, I, P, P],
     "nova_op_argmax_finalize": [P, I, P, P, P, I, P],
     "nova_op_block_weights": [P, P, I, I, P],
     "nova_op_gemv_stream": [P, P, I, P, I, I, P, I, P, I, I, P, P, P, I, P],
-    "nova_op_gemv_umma": [P, P, I, P, I, I, P, I, P, I, I, P, P, P, I, P, F, P],
+    "nova_op_gemv_umma": [P, P, I, P, I, I, P, I, P, I, I, P, P, P, I, P, F, P, P, I, P],
     "nova_op_gemv_umma_splits": [I, I, I],
+    "nova_op_gemv_umma_qkv": [P, I, P, I, I, P, I, P, I, P, F, I, I, I, F, P, P, I, I, P, I, P, P, I, P],
+    "nova_op_scale_rows_bf16": [P, I, P, P, I, I, I, P],
     "nova_op_chunk_attn": [P, I, P, I, I, I, I, I, I, P, I, I, P, P],
     "nova_op_decode_attn_p": [P, I, P, I, P, I, I, I, I, I, P, I, P, I, I, P, P, I, I, P],
     "nova_op_layernorm": [P, I, P, P, P, I, I, I, F, P],

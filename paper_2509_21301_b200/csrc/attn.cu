@@ -9,6 +9,8 @@
 //   256-token chunk); the GQA group shares every K/V load; chunk partials are
 //   merged by a second kernel in fixed chunk order (deterministic; the chunking
 //   depends only on the context length).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -540,15 +542,19 @@ constexpr int TKW = 32;   // keys per block
 // of a decode slice idle at the paper's small batches), else 4.  Depends on the model shape only, so
 // a request's result does not depend on the batch or the partition.
 inline int da_cluster(int KV) { return KV <= 2 ? 8 : 4; }
-constexpr int DA_W = 6;   // warps per CTA (smem: 6 x 2 stages x 17 KB): DA_W x CL block streams per (request, KV head)
-template <int HD>
+constexpr int DA_W = 6;   // warps per CTA (smem: 6 x NST stages x 17 KB): DA_W x CL block streams per (request, KV head)
+// NST = K/V ring stages per warp: 2 (one CTA per SM at hd 128) or 1 (two CTAs per SM; blocks are
+// gathered one at a time, from L2 after the pre-wait prefetch).  The sums do not depend on NST, so the
+// launcher picks it from the partition size.
+template <int HD, int NST = 2>
 struct DtcCfg {
   static constexpr int HDP = HD + 8;                       // padded row (conflict-free ldmatrix)
   static constexpr int BLK = 2 * TKW * HDP * 2;            // one K+V block (bytes)
   static constexpr int Q_BYTES = 16 * HDP * 2;
-  static constexpr int RING = DA_W * 2 * BLK;              // DA_W warps x 2 stages
-  static constexpr int ST_OFF = Q_BYTES + RING;            // CTA state [16][HD + 2] f32
-  static constexpr int SMEM = ST_OFF + 16 * (HD + 2) * 4;
+  static constexpr int RING = DA_W * NST * BLK;            // DA_W warps x NST stages
+  // after the ring drains: warp states [DA_W][16][HD + 2] f32, then the CTA state [16][HD + 2] f32
+  static constexpr int ST_OFF = Q_BYTES + DA_W * 16 * (HD + 2) * 4;
+  static constexpr int SMEM = Q_BYTES + (RING > ST_OFF - Q_BYTES + 16 * (HD + 2) * 4 ? RING : ST_OFF - Q_BYTES + 16 * (HD + 2) * 4);
 };
 
 NOVA_DEV void cluster_sync_all() {
@@ -567,13 +573,13 @@ NOVA_DEV float ld_dsmem_f32(uint32_t local_saddr, uint32_t rank) {
   return v;
 }
 
-template <int HD, int CL>
+template <int HD, int CL, int NST>
 __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* __restrict__ qkv, int ld,
                                                              const bf16* __restrict__ pool, int layer, int n_pages,
                                                              int H, int KV, const int* __restrict__ bt, int max_pages,
                                                              const DecodeRow* __restrict__ rows, bf16* __restrict__ out,
                                                              int ldo, float scale_log2) {
-  using Cf = DtcCfg<HD>;
+  using Cf = DtcCfg<HD, NST>;
   constexpr int HDP = Cf::HDP, CH = HD / 8, KT = HD / 16, DT = HD / 8, PW = HD + 2;
   extern __shared__ __align__(16) uint8_t dsm[];
   bf16* sQ = reinterpret_cast<bf16*>(dsm);
@@ -620,7 +626,7 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
   const int* btr = bt + (size_t)rr.slot * max_pages;
   const int nblk = (L + TKW - 1) / TKW;
   const int wg = rank * DA_W + warp, wstride = DA_W * CL;
-  bf16* ring = reinterpret_cast<bf16*>(dsm + Cf::Q_BYTES) + (size_t)warp * 2 * (Cf::BLK / 2);
+  bf16* ring = reinterpret_cast<bf16*>(dsm + Cf::Q_BYTES) + (size_t)warp * NST * (Cf::BLK / 2);
   auto issue = [&](int blk, int stage) {  // gather K and V rows of block blk into stage
     bf16* wK = ring + (size_t)stage * (Cf::BLK / 2);
     bf16* wV = wK + TKW * HDP;
@@ -649,11 +655,15 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
   int it = 0;
   for (int blk = wg; blk < nblk; blk += wstride, ++it) {
     const int nxt = blk + wstride;
-    if (nxt < nblk) issue(nxt, (it + 1) & 1);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (NST == 2) {
+      if (nxt < nblk) issue(nxt, (it + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncwarp();
-    const bf16* wK = ring + (size_t)(it & 1) * (Cf::BLK / 2);
+    const bf16* wK = ring + (size_t)(NST == 2 ? (it & 1) : 0) * (Cf::BLK / 2);
     const bf16* wV = wK + TKW * HDP;
     const int k0 = blk * TKW;
     float sc[4][4];
@@ -719,7 +729,11 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
         mma_bf16_16816(o[dt], pa[kk], bb);
       }
     }
-    __syncwarp();  // this stage is refilled two blocks later
+    __syncwarp();  // this stage is refilled NST blocks later
+    if constexpr (NST == 1) {
+      if (nxt < nblk) issue(nxt, 0);
+      cp_async_commit();
+    }
   }
   cp_async_wait<0>();
   __syncthreads();  // every warp is done with the ring: reuse it for the warp states
@@ -809,24 +823,32 @@ __global__ void decode_attn_combine(const float* __restrict__ ws, const DecodeRo
 template <int HD>
 cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
                       int KV, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx, float* ws,
-                      int* tickets, cudaStream_t s) {
+                      int* tickets, int sms, cudaStream_t s) {
   if (H / KV > 16) return cudaErrorInvalidValue;
   const float sl2 = LOG2E / sqrtf((float)HD);
   cudaError_t e;
   if (g_decode_attn_tc) {  // tensor-core version: one cluster of da_cluster(KV) CTAs per (request, KV head)
     if (H / KV > 16) return cudaErrorInvalidValue;
     const int CLN = da_cluster(KV);
-    auto kern = CLN == 8 ? decode_attn_tc_kernel<HD, 8> : decode_attn_tc_kernel<HD, 4>;
+    // ring depth by the partition (never the sums): one stage and two CTAs per SM when the clusters
+    // would take more than one wave of the partition at one CTA per SM (env NOVA_DA_NST forces 1 / 2)
+    static const int force = getenv("NOVA_DA_NST") ? atoi(getenv("NOVA_DA_NST")) : 0;
+    const int nsm = sms > 0 ? sms : 148;
+    const int nst = force ? force : (CLN * KV * B > nsm ? 1 : 2);
+    auto kern = CLN == 8 ? (nst == 1 ? decode_attn_tc_kernel<HD, 8, 1> : decode_attn_tc_kernel<HD, 8, 2>)
+                         : (nst == 1 ? decode_attn_tc_kernel<HD, 4, 1> : decode_attn_tc_kernel<HD, 4, 2>);
     static bool set = false;
     if (!set) {
-      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD>::SMEM);
-      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 2>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 2>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 1>::SMEM);
+      cudaFuncSetAttribute(decode_attn_tc_kernel<HD, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 1>::SMEM);
       set = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CLN, KV, B);
     cfg.blockDim = dim3(32 * DA_W);
-    cfg.dynamicSmemBytes = DtcCfg<HD>::SMEM;
+    cfg.dynamicSmemBytes = nst == 1 ? DtcCfg<HD, 1>::SMEM : DtcCfg<HD, 2>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -879,13 +901,13 @@ cudaError_t flash_attn_mma(const bf16* qkv, int ld, bf16* out, int ldo, int S, i
 
 cudaError_t decode_attn(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* pool, int layer, int n_pages, int H,
                         int KV, int hd, const int* bt, int max_pages, const DecodeRow* rows, int B, int max_ctx,
-                        float* ws, int* tickets, cudaStream_t s) {
+                        float* ws, int* tickets, cudaStream_t s, int sms) {
   if (B <= 0) return cudaSuccess;
   switch (hd) {
-    case 32: return da_launch<32>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
-    case 64: return da_launch<64>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
+    case 32: return da_launch<32>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, sms, s);
+    case 64: return da_launch<64>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, sms, s);
     case 128:
-      return da_launch<128>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, s);
+      return da_launch<128>(qkv, ld, out, ldo, pool, layer, n_pages, H, KV, bt, max_pages, rows, B, max_ctx, ws, tickets, sms, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -51,13 +51,16 @@ constexpr int NACC = 4;              // TMEM accumulators (16 columns each): MMA
 constexpr int TMEM_COLS = NACC * 16;
 
 // ring shapes (same shared memory per SM): RING 0 = 3 stages x 4 CTAs per SM, 1 = 6 x 2, 2 = 12 x 1
-// (hi/lo x: 3 x 3, 5 x 2, 10 x 1)
-template <int XHL, int RING>
+// (hi/lo x: 3 x 3, 5 x 2, 10 x 1; with the 8 KB RoPE pair-exchange buffer of the qkv epilogue
+// (XB): 3 x 3, 5 x 2, 11 x 1)
+constexpr int XB_BYTES = RB * 16 * 4;  // [16 batch columns][128 rows] f32
+template <int XHL, int RING, int XB = 0>
 struct UCfg {
-  static constexpr int ST = RING == 0 ? 3 : RING == 1 ? (XHL ? 5 : 6) : (XHL ? 10 : 12);
-  static constexpr int CPS = RING == 0 ? (XHL ? 3 : 4) : RING == 1 ? 2 : 1;  // CTAs per SM of the partition
+  static constexpr int ST = RING == 0 ? 3 : RING == 1 ? ((XHL || XB) ? 5 : 6) : (XHL ? 10 : XB ? 11 : 12);
+  static constexpr int CPS = RING == 0 ? ((XHL || XB) ? 3 : 4) : RING == 1 ? 2 : 1;  // CTAs per SM of the partition
   static constexpr int STAGE = W_BYTES + (1 + XHL) * X_BYTES;
-  static constexpr int SMEM = 1024 + ST * STAGE + 512;
+  static constexpr int XB_OFF = ST * STAGE + 512;
+  static constexpr int SMEM = 1024 + ST * STAGE + 512 + (XB ? XB_BYTES : 0);
 };
 
 NOVA_DEV float silu_u(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
@@ -141,6 +144,16 @@ struct UArgs {
   unsigned long long* keys;  // EPI_F32_ARGMAX
   const float* nhid;         // RMSNorm folded (R25): residual rows [B][K] (null = off)
   float neps;
+  const bf16* ngamma;        // EPI_F32_RESID next-norm prep (R25): nxout[b][n] = bf16(Y_new[b][n] * ngamma[n])
+  bf16* nxout;
+  int ldnx;
+  // EPI_QKV_ROPE_KV (hd = 128 = one block per head): bias + RoPE at rows[b].pos on q / k, q -> Y (bf16),
+  // k / v -> the paged cache at rows[b].ctx
+  const DecodeRow* rows;
+  bf16* pool;
+  const int* bt;
+  int H, KV, layer, n_pages, max_pages;
+  float log2_theta;
 #ifdef NOVA_UMMA_TRACE
   int trace = 0;
 #endif
@@ -185,9 +198,9 @@ NOVA_DEV int prefix_len(int blk, int P, int T, int R, int G) {
 }
 
 template <int EPI, int XHL, int RING>
-__global__ void __launch_bounds__(NTHR, UCfg<XHL, RING>::CPS)
+__global__ void __launch_bounds__(NTHR, UCfg<XHL, RING, EPI == EPI_QKV_ROPE_KV>::CPS)
     gemv_umma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmX2, UArgs a) {
-  using C = UCfg<XHL, RING>;
+  using C = UCfg<XHL, RING, EPI == EPI_QKV_ROPE_KV>;
   constexpr int ST = C::ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -314,17 +327,36 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL, RING>::CPS)
     if (a.nhid) {
       // RMSNorm row scales (R25), while the first MMAs run: thread et sums float4 chunks et, et + 128,
       // ... in order, xor butterfly per warp, warps combined ((w0 + w1) + w2) + w3 -- one fixed order
+      // (the loads of RJ rows x 4 chunks issued together: one L2 round trip per RJ rows, not per row)
+      constexpr int RJ = C::CPS >= 3 ? 2 : 4;
       const int nch = a.K / 4, ew = et >> 5;
-      for (int b = 0; b < a.B; ++b) {
-        const float4* hr = reinterpret_cast<const float4*>(a.nhid + (size_t)b * a.K);
-        float sq = 0.f;
-        for (int q = et; q < nch; q += 128) {
-          const float4 h4 = __ldcg(hr + q);
-          sq += (h4.x * h4.x + h4.y * h4.y) + (h4.z * h4.z + h4.w * h4.w);
+      for (int b0 = 0; b0 < a.B; b0 += RJ) {
+        float sq[RJ];
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) sq[j] = 0.f;
+        for (int q = et; q < nch; q += 4 * 128) {
+          float4 h4[RJ][4];
+#pragma unroll
+          for (int j = 0; j < RJ; ++j)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              h4[j][u] = (b0 + j < a.B && q + u * 128 < nch)
+                             ? __ldcg(reinterpret_cast<const float4*>(a.nhid + (size_t)(b0 + j) * a.K) + q + u * 128)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < RJ; ++j)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (q + u * 128 < nch)
+                sq[j] += (h4[j][u].x * h4[j][u].x + h4[j][u].y * h4[j][u].y) +
+                         (h4[j][u].z * h4[j][u].z + h4[j][u].w * h4[j][u].w);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) s_red[ew * 16 + b] = sq;
+        for (int j = 0; j < RJ; ++j) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sq[j] += __shfl_xor_sync(0xffffffffu, sq[j], o);
+          if (lane == 0 && b0 + j < a.B) s_red[ew * 16 + b0 + j] = sq[j];
+        }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (et < a.B)
@@ -410,26 +442,76 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL, RING>::CPS)
           }
 #pragma unroll
           for (int b = 0; b < 16; ++b) v[b] = b == 0 ? f0 : b == 1 ? f1 : 0.f;
-        } else {  // one chunk's batch columns per round trip
+        } else {  // the batch columns of FD chunks per round trip (the prefix with the first), folded in order;
+                  // FD = 2 where the register budget allows it (<= 2 CTAs per SM), else 1
+          constexpr int FD = C::CPS >= 3 ? 1 : 2;
+          for (int c = b0 - 1; c < P; c += FD) {
+            float w[FD][16];
 #pragma unroll
-          for (int b = 0; b < 16; ++b) v[b] = b < B ? __ldcg(slot(i0 + b0 - 1, b)) : 0.f;
-          for (int c = b0; c < P; ++c) {
-            float w[16];
+            for (int j = 0; j < FD; ++j)
 #pragma unroll
-            for (int b = 0; b < 16; ++b) w[b] = b < B ? __ldcg(slot(i0 + c, b)) : 0.f;
+              for (int b = 0; b < 16; ++b) w[j][b] = (b < B && c + j < P) ? __ldcg(slot(i0 + c + j, b)) : 0.f;
 #pragma unroll
-            for (int b = 0; b < 16; ++b) v[b] += w[b];
+            for (int j = 0; j < FD; ++j) {
+              if (c + j >= P) break;
+#pragma unroll
+              for (int b = 0; b < 16; ++b) v[b] = (c + j == b0 - 1) ? w[j][b] : v[b] + w[j][b];
+            }
           }
         }
         if (et == 0) a.tickets[blk] = 0;
       }
       const int nrow = blk * RB + r;
       // ---- epilogues (row nrow, batch columns b < B)
-      if constexpr (EPI == EPI_BF16_SILUMUL) {
+      if constexpr (EPI == EPI_BF16_SILUMUL || EPI == EPI_QKV_ROPE_KV) {
         if (a.nhid) {
 #pragma unroll
           for (int b = 0; b < 16; ++b) v[b] *= b < B ? s_inv[b] : 0.f;
         }
+      }
+      if constexpr (EPI == EPI_QKV_ROPE_KV) {
+        // one block = one head (hd 128): row r pairs with r ^ 64 (rotate_half); rows 64..127 hand
+        // their sums to rows 0..63 through shared memory, the owners rotate and store both
+        float* xb = reinterpret_cast<float*>(smem + C::XB_OFF);
+        const float bi = a.bias ? __bfloat162float(a.bias[nrow]) : 0.f;
+        if (r >= 64) {
+#pragma unroll
+          for (int b = 0; b < 16; ++b) xb[b * RB + r] = v[b] + bi;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (r < 64) {
+          const int hh = blk, hd = RB, half = 64;
+          const float inv = exp2f(-(2.0f * r / hd) * a.log2_theta);
+#pragma unroll
+          for (int b = 0; b < 16; ++b) {
+            if (b >= B) continue;
+            float v1 = v[b] + bi, v2 = xb[b * RB + r + half];
+            const DecodeRow rr = a.rows[b];
+            if (hh < a.H + a.KV) {  // t = h = w = pos for generated text: plain RoPE at pos
+              float sn, cs;
+              sincosf((float)rr.pos * inv, &sn, &cs);
+              const float o1 = v1 * cs - v2 * sn, o2 = v2 * cs + v1 * sn;
+              v1 = o1;
+              v2 = o2;
+            }
+            if (hh < a.H) {
+              bf16* q = reinterpret_cast<bf16*>(a.Y) + (size_t)b * a.ldy + (size_t)hh * hd;
+              q[r] = __float2bfloat16_rn(v1);
+              q[r + half] = __float2bfloat16_rn(v2);
+            } else {
+              const int isv = hh >= a.H + a.KV;
+              const int kvh = hh - a.H - (isv ? a.KV : 0);
+              const size_t page_stride = (size_t)2 * a.KV * 64 * hd;
+              bf16* pg = a.pool + ((size_t)a.layer * a.n_pages + a.bt[(size_t)rr.slot * a.max_pages + (rr.ctx >> 6)]) *
+                                      page_stride;
+              bf16* dst = pg + (((size_t)isv * a.KV + kvh) * 64 + (rr.ctx & 63)) * hd;
+              dst[r] = __float2bfloat16_rn(v1);
+              dst[r + half] = __float2bfloat16_rn(v2);
+            }
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // xb is reused by the next block
+      } else if constexpr (EPI == EPI_BF16_SILUMUL) {
         // rows interleave 16 gate | 16 up: lane l < 16 (gate) pairs with lane l + 16 (up)
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
@@ -461,7 +543,10 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL, RING>::CPS)
           if constexpr (EPI == EPI_BF16) {
             reinterpret_cast<bf16*>(a.Y)[(size_t)b * a.ldy + nrow] = __float2bfloat16_rn(y);
           } else if constexpr (EPI == EPI_F32_RESID) {
-            reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + nrow] += y;
+            float* yp = reinterpret_cast<float*>(a.Y) + (size_t)b * a.ldy + nrow;
+            const float hn = *yp + y;
+            *yp = hn;
+            if (a.nxout) a.nxout[(size_t)b * a.ldnx + nrow] = __float2bfloat16_rn(hn * __bfloat162float(a.ngamma[nrow]));
           } else {
             reinterpret_cast<float*>(a.Y)[(size_t)b * a.ldy + nrow] = y;
           }
@@ -508,7 +593,7 @@ std::mutex g_u_mu;
 
 template <int EPI, int XHL, int RING>
 cudaError_t ulaunch_r(const CUtensorMap& mx, const CUtensorMap& mx2, const UArgs& a, int sms, cudaStream_t s) {
-  using C = UCfg<XHL, RING>;
+  using C = UCfg<XHL, RING, EPI == EPI_QKV_ROPE_KV>;
   auto kern = gemv_umma_kernel<EPI, XHL, RING>;
   static bool set = false;
   {
@@ -572,12 +657,13 @@ GemvTmaPlan gemv_umma_plan(int N, int K, int epi) {
 bool gemv_umma_supported(int N, int K, int epi) {
   return N % RB == 0 && K % KC == 0 &&
          (epi == EPI_BF16 || epi == EPI_BF16_SILUMUL || epi == EPI_F32_RESID || epi == EPI_F32_STORE ||
-          epi == EPI_F32_ARGMAX);
+          epi == EPI_F32_ARGMAX || epi == EPI_QKV_ROPE_KV);
 }
 
 cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int K, void* Y, int ldy, const bf16* bias,
                       int B, int epi, float* ws, int* tickets, cudaStream_t s, int sms, unsigned long long* keys,
-                      const bf16* X_lo, const float* norm_hid, float norm_eps) {
+                      const bf16* X_lo, const float* norm_hid, float norm_eps, const bf16* ngamma,
+                      bf16* nxout, int ldnx, const GemvAux* qa) {
   if (B <= 0) return cudaSuccess;
   if (B > 16 || !gemv_umma_supported(N, K, epi) || ldx % 8 || !W_blocked) return cudaErrorInvalidValue;
   if (epi == EPI_F32_ARGMAX && (!keys || !X_lo)) return cudaErrorInvalidValue;
@@ -590,8 +676,17 @@ cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int 
   } else {
     mx2 = mx;
   }
-  if (norm_hid && (epi != EPI_BF16_SILUMUL || K % 4)) return cudaErrorInvalidValue;
-  UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks / KC, pl.P, N / RB, pl.units, 0, keys, norm_hid, norm_eps};
+  if (norm_hid && ((epi != EPI_BF16_SILUMUL && epi != EPI_QKV_ROPE_KV) || K % 4)) return cudaErrorInvalidValue;
+  if (nxout && (epi != EPI_F32_RESID || !ngamma)) return cudaErrorInvalidValue;
+  if (epi == EPI_QKV_ROPE_KV &&
+      (!qa || qa->hd != RB || N != (qa->H + 2 * qa->KV) * RB || !qa->rows || !qa->pool || !qa->bt || X_lo))
+    return cudaErrorInvalidValue;
+  UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks / KC, pl.P, N / RB, pl.units, 0, keys, norm_hid, norm_eps,
+          ngamma, nxout, ldnx};
+  if (qa) {
+    a.rows = qa->rows, a.pool = qa->pool, a.bt = qa->bt, a.H = qa->H, a.KV = qa->KV, a.layer = qa->layer;
+    a.n_pages = qa->n_pages, a.max_pages = qa->max_pages, a.log2_theta = qa->log2_theta;
+  }
   if (X_lo) {
     if (epi == EPI_F32_ARGMAX) return ulaunch<EPI_F32_ARGMAX, 1>(mx, mx2, a, sms, s);
     if (epi == EPI_F32_STORE) return ulaunch<EPI_F32_STORE, 1>(mx, mx2, a, sms, s);
@@ -602,6 +697,7 @@ cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int 
     case EPI_BF16_SILUMUL: return ulaunch<EPI_BF16_SILUMUL, 0>(mx, mx2, a, sms, s);
     case EPI_F32_RESID: return ulaunch<EPI_F32_RESID, 0>(mx, mx2, a, sms, s);
     case EPI_F32_STORE: return ulaunch<EPI_F32_STORE, 0>(mx, mx2, a, sms, s);
+    case EPI_QKV_ROPE_KV: return ulaunch<EPI_QKV_ROPE_KV, 0>(mx, mx2, a, sms, s);
   }
   return cudaErrorInvalidValue;
 }

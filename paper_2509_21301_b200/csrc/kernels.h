@@ -92,11 +92,14 @@ extern bool g_use_tma_gemv;
 extern int g_dec_umma;  // env NOVA_DEC_UMMA (default 1): decode linears on gemv_umma where supported
 GemvTmaPlan gemv_umma_plan(int N, int K, int epi);
 bool gemv_umma_supported(int N, int K, int epi);
-// norm_hid != null (EPI_BF16_SILUMUL): X is x~ = bf16(h * gamma) and every output row b is scaled by
-// rsqrt(mean_k h[b][k]^2 + eps) after the GEMV (h = norm_hid rows, ld D) -- RMSNorm folded (R25).
+// norm_hid != null (EPI_BF16_SILUMUL, EPI_QKV_ROPE_KV): X is x~ = bf16(h * gamma) and every output row b is
+// scaled by rsqrt(mean_k h[b][k]^2 + eps) after the GEMV, before the bias (h = norm_hid rows, ld D) --
+// RMSNorm folded (R25).  EPI_QKV_ROPE_KV needs qa (hd 128: one 128-row block per head; rows, pool, bt, ...).
 cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int K, void* Y, int ldy, const bf16* bias,
                       int B, int epi, float* ws, int* tickets, cudaStream_t s, int sms, unsigned long long* keys,
-                      const bf16* X_lo, const float* norm_hid = nullptr, float norm_eps = 0.f);
+                      const bf16* X_lo, const float* norm_hid = nullptr, float norm_eps = 0.f,
+                      const bf16* ngamma = nullptr, bf16* nxout = nullptr, int ldnx = 0,
+                      const GemvAux* qa = nullptr);
 extern int g_dec_tma_mask;  // decode linears on the persistent TMA GEMV: bit 0 qkv, 1 o, 2 gate|up, 3 down, 4 lm_head
 
 // Flash attention over a fused qkv buffer [S][(H + 2KV) * hd] (q heads, k heads, v heads).
@@ -198,7 +201,7 @@ extern bool g_decode_attn_tc;  // tensor-core decode attention (default) vs the 
 // fixed-order merge); CUDA-core path: partial + combine kernels.
 cudaError_t decode_attn(const bf16* qkv, int ldqkv, bf16* out, int ldo, const bf16* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int* block_tables, int max_pages, const DecodeRow* rows, int B,
-                        int max_ctx, float* ws, int* tickets, cudaStream_t s);
+                        int max_ctx, float* ws, int* tickets, cudaStream_t s, int sms = 0);
 
 // Persistent paged decode attention (decode_attn_p.cu): units (request, KV head, 128-key chunk)
 // on a grid of 3 CTAs per SM of the partition (sms; 0 = whole GPU), chunk partials in ws
@@ -222,6 +225,8 @@ cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf1
 // y_f32: 0 bf16 rows, 1 f32 rows, 2 bf16 hi rows at y and bf16 lo rows at y + M * ldy
 cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
                     cudaStream_t s);
+// x~ = bf16(x * g) rows (the R25 fold's GEMV input when no preceding epilogue wrote it)
+cudaError_t scale_rows_bf16(const float* x, int ldx, const bf16* g, bf16* y, int ldy, int M, int d, cudaStream_t s);
 // streaming layout of a decode weight: [N/64][K/64] pre-swizzled 64 x 64 tiles (8 KB each)
 cudaError_t block_weights(const bf16* src, bf16* dst, int N, int K, cudaStream_t s);
 

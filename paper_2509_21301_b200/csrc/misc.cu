@@ -2,6 +2,8 @@
 // a5-a7): patchify, LayerNorm / RMSNorm ("kernel fusion ... RoPE and
 // RMSNorm"), ViT 2D RoPE, LLM M-RoPE fused with the paged KV-cache write,
 // embedding gather, deterministic argmax.  All are HBM/latency-bound row kernels.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -412,6 +414,22 @@ cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf1
   if (M <= 0) return cudaSuccess;
   if (d % 4) return cudaErrorInvalidValue;
   return launch_k(layernorm_kernel, dim3((M + 7) / 8), dim3(256), 0, s, true, x, ldx, g, b, y, ldy, M, d, eps);
+}
+// x~ = bf16(x * g) rows (DESIGN R25: the input of a GEMV whose RMSNorm row scale is folded after it)
+__global__ void scale_rows_bf16_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ g,
+                                       bf16* __restrict__ y, int ldy, int M, int d) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int n = M * d;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = i / d, c = i - r * d;
+    y[(size_t)r * ldy + c] = __float2bfloat16_rn(x[(size_t)r * ldx + c] * __bfloat162float(g[c]));
+  }
+}
+cudaError_t scale_rows_bf16(const float* x, int ldx, const bf16* g, bf16* y, int ldy, int M, int d, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  const int blocks = std::min(64, (M * d + 255) / 256);
+  return launch_k(scale_rows_bf16_kernel, dim3(blocks), dim3(256), 0, s, true, x, ldx, g, y, ldy, M, d);
 }
 cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
                     cudaStream_t s) {

@@ -36,9 +36,9 @@ int nova_op_flash_attn_mma(const void* qkv, int ld, void* out, int ldo, int Sq, 
 }
 int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int32_t* bt, int max_pages, const nova_decode_row* rows, int B,
-                        int max_ctx, float* ws, int32_t* tickets, void* stream) {
+                        int max_ctx, float* ws, int32_t* tickets, int max_ctas, void* stream) {
   return st(decode_attn((const bf16*)qkv, ld, (bf16*)out, ldo, (const bf16*)kv_pool, layer, n_pages, H, KV, hd, bt,
-                        max_pages, (const DecodeRow*)rows, B, max_ctx, ws, tickets, S(stream)));
+                        max_pages, (const DecodeRow*)rows, B, max_ctx, ws, tickets, S(stream), max_ctas));
 }
 int nova_op_gemv_fused(const void* X, int x_mode, int ldx, const void* W, int N, int K, void* Y, int ldy,
                        const void* bias, int B, int epi, const void* gamma, float eps, int H, int KV, int hd,
@@ -82,9 +82,33 @@ int nova_op_gemv_stream(const void* X, const void* X_lo, int ldx, const void* W_
 }
 int nova_op_gemv_umma(const void* X, const void* X_lo, int ldx, const void* W_blocked, int N, int K, void* Y, int ldy,
                       const void* bias, int B, int epi, float* ws, int32_t* tickets, uint64_t* keys, int max_ctas,
-                      const float* norm_hid, float norm_eps, void* stream) {
+                      const float* norm_hid, float norm_eps, const void* ngamma, void* nxout, int ldnx,
+                      void* stream) {
   return st(gemv_umma((const bf16*)X, ldx, (const bf16*)W_blocked, N, K, Y, ldy, (const bf16*)bias, B, epi, ws,
-                      tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo, norm_hid, norm_eps));
+                      tickets, S(stream), max_ctas, (unsigned long long*)keys, (const bf16*)X_lo, norm_hid, norm_eps,
+                      (const bf16*)ngamma, (bf16*)nxout, ldnx));
+}
+int nova_op_gemv_umma_qkv(const void* X, int ldx, const void* W_blocked, int N, int K, void* Q, int ldq,
+                          const void* bias, int B, const float* norm_hid, float norm_eps, int H, int KV, int hd,
+                          float theta, const nova_decode_row* rows, void* kv_pool, int layer, int n_pages,
+                          const int32_t* bt, int max_pages, float* ws, int32_t* tickets, int max_ctas, void* stream) {
+  GemvAux a;
+  a.H = H;
+  a.KV = KV;
+  a.hd = hd;
+  a.log2_theta = theta > 0.f ? log2f(theta) : 0.f;
+  a.rows = (const DecodeRow*)rows;
+  a.pool = (bf16*)kv_pool;
+  a.layer = layer;
+  a.n_pages = n_pages;
+  a.bt = bt;
+  a.max_pages = max_pages;
+  return st(gemv_umma((const bf16*)X, ldx, (const bf16*)W_blocked, N, K, Q, ldq, (const bf16*)bias, B,
+                      EPI_QKV_ROPE_KV, ws, tickets, S(stream), max_ctas, nullptr, nullptr, norm_hid, norm_eps, nullptr,
+                      nullptr, 0, &a));
+}
+int nova_op_scale_rows_bf16(const float* x, int ldx, const void* gamma, void* y, int ldy, int M, int d, void* stream) {
+  return st(scale_rows_bf16(x, ldx, (const bf16*)gamma, (bf16*)y, ldy, M, d, S(stream)));
 }
 int nova_op_gemv_umma_splits(int N, int K, int epi) { return gemv_umma_plan(N, K, epi).P; }
 int nova_op_decode_attn_p(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,

@@ -80,14 +80,15 @@ static cudaError_t t_gemv(Engine* E, int cls, const void* X, int xmode, int ldx,
   return cudaSuccess;
 }
 
-// Which decode linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 2 o, 4 gate|up,
-// 8 down, 16 lm_head); the choice depends on the op only, never on the partition (co-execution is
-// bitwise == serial).  Default all four (30): with the stream-K decomposition and one elect per ring
+// Which decode linears run on gemv_umma: env NOVA_UMMA_MASK (bits as g_dec_tma_mask: 1 qkv, 2 o,
+// 4 gate|up, 8 down, 16 lm_head); the choice depends on the op only, never on the partition (co-execution
+// is bitwise == serial).  Default all five (31; qkv with its RoPE + KV-append epilogue and the ln1 RMSNorm
+// folded, R25, since round 2 session 3): with the stream-K decomposition and one elect per ring
 // stage (gemv_umma.cu) decode iterations on 24-SM slices and the full GPU are faster than with o /
 // down on the mma.sync GEMVs at B = 2..16 (scripts/gpu_r2_mask.sh; 2B 24 SMs B = 16 6.18 -> 5.97 ms,
 // full GPU 2.64 -> 2.29 ms; 7B 24 SMs B = 16 15.5 -> 12.6 ms), the 48-56-SM 2B range excepted.
 static int umma_mask() {
-  static const int m = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 30;
+  static const int m = getenv("NOVA_UMMA_MASK") ? atoi(getenv("NOVA_UMMA_MASK")) : 31;
   return g_dec_umma ? m : 0;
 }
 
@@ -101,13 +102,14 @@ static cudaError_t t_gemv_tma(Engine* E, const bf16* X, int ldx, const bf16* W, 
   const double bytes = (double)N * K * 2 + (double)B * K * (X_lo ? 4 : 2) + (double)B * nout * ysz;
   E->pass_work[1] += bytes;
   const int i = E->ktimer[1].begin(s);
-  const int op_bit = epi == EPI_BF16_SILUMUL ? 4 : epi == EPI_F32_ARGMAX ? 16 : (K > N ? 8 : 2);
+  const int op_bit = epi == EPI_QKV_ROPE_KV ? 1 : epi == EPI_BF16_SILUMUL ? 4 : epi == EPI_F32_ARGMAX ? 16 : (K > N ? 8 : 2);
   if ((umma_mask() & op_bit) && Wb && gemv_umma_supported(N, K, epi) && (epi != EPI_F32_ARGMAX || X_lo)) {
     // tcgen05 consumer (gemv_umma.cu): the same contract, the ring stage released by the MMA commit
     CUDA_TRY(gemv_umma(X, ldx, Wb, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms,
-                       aux ? aux->keys : nullptr, X_lo, norm_hid, norm_eps));
+                       aux ? aux->keys : nullptr, X_lo, norm_hid, norm_eps, aux ? aux->ngamma : nullptr,
+                       aux ? aux->nxout : nullptr, aux ? aux->ldnx : 0, epi == EPI_QKV_ROPE_KV ? aux : nullptr));
   } else {
-    if (norm_hid) return cudaErrorInvalidValue;  // the folded RMSNorm needs the tcgen05 GEMV
+    if (norm_hid || (aux && aux->nxout)) return cudaErrorInvalidValue;  // the R25 fold needs the tcgen05 GEMV
     CUDA_TRY(gemv_tma(X, ldx, W, N, K, Y, ldy, bias, B, epi, E->dw.gemv_ws, E->dw.tickets, s, sms, aux, Wb, X_lo));
   }
   E->ktimer[1].end(i, cls, bytes, s);
@@ -318,7 +320,6 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
   } else {
     CUDA_TRY(embed(W.embed, D, nullptr, dw.rows, d_last, dw.hid, D, B, s));
   }
-  GemvAux plain;
   GemvAux qa;  // RMSNorm(ln1) on load; bias + RoPE + KV append epilogue
   qa.eps = m.rms_eps;
   qa.H = H;
@@ -336,15 +337,26 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
   // Default, from the model shape only (scripts/gpu_s3p.sh, decode iterations on 8..148 SMs):
   // gate|up, down and lm_head on the TMA GEMV; o as well once it is >= 8 M weights (7B: 4-15%
   // faster on slices, level on the full GPU; 2B's 2.4 M o-proj is faster on the register GEMV).
-  const int tm = g_dec_tma_mask >= 0 ? g_dec_tma_mask : (28 | ((size_t)D * H * hd >= (size_t)8 << 20 ? 2 : 0));
+  // Round 2 session 3: with the stream-K gemv_umma (+ qkv on it, umma_mask) the o-proj goes there for
+  // every shape -- 2B decode B = 2 / 16 on a 24-SM slice 2.56 -> 2.38 / 5.65 -> 5.21 ms, full GPU level
+  // (scripts/gpu_r2_qkv.sh).
+  const int tm = g_dec_tma_mask >= 0 ? g_dec_tma_mask : 30;
   const bool rope_tma = (tm & 1) && hd == 128;
+  // qkv on gemv_umma (RoPE + KV append in its epilogue) with RMSNorm(ln1) folded (R25): x~ = bf16(h * ln1)
+  // comes from the previous layer's down-proj epilogue (or a scale kernel for the first layer run here)
+  const bool qkv_umma = (umma_mask() & 1) && hd == 128 && g_fold_norm && gemv_umma_supported(ldq, D, EPI_QKV_ROPE_KV);
+  bool xt_ln1 = false;  // dw.xb holds x~ for this layer's ln1
   for (int l = l0; l < m.llm_layers; ++l) {
     const LlmLayerW& L = W.llm[l];
     qa.gamma = L.ln1;
     qa.layer = l;
     const int sub = l == l0 ? sub0 : 0;
     if (sub > 0) goto resume;
-    if (rope_tma) {
+    if (qkv_umma) {
+      if (!xt_ln1) CUDA_TRY(scale_rows_bf16(dw.hid, D, L.ln1, dw.xb, D, B, D, s));
+      CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.qkv_w, L.qkv_wb, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV, sms,
+                          &qa, s, nullptr, NOVA_K_DEC_GEMV, dw.hid, m.rms_eps));
+    } else if (rope_tma) {
       CUDA_TRY(rmsnorm(dw.hid, D, L.ln1, dw.xb, 0, D, B, D, m.rms_eps, s));
       CUDA_TRY(t_gemv_tma(this, dw.xb, D, L.qkv_w, L.qkv_wb, ldq, D, dw.qkv, ldq, L.qkv_b, B, EPI_QKV_ROPE_KV, sms,
                           &qa, s));
@@ -361,13 +373,15 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
                                s));
       else
         CUDA_TRY(decode_attn(dw.qkv, ldq, dw.attn, H * hd, pool, l, cfg.kv_pages, H, KV, hd, d_bt, max_pages_per_req,
-                             dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s));
+                             dw.rows, B, max_ctx, dw.attn_ws, dw.tickets + 4096, s, sms));
       ktimer[1].end(i, NOVA_K_DEC_ATTN, kv_bytes_layer, s);
     }
   resume:
-    // RMSNorm(ln2) folded (R25) when gate|up runs on gemv_umma and o on the mma.sync GEMVs: the o-proj
-    // residual epilogue writes x~ = bf16(h * ln2) into dw.xb, gate|up scales rows by rsqrt(mean h^2 + eps)
-    const bool fold = (tm & 4) && (umma_mask() & 4) && !(umma_mask() & 2) && sub == 0 &&
+    // RMSNorm(ln2) folded (R25) when gate|up runs on gemv_umma and o on a GEMV with the next-norm
+    // epilogue (the mma.sync register GEMV or gemv_umma): the o-proj residual epilogue writes
+    // x~ = bf16(h * ln2) into dw.xb, gate|up scales rows by rsqrt(mean h^2 + eps).  Shape-only choice.
+    const bool o_umma = (tm & 2) && (umma_mask() & 2) && gemv_umma_supported(D, H * hd, EPI_F32_RESID);
+    const bool fold = (tm & 4) && (umma_mask() & 4) && (!(tm & 2) || o_umma) && sub == 0 &&
                       gemv_umma_supported(2 * F, D, EPI_BF16_SILUMUL) && g_fold_norm;
     if (sub <= 2) {
     GemvAux oa;
@@ -392,12 +406,19 @@ cudaError_t Engine::run_decode(const std::vector<Request*>& rq, const std::vecto
                       na, s));
     }
     }
+    {
+    // the next layer's folded ln1 input from this residual epilogue (gemv_umma or the register GEMV)
+    GemvAux da;
+    const bool down_umma = (tm & 8) && (umma_mask() & 8) && gemv_umma_supported(D, F, EPI_F32_RESID);
+    xt_ln1 = qkv_umma && l + 1 < m.llm_layers && (down_umma || !(tm & 8));
+    if (xt_ln1) da.ngamma = W.llm[l + 1].ln1, da.nxout = dw.xb, da.ldnx = D;
     if (tm & 8)
       CUDA_TRY(t_gemv_tma(this, dw.act, F, L.down_w, L.down_wb, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID, sms,
-                          nullptr, s));
+                          &da, s));
     else
       CUDA_TRY(t_gemv(this, NOVA_K_DEC_GEMV, dw.act, 0, F, L.down_w, D, F, dw.hid, D, nullptr, B, EPI_F32_RESID,
-                      plain, s));
+                      da, s));
+    }
   }
   // final RMSNorm -> lm_head -> fused greedy argmax (f32 lm_head input, R7)
   GemvAux la;

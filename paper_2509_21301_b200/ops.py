@@ -67,12 +67,12 @@ def nova_op_flash_attn_mma(qkv, out, S, H, KV, hd, causal, stream=None):
 
 
 def nova_op_decode_attn(qkv, out, kv_pool, layer, n_pages, H, KV, hd, block_tables, rows, B, max_ctx, ws,
-                        tickets=None, stream=None):
+                        tickets=None, max_ctas=0, stream=None):
     if tickets is None:
         tickets = torch.zeros(B * KV, dtype=torch.int32, device=qkv.device)
     check(lib().nova_op_decode_attn(_p(qkv), qkv.stride(0), _p(out), out.stride(0), _p(kv_pool), layer, n_pages,
                                     H, KV, hd, _p(block_tables), block_tables.shape[1], _p(rows), B, max_ctx, _p(ws),
-                                    _p(tickets), _s(stream)), "decode_attn")
+                                    _p(tickets), max_ctas, _s(stream)), "decode_attn")
 
 
 def nova_op_gemv_fused(X, x_mode, W, Y, bias, N, K, B, epi, gamma=None, eps=0.0, H=0, KV=0, hd=0, theta=0.0,
@@ -145,7 +145,7 @@ def nova_op_gemv_stream(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_
 
 
 def nova_op_gemv_umma(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_ctas=0, ldx=None, ldy=None,
-                      norm_hid=None, norm_eps=0.0, stream=None):
+                      norm_hid=None, norm_eps=0.0, ngamma=None, nxout=None, stream=None):
     dev = X.device
     if dev not in _ws_cache:
         _ws_cache[dev] = (torch.empty(16 * 16 * 160000, dtype=torch.float32, device=dev),
@@ -153,7 +153,27 @@ def nova_op_gemv_umma(X, Wb, Y, bias, N, K, B, epi, X_lo=None, keys=None, max_ct
     ws, tk = _ws_cache[dev]
     check(lib().nova_op_gemv_umma(_p(X), _p(X_lo), ldx or X.stride(0), _p(Wb), N, K, _p(Y), ldy or Y.stride(0),
                                   _p(bias), B, epi, _p(ws), _p(tk), _p(keys), max_ctas, _p(norm_hid), float(norm_eps),
+                                  _p(ngamma), _p(nxout), nxout.stride(0) if nxout is not None else 0,
                                   _s(stream)), "gemv_umma")
+
+
+def nova_op_gemv_umma_qkv(X, Wb, Q, bias, N, K, B, norm_hid, norm_eps, H, KV, hd, theta, rows, kv_pool, layer,
+                          n_pages, block_tables, max_ctas=0, stream=None):
+    import ctypes as C
+    dev = X.device
+    if dev not in _ws_cache:
+        _ws_cache[dev] = (torch.empty(16 * 16 * 160000, dtype=torch.float32, device=dev),
+                          torch.zeros(8192, dtype=torch.int32, device=dev))
+    ws, tk = _ws_cache[dev]
+    check(lib().nova_op_gemv_umma_qkv(_p(X), X.stride(0), _p(Wb), N, K, _p(Q), Q.stride(0), _p(bias), B,
+                                      _p(norm_hid), C.c_float(norm_eps), H, KV, hd, C.c_float(theta), _p(rows),
+                                      _p(kv_pool), layer, n_pages, _p(block_tables), block_tables.shape[1], _p(ws),
+                                      _p(tk), max_ctas, _s(stream)), "gemv_umma_qkv")
+
+
+def nova_op_scale_rows_bf16(x, gamma, y, M, d, stream=None):
+    check(lib().nova_op_scale_rows_bf16(_p(x), x.stride(0), _p(gamma), _p(y), y.stride(0), M, d, _s(stream)),
+          "scale_rows_bf16")
 
 
 def nova_op_gemv_umma_splits(N: int, K: int, epi: int) -> int:

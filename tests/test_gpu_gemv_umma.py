@@ -156,3 +156,83 @@ def test_umma_gate_up_with_folded_rmsnorm(F, D, B):
     xn = V.rms_norm(h.astype(np.float64), gam, 1e-6)
     ref = V.silu(V.linear(xn, G.astype(np.float64))) * V.linear(xn, U.astype(np.float64))
     assert rel_inf(bf16_host(outs[0]), ref) <= 8e-3
+
+
+@pytest.mark.parametrize("D,F,B", [(1536, 8960, 2), (3584, 3584, 16), (128, 256, 3)])
+def test_umma_resid_writes_next_norm_input(D, F, B):
+    """DESIGN R25, the o-proj half of the fold: Y += X W^T (f32, oracle linear) and nxout = bf16(Y_new * gamma),
+    bitwise against the host rounding of the GPU's own Y_new; bitwise invariant to the SM budget."""
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    rng = np.random.default_rng(D + F + B)
+    Wd = rand_bf16(rng, (D, F), F ** -0.5)
+    Xa = rand_bf16(rng, (B, F))
+    gam = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (D,), 0.1) + 1.0))
+    base = rng.standard_normal((B, D)).astype(np.float32)
+    Wb = _blocked(Wd, D, F)
+    got = []
+    for ctas in (0, 24):
+        Y = torch.from_numpy(base.copy()).cuda()
+        nx = torch.zeros(B, D, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_gemv_umma(bf16_dev(Xa), Wb, Y, None, D, F, B, O.EPI_F32_RESID, max_ctas=ctas,
+                            ngamma=bf16_dev(gam), nxout=nx)
+        torch.cuda.synchronize()
+        got.append((Y, nx))
+    assert torch.equal(got[0][0], got[1][0]) and torch.equal(got[0][1], got[1][1])
+    Y, nx = got[0][0].cpu().numpy(), got[0][1]
+    ref = base.astype(np.float64) + V.linear(Xa.astype(np.float64), Wd.astype(np.float64))
+    assert rel_inf(Y, ref) <= 1e-4
+    want = f32_to_bf16_bits((Y * gam).astype(np.float32))
+    assert np.array_equal(nx.view(torch.int16).cpu().numpy().view(np.uint16), want)
+
+
+@pytest.mark.parametrize("H,KV,D", [(12, 2, 1536), (28, 4, 3584), (2, 1, 256)])
+def test_umma_qkv_folded_rmsnorm_rope_kv_append(H, KV, D):
+    """Decode qkv on tcgen05: x~ = bf16(h * ln1) (scale_rows_bf16), the RMSNorm row scale
+    folded after the GEMV (R25), + bias, RoPE at pos on q / k, k / v appended to the paged cache -- vs the
+    oracle (rms_norm, linear, mrope_tables / apply_rope at t = h = w), bf16 rel-inf <= 8e-3; bitwise
+    invariant to the SM budget and to the batch composition (row 0)."""
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    hd, n_pages, max_pages, theta, eps = 128, 64, 8, 1e6, 1e-6
+    rng = np.random.default_rng(H * 11 + D)
+    N = (H + 2 * KV) * hd
+    W = rand_bf16(rng, (N, D), D ** -0.5)
+    bias = rand_bf16(rng, (N,), 0.05)
+    gam = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (D,), 0.1) + 1.0))
+    bt = torch.from_numpy(rng.permutation(n_pages)[:4 * max_pages].reshape(4, max_pages).astype(np.int32)).cuda()
+    Wb, db, dg = _blocked(W, N, D), bf16_dev(bias), bf16_dev(gam)
+    Xh = (rng.standard_normal((16, D)) * 2).astype(np.float32)
+    got0 = None
+    for B, ctas in ((1, 0), (4, 24), (16, 0), (16, 40)):
+        r = np.array([[b % 4, 320 + b, int(rng.integers(0, 3000)), 0] for b in range(B)], np.int32)
+        r[:min(B, 4), 1] = [0, 63, 64, 300][:min(B, 4)]    # page boundaries
+        r[0, 2] = 1234
+        pool = torch.zeros(2, n_pages, 2, KV, 64, hd, dtype=torch.bfloat16, device="cuda")
+        rows = torch.from_numpy(r).cuda()
+        Q = torch.zeros(B, N, dtype=torch.bfloat16, device="cuda")
+        hd_ = torch.from_numpy(Xh[:B]).cuda()
+        xt = torch.empty(B, D, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_scale_rows_bf16(hd_, dg, xt, B, D)
+        O.nova_op_gemv_umma_qkv(xt, Wb, Q, db, N, D, B, hd_, eps, H, KV, hd, theta, rows, pool, 1, n_pages, bt,
+                                max_ctas=ctas)
+        torch.cuda.synchronize()
+        assert np.array_equal(xt.view(torch.int16).cpu().numpy().view(np.uint16),
+                              f32_to_bf16_bits((Xh[:B] * gam).astype(np.float32)))
+        xn = V.rms_norm(Xh[:B].astype(np.float64), gam, eps)
+        y = V.linear(xn, W.astype(np.float64), bias.astype(np.float64))
+        pos3 = np.tile(r[:, 2], (3, 1))
+        c, s = V.mrope_tables(pos3, hd, theta, (hd // 2, 0, 0), np.float64)
+        q = V.apply_rope(y[:, :H * hd].reshape(B, H, hd), c, s)
+        k = V.apply_rope(y[:, H * hd:(H + KV) * hd].reshape(B, KV, hd), c, s)
+        v = y[:, (H + KV) * hd:].reshape(B, KV, hd)
+        assert rel_inf(bf16_host(Q[:, :H * hd]).reshape(B, H, hd), q) <= 8e-3
+        P = bf16_host(pool[1])
+        btn = bt.cpu().numpy()
+        for b in range(B):
+            pg, off = btn[r[b, 0], r[b, 1] // 64], r[b, 1] % 64
+            assert rel_inf(P[pg, 0, :, off], k[b]) <= 8e-3
+            assert rel_inf(P[pg, 1, :, off], v[b]) <= 8e-3
+        assert float(np.abs(bf16_host(pool[0])).max()) == 0.0     # other layers untouched
+        row0 = Q[0].view(torch.int16).cpu()
+        if got0 is None:
+            got0 = row0
+        assert torch.equal(row0, got0)
