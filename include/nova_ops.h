@@ -42,6 +42,24 @@ enum {
  * Bitwise independent of max_ctas. */
 int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
                  int K, int epi, int max_ctas, void* stream);
+/* The same GEMM with the prefill RMSNorm fold (DESIGN R25; "kernel fusion ... RMSNorm";
+ * RMSNorm(h) W^T = rsqrt(mean h^2 + eps) * ((h * gamma) W^T) row by row):
+ *  - epi NOVA_EPI_F32_RESID with nxout != NULL (ngamma bf16 [N], nss f32 required; N % 32 == 0): after
+ *    C[m][n] += acc also nxout[m * ldnx + n] = bf16(C[m][n] * ngamma[n]) and, for each 32-column chunk t,
+ *    nss[m * nss_ld + t] = sum over the chunk of C[m][n]^2 (one fixed order);
+ *  - epi NOVA_EPI_BF16 / NOVA_EPI_BF16_SILUMUL with rscale != NULL: A holds x~ and row m's accumulators are
+ *    multiplied by rscale[m] (nova_op_fold_rows) before the bias.
+ * NULL pointers = that half off.  Bitwise independent of max_ctas. */
+int nova_op_gemm_fold(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
+                      int K, int epi, int max_ctas, const void* ngamma, void* nxout, int ldnx, float* nss, int nss_ld,
+                      const float* rscale, void* stream);
+/* rscale[m] = rsqrt((ss[m * ss_ld + 0] + ... + ss[m * ss_ld + d / 32 - 1], in that order) / d + eps) for
+ * M rows (d % 128 == 0, ss_ld % 4 == 0): the folded RMSNorm's row scales from the chunk sums. */
+int nova_op_fold_rows(const float* ss, int ss_ld, int d, float eps, float* rscale, int M, void* stream);
+/* The first folded RMSNorm's inputs from f32 rows x [M][d] (d % 32 == 0): y = bf16(x * gamma) (ldy) and
+ * ss[m * ss_ld + t] = sum of x[m][32 t .. 32 t + 31]^2 in column order. */
+int nova_op_rms_prep(const float* x, int ldx, const void* gamma, void* y, int ldy, float* ss, int ss_ld, int M, int d,
+                     void* stream);
 
 /* GEMM tile selection.  nova_op_gemm chooses, from the shape alone (never from max_ctas,
  * so results stay bitwise independent of the partition), between single-CTA 128 x BN
@@ -95,14 +113,15 @@ typedef struct {
 /* Paged decode attention (a7; PAPER.md P:141, P:283 -- memory-bound, PagedAttention
  * KV layout P:48).  Keys 0..ctx (inclusive) of each row.  kv_pool bf16
  * [layers][n_pages][2][KV][64][hd]; block_tables int32 [slots][max_pages];
- * ws f32 workspace of B*H*ceil((max_ctx+1)/64)*(hd+2) floats; tickets int32 [B*KV],
+ * ws f32 workspace of max(B*H*ceil((max_ctx+1)/64), B*H*48)*(hd+2) floats; tickets int32 [B*KV],
  * zero on entry and left zero (one launch: chunk partials + last-CTA fixed-order merge).
  * ceil((max_ctx+1)/128) <= 64, H/KV <= 16.  Deterministic, batch- and grid-invariant. */
 int nova_op_decode_attn(const void* qkv, int ld, void* out, int ldo, const void* kv_pool, int layer, int n_pages,
                         int H, int KV, int hd, const int32_t* block_tables, int max_pages, const nova_decode_row* rows,
                         int B, int max_ctx, float* ws, int32_t* tickets, int max_ctas, void* stream);
 /* max_ctas: SM budget of the partition (0 = whole GPU); it picks the K/V ring depth (2 stages, one CTA per
- * SM, or 1 stage, two CTAs per SM), never the result. */
+ * SM, or 1 stage, two CTAs per SM) and, when even that takes more than one wave, fewer physical CTAs per
+ * (request, KV head) that run the cluster's virtual CTAs in turn and merge through ws -- never the result. */
 
 /* Persistent paged decode attention (decode_attn_p.cu): same contract as nova_op_decode_attn
  * (rows[b] = {slot, ctx, pos, pad}: query b attends keys 0..ctx of its slot's pages; GQA), work

@@ -573,6 +573,79 @@ NOVA_DEV float ld_dsmem_f32(uint32_t local_saddr, uint32_t rank) {
   return v;
 }
 
+// One 32-key block of the tensor-core decode attention for one warp: scores of the (<= 16) GQA rows
+// against keys k0..k0+31 (K rows wK, V rows wV in shared memory, padded pitch HDP), online softmax
+// (running max mx, sum ls per row pair) and P.V into o.  Shared by both decode-attention kernels.
+template <int HD>
+NOVA_DEV void da_block(const bf16* wK, const bf16* wV, int k0, int L, const uint32_t (&qa)[HD / 16][4],
+                       float (&mx)[2], float (&ls)[2], float (&o)[HD / 8][4], float scale_log2, int lane) {
+  constexpr int HDP = HD + 8, KT = HD / 16, DT = HD / 8;
+  const int c = lane & 3;
+  float sc[4][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      uint32_t bb[2];
+      ldmatrix_x2(bb, smem_u32(wK + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
+      mma_bf16_16816(sc[nt], qa[kk], bb);
+    }
+  }
+  // rows g (sc[.][0..1]) and g+8 (sc[.][2..3]); keys k0 + nt*8 + 2c + (j&1)
+  float bm[2] = {-1e30f, -1e30f};
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = k0 + nt * 8 + 2 * c + (j & 1) < L;
+      sc[nt][j] = ok ? sc[nt][j] * scale_log2 : -1e30f;
+      bm[j >> 1] = fmaxf(bm[j >> 1], sc[nt][j]);
+    }
+  float corr[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 1));
+    bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 2));
+    const float mn = fmaxf(mx[r], bm[r]);
+    corr[r] = exp2f(mx[r] - mn);
+    mx[r] = mn;
+  }
+  float ps[2] = {0.f, 0.f};
+  uint32_t pa[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const float p0 = exp2f(sc[nt][0] - mx[0]), p1 = exp2f(sc[nt][1] - mx[0]);
+    const float p2 = exp2f(sc[nt][2] - mx[1]), p3 = exp2f(sc[nt][3] - mx[1]);
+    ps[0] += p0 + p1;
+    ps[1] += p2 + p3;
+    pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+    pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 1);
+    ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 2);
+    ls[r] = ls[r] * corr[r] + ps[r];
+  }
+#pragma unroll
+  for (int dt = 0; dt < DT; ++dt) {
+    o[dt][0] *= corr[0];
+    o[dt][1] *= corr[0];
+    o[dt][2] *= corr[1];
+    o[dt][3] *= corr[1];
+  }
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      uint32_t bb[2];
+      ldmatrix_x2_trans(bb, smem_u32(wV + (kk * 16 + (lane & 15)) * HDP + dt * 8));
+      mma_bf16_16816(o[dt], pa[kk], bb);
+    }
+  }
+}
+
 template <int HD, int CL, int NST>
 __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* __restrict__ qkv, int ld,
                                                              const bf16* __restrict__ pool, int layer, int n_pages,
@@ -666,69 +739,7 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
     const bf16* wK = ring + (size_t)(NST == 2 ? (it & 1) : 0) * (Cf::BLK / 2);
     const bf16* wV = wK + TKW * HDP;
     const int k0 = blk * TKW;
-    float sc[4][4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < KT; ++kk) {
-        uint32_t bb[2];
-        ldmatrix_x2(bb, smem_u32(wK + (nt * 8 + (lane & 7)) * HDP + kk * 16 + ((lane >> 3) & 1) * 8));
-        mma_bf16_16816(sc[nt], qa[kk], bb);
-      }
-    }
-    // rows g (sc[.][0..1]) and g+8 (sc[.][2..3]); keys k0 + nt*8 + 2c + (j&1)
-    float bm[2] = {-1e30f, -1e30f};
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool ok = k0 + nt * 8 + 2 * c + (j & 1) < L;
-        sc[nt][j] = ok ? sc[nt][j] * scale_log2 : -1e30f;
-        bm[j >> 1] = fmaxf(bm[j >> 1], sc[nt][j]);
-      }
-    float corr[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 1));
-      bm[r] = fmaxf(bm[r], __shfl_xor_sync(0xffffffffu, bm[r], 2));
-      const float mn = fmaxf(mx[r], bm[r]);
-      corr[r] = exp2f(mx[r] - mn);
-      mx[r] = mn;
-    }
-    float ps[2] = {0.f, 0.f};
-    uint32_t pa[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const float p0 = exp2f(sc[nt][0] - mx[0]), p1 = exp2f(sc[nt][1] - mx[0]);
-      const float p2 = exp2f(sc[nt][2] - mx[1]), p3 = exp2f(sc[nt][3] - mx[1]);
-      ps[0] += p0 + p1;
-      ps[1] += p2 + p3;
-      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
-      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 1);
-      ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 2);
-      ls[r] = ls[r] * corr[r] + ps[r];
-    }
-#pragma unroll
-    for (int dt = 0; dt < DT; ++dt) {
-      o[dt][0] *= corr[0];
-      o[dt][1] *= corr[0];
-      o[dt][2] *= corr[1];
-      o[dt][3] *= corr[1];
-    }
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-#pragma unroll
-      for (int dt = 0; dt < DT; ++dt) {
-        uint32_t bb[2];
-        ldmatrix_x2_trans(bb, smem_u32(wV + (kk * 16 + (lane & 15)) * HDP + dt * 8));
-        mma_bf16_16816(o[dt], pa[kk], bb);
-      }
-    }
+    da_block<HD>(wK, wV, k0, L, qa, mx, ls, o, scale_log2, lane);
     __syncwarp();  // this stage is refilled NST blocks later
     if constexpr (NST == 1) {
       if (nxt < nblk) issue(nxt, 0);
@@ -800,6 +811,198 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
   cluster_sync_all();  // peers keep their shared memory alive until rank 0 has read it
 }
 
+// The same decode attention with CLP < VC physical CTAs per (request, KV head) (session 3): the
+// VC = da_cluster(KV) "virtual" CTAs of the cluster kernel above keep their block streams (virtual
+// rank v, warp w: blocks v DA_W + w, + DA_W VC, ...), physical rank p runs the virtual ranks p, p + CLP,
+// ... one after another through one continuous cp.async ring, and every (virtual rank, warp) state goes
+// to the workspace; after a cluster barrier the CLP CTAs merge disjoint column ranges: per virtual rank
+// the warp states in warp order, then the virtual ranks in rank order -- the cluster kernel's
+// operations in its order, so the output is bitwise the same.  Fewer, longer CTAs for large batches
+// on a small partition (one wave instead of B KV VC / (2 SMs) of them).  ws: B KV VC DA_W G (HD + 2) floats.
+template <int HD, int VC, int NST>
+__global__ void __launch_bounds__(32 * DA_W) decode_attn_v_kernel(const bf16* __restrict__ qkv, int ld,
+                                                            const bf16* __restrict__ pool, int layer, int n_pages,
+                                                            int H, int KV, const int* __restrict__ bt, int max_pages,
+                                                            const DecodeRow* __restrict__ rows, bf16* __restrict__ out,
+                                                            int ldo, float scale_log2, float* __restrict__ ws) {
+  using Cf = DtcCfg<HD, NST>;
+  constexpr int HDP = Cf::HDP, CH = HD / 8, KT = HD / 16, DT = HD / 8, PW = HD + 2;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  bf16* sQ = reinterpret_cast<bf16*>(dsm);
+  float* sML = reinterpret_cast<float*>(dsm + Cf::Q_BYTES);  // phase 2: [VC][DA_W][16] (m, l) (the ring is free)
+  pdl_launch_dependents();
+  const int CLP = gridDim.x;
+  const int rank = (int)cluster_rank();
+  const int kvh = blockIdx.y, b = blockIdx.z;
+  const int G = H / KV;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {  // L2 warm-up before griddepcontrol.wait, as in the cluster kernel
+    const DecodeRow r0 = rows[b];
+    const int L0 = r0.ctx + 1, nb = (L0 + TKW - 1) / TKW;
+    const size_t ps = (size_t)2 * KV * 64 * HD;
+    const bf16* lb = pool + (size_t)layer * n_pages * ps;
+    const int* bt0 = bt + (size_t)r0.slot * max_pages;
+    for (int v = rank; v < VC; v += CLP)
+      for (int blk = v * DA_W + warp; blk < nb; blk += DA_W * VC) {
+        const int j = blk * TKW + lane;
+        if (j < L0) {
+          const bf16* kp = lb + (size_t)bt0[j >> 6] * ps + ((size_t)kvh * 64 + (j & 63)) * HD;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + 64));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + (size_t)KV * 64 * HD));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kp + (size_t)KV * 64 * HD + 64));
+        }
+      }
+  }
+  pdl_wait();
+  const DecodeRow rr = rows[b];
+  const int L = rr.ctx + 1;
+  for (int i = tid; i < 16 * CH; i += 32 * DA_W) {  // Q rows g < G (rows >= G zero)
+    const int r = i / CH, c = i % CH;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < G) v = *reinterpret_cast<const uint4*>(qkv + (size_t)b * ld + (size_t)(kvh * G + r) * HD + c * 8);
+    *reinterpret_cast<uint4*>(sQ + r * HDP + c * 8) = v;
+  }
+  const size_t page_stride = (size_t)2 * KV * 64 * HD;
+  const bf16* lbase = pool + (size_t)layer * n_pages * page_stride;
+  const int* btr = bt + (size_t)rr.slot * max_pages;
+  const int nblk = (L + TKW - 1) / TKW;
+  const int wstride = DA_W * VC;
+  bf16* ring = reinterpret_cast<bf16*>(dsm + Cf::Q_BYTES) + (size_t)warp * NST * (Cf::BLK / 2);
+  auto issue = [&](int blk, int stage) {
+    bf16* wK = ring + (size_t)stage * (Cf::BLK / 2);
+    bf16* wV = wK + TKW * HDP;
+    const int k0 = blk * TKW;
+    for (int i = lane; i < TKW * CH; i += 32) {
+      const int r = i / CH, c = i % CH;
+      const int j = k0 + r;
+      const bool ok = j < L;
+      const int jj = ok ? j : k0;
+      const bf16* kp = lbase + (size_t)btr[jj >> 6] * page_stride + ((size_t)kvh * 64 + (jj & 63)) * HD + c * 8;
+      cp_async16(wK + r * HDP + c * 8, kp, ok);
+      cp_async16(wV + r * HDP + c * 8, kp + (size_t)KV * 64 * HD, ok);
+    }
+  };
+  // this warp's blocks, virtual rank by virtual rank: (v, blk) -> the next one (v = VC: none)
+  auto next = [&](int& v, int& blk) {
+    blk += wstride;
+    if (blk >= nblk) {
+      v += CLP;
+      blk = v * DA_W + warp;
+      if (blk >= nblk) v = VC;  // later virtual ranks of this warp are empty too
+    }
+  };
+  int v0 = rank, b0 = rank * DA_W + warp;
+  if (b0 >= nblk) v0 = VC;
+  if (v0 < VC) issue(b0, 0);
+  cp_async_commit();
+  __syncthreads();  // Q in smem
+  const int g = lane >> 2, c = lane & 3;
+  uint32_t qa[KT][4];
+#pragma unroll
+  for (int kk = 0; kk < KT; ++kk) ldmatrix_x4(qa[kk], smem_u32(sQ + (lane & 15) * HDP + kk * 16 + (lane >> 4) * 8));
+  float* wsb = ws + (size_t)(b * KV + kvh) * VC * DA_W * G * PW;
+  auto store_state = [&](int v, const float (&mx)[2], const float (&ls)[2], const float (&o)[DT][4]) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = g + 8 * r;
+      if (row >= G) continue;
+      float* w = wsb + ((size_t)(v * DA_W + warp) * G + row) * PW;
+      if (c == 0) {
+        w[0] = mx[r];
+        w[1] = ls[r];
+      }
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        w[2 + dt * 8 + 2 * c] = o[dt][2 * r];
+        w[2 + dt * 8 + 2 * c + 1] = o[dt][2 * r + 1];
+      }
+    }
+  };
+  float mx[2] = {-1e30f, -1e30f}, ls[2] = {0.f, 0.f};
+  float o[DT][4];
+#pragma unroll
+  for (int dt = 0; dt < DT; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+  int vs = rank;  // the virtual rank whose state is being accumulated (states of empty ones are stored too)
+  int it = 0;
+  for (int v = v0, blk = b0; v < VC; ++it) {
+    int nv = v, nb = blk;
+    next(nv, nb);
+    if constexpr (NST == 2) {
+      if (nv < VC) issue(nb, (it + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    while (vs < v) {  // virtual ranks finished (or empty) before this block's
+      store_state(vs, mx, ls, o);
+      mx[0] = mx[1] = -1e30f, ls[0] = ls[1] = 0.f;
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+      vs += CLP;
+    }
+    const bf16* wK = ring + (size_t)(NST == 2 ? (it & 1) : 0) * (Cf::BLK / 2);
+    const bf16* wV = wK + TKW * HDP;
+    da_block<HD>(wK, wV, blk * TKW, L, qa, mx, ls, o, scale_log2, lane);
+    __syncwarp();
+    if constexpr (NST == 1) {
+      if (nv < VC) issue(nb, 0);
+      cp_async_commit();
+    }
+    v = nv, blk = nb;
+  }
+  for (; vs < VC; vs += CLP) {  // the last accumulated state, then the empty ones
+    store_state(vs, mx, ls, o);
+    mx[0] = mx[1] = -1e30f, ls[0] = ls[1] = 0.f;
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+  }
+  cp_async_wait<0>();
+  __threadfence();
+  __syncthreads();
+  if (CLP > 1) cluster_sync_all();  // every warp state of the (request, KV head) is in ws
+  // phase 2: (m, l) of all VC x DA_W states to smem, then this CTA's columns d in [d0, d1)
+  for (int i = tid; i < VC * DA_W * G; i += 32 * DA_W) {
+    const float* w = wsb + (size_t)i * PW;
+    sML[2 * i] = __ldcg(w);
+    sML[2 * i + 1] = __ldcg(w + 1);
+  }
+  __syncthreads();
+  const int d0 = (rank * HD) / CLP, d1 = ((rank + 1) * HD) / CLP;
+  for (int i = tid; i < G * (d1 - d0); i += 32 * DA_W) {
+    const int row = i / (d1 - d0), d = d0 + i % (d1 - d0);
+    float Mv[VC], Lv[VC], Av[VC];
+#pragma unroll
+    for (int q = 0; q < VC; ++q) {
+      float M = -1e30f;
+#pragma unroll
+      for (int w = 0; w < DA_W; ++w) M = fmaxf(M, sML[2 * ((q * DA_W + w) * G + row)]);
+      float accl = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < DA_W; ++w) {
+        const int k = (q * DA_W + w) * G + row;
+        const float f = exp2f(sML[2 * k] - M);
+        accl += f * sML[2 * k + 1];
+        acc += f * __ldcg(wsb + (size_t)k * PW + 2 + d);
+      }
+      Mv[q] = M, Lv[q] = accl, Av[q] = acc;
+    }
+    float M = Mv[0];
+#pragma unroll
+    for (int q = 1; q < VC; ++q) M = fmaxf(M, Mv[q]);
+    float num = 0.f, den = 0.f;
+#pragma unroll
+    for (int q = 0; q < VC; ++q) {
+      const float f = exp2f(Mv[q] - M);
+      den += f * Lv[q];
+      num += f * Av[q];
+    }
+    out[(size_t)b * ldo + (size_t)(kvh * G + row) * HD + d] = __float2bfloat16_rn(num / den);
+  }
+}
+
 template <int HD>
 __global__ void decode_attn_combine(const float* __restrict__ ws, const DecodeRow* __restrict__ rows, bf16* out,
                                     int ldo, int H, int n_chunks, int keys_per_part) {
@@ -835,6 +1038,44 @@ cudaError_t da_launch(const bf16* qkv, int ld, bf16* out, int ldo, const bf16* p
     static const int force = getenv("NOVA_DA_NST") ? atoi(getenv("NOVA_DA_NST")) : 0;
     const int nsm = sms > 0 ? sms : 148;
     const int nst = force ? force : (CLN * KV * B > nsm ? 1 : 2);
+    // more than three waves even at two CTAs per SM: CLP < CLN physical CTAs per (request, KV head) run the
+    // CLN virtual ones (decode_attn_v_kernel, bitwise the same output; its workspace merge costs more
+    // than one or two extra waves -- scripts/gpu_r2_dav.sh: 2B B = 16 on 16 / 24 / 32 SMs -12% / -4% / -7%,
+    // 2B B = 8 on 32 SMs (two waves) +5%); env NOVA_DA_V = 0 disables, 2 = 2-stage ring
+    static const int vmode = getenv("NOVA_DA_V") ? atoi(getenv("NOVA_DA_V")) : 1;
+    if (vmode && ws && CLN * KV * B > 3 * 2 * nsm) {
+      int clp = CLN / 2;
+      while (clp > 1 && clp * KV * B > 2 * nsm) clp /= 2;
+      const int vst = vmode == 2 ? 2 : 1;
+      auto vk = CLN == 8 ? (vst == 1 ? decode_attn_v_kernel<HD, 8, 1> : decode_attn_v_kernel<HD, 8, 2>)
+                         : (vst == 1 ? decode_attn_v_kernel<HD, 4, 1> : decode_attn_v_kernel<HD, 4, 2>);
+      static bool vset = false;
+      if (!vset) {
+        cudaFuncSetAttribute(decode_attn_v_kernel<HD, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 1>::SMEM);
+        cudaFuncSetAttribute(decode_attn_v_kernel<HD, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 1>::SMEM);
+        cudaFuncSetAttribute(decode_attn_v_kernel<HD, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 2>::SMEM);
+        cudaFuncSetAttribute(decode_attn_v_kernel<HD, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DtcCfg<HD, 2>::SMEM);
+        vset = true;
+      }
+      cudaLaunchConfig_t vc = {};
+      vc.gridDim = dim3(clp, KV, B);
+      vc.blockDim = dim3(32 * DA_W);
+      vc.dynamicSmemBytes = vst == 1 ? DtcCfg<HD, 1>::SMEM : DtcCfg<HD, 2>::SMEM;
+      vc.stream = s;
+      cudaLaunchAttribute va[2];
+      va[0].id = cudaLaunchAttributeClusterDimension;
+      va[0].val.clusterDim.x = clp;
+      va[0].val.clusterDim.y = 1;
+      va[0].val.clusterDim.z = 1;
+      va[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      va[1].val.programmaticStreamSerializationAllowed = 1;
+      vc.attrs = va;
+      vc.numAttrs = g_use_pdl ? 2 : 1;
+      count_launch();
+      e = cudaLaunchKernelEx(&vc, vk, qkv, ld, pool, layer, n_pages, H, KV, bt, max_pages, rows, out, ldo, sl2, ws);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
     auto kern = CLN == 8 ? (nst == 1 ? decode_attn_tc_kernel<HD, 8, 1> : decode_attn_tc_kernel<HD, 8, 2>)
                          : (nst == 1 ? decode_attn_tc_kernel<HD, 4, 1> : decode_attn_tc_kernel<HD, 4, 2>);
     static bool set = false;

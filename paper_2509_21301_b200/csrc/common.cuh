@@ -126,6 +126,20 @@ NOVA_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* ba
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// L2 policy for data read once per pass (decode weights): evict first, so a co-running stage's
+// working set (ViT / prefill GEMM tiles, attention K/V) keeps its L2 lines
+NOVA_DEV uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+NOVA_DEV void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 
 // ------------------------------------------------------------------ tcgen05 (UMMA, TMEM)
 NOVA_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {  // whole warp

@@ -211,6 +211,8 @@ class Engine {
   struct FrontWS {
     bf16 *x0, *xb, *qkv, *attn, *act;
     float *hid, *vhid, *xf, *logits;
+    float* nss;     // prefill RMSNorm fold (R25): [S][D / 32] partial sums of squares
+    float* rscale;  // ... and the row scales [S]
     int *pos3, *tok;
     unsigned long long* keys;  // greedy argmax (EPI_F32_ARGMAX), zero between passes
     int* h_pos3;  // pinned

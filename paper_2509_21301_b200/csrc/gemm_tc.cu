@@ -27,6 +27,7 @@ struct GemmArgs {
   void* C;
   const bf16* bias;
   int M, N, K, ldc;
+  GemmFold f;  // RMSNorm fold (DESIGN R25; all null = off)
 };
 
 template <int BN>
@@ -114,7 +115,7 @@ NOVA_DEV void epilogue32(const GemmArgs& g, int m, int n0, float* v) {
 // 32 rows per instruction -- the residual read-modify-write of the row-per-thread form was the
 // bottleneck of the K = 1280 ViT linears (27.7 vs 16.2 us with a plain bf16 store).
 template <int EPI>
-NOVA_DEV void epilogue32_staged(const GemmArgs& g, int m_base, int n0, float* v, float* stg, int lane) {
+NOVA_DEV void epilogue32_staged(const GemmArgs& g, int m_base, int n0, float* v, float* stg, int lane, float rs = 1.f) {
   constexpr int NC_ = EPI == EPI_BF16_SILUMUL ? 16 : 32;
   constexpr int RPI_ = 32 / (NC_ / 4);
   // residual rows of the read-back pattern, requested first so their latency hides behind the
@@ -127,6 +128,12 @@ NOVA_DEV void epilogue32_staged(const GemmArgs& g, int m_base, int n0, float* v,
       const int m = m_base + it * RPI_ + rsub;
       res[it] = m < g.M ? __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(g.C) + (size_t)m * g.ldc + n0) + q)
                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_SILUMUL) {
+    if (g.f.rscale != nullptr) {  // folded RMSNorm: row scale before the bias
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= rs;
     }
   }
   if (g.bias != nullptr) {
@@ -169,6 +176,26 @@ NOVA_DEV void epilogue32_staged(const GemmArgs& g, int m_base, int n0, float* v,
     const int r = it * RPI + rsub;
     const float4 x = st4[r * 8 + ((q ^ (r & 7)) & 7)];
     const int m = m_base + r;
+    if constexpr (EPI == EPI_F32_RESID) {
+      if (g.f.nxout != nullptr) {  // next RMSNorm's x~ = bf16(h * gamma) + this 32-column chunk's sum of h^2
+        float4 o = x;
+        o.x += res[it].x;
+        o.y += res[it].y;
+        o.z += res[it].z;
+        o.w += res[it].w;
+        float ss = (o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+        if (m < g.M) {
+          const uint2 gg = *reinterpret_cast<const uint2*>(g.f.ngamma + n0 + 4 * q);
+          const float2 g01 = unpack_bf16(gg.x), g23 = unpack_bf16(gg.y);
+          *reinterpret_cast<uint2*>(g.f.nxout + (size_t)m * g.f.ldnx + n0 + 4 * q) =
+              make_uint2(pack_bf16(o.x * g01.x, o.y * g01.y), pack_bf16(o.z * g23.x, o.w * g23.y));
+          if (q == 0) g.f.nss[(size_t)m * g.f.nss_ld + n0 / 32] = ss;
+        }
+      }
+    }
     if (m < g.M) {
       if constexpr (EPI == EPI_F32_RESID || EPI == EPI_F32_STORE) {
         float4* c4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.C) + (size_t)m * g.ldc + n0) + q;
@@ -302,15 +329,16 @@ __global__ void __launch_bounds__(384, 1)
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int mb = t % num_m, nb = t / num_m;
+      const int m = mb * BM + row;
+      const float rs = (g.f.rscale != nullptr && m < g.M) ? __ldcg(g.f.rscale + m) : 1.f;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const int m = mb * BM + row;
 #pragma unroll 1
       for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, v);
         epilogue32_staged<EPI>(g, m - lane, nb * BN + c * 32, v,
-                               reinterpret_cast<float*>(smem + Cfg::STG_OFF) + (warp - 4) * 1024, lane);
+                               reinterpret_cast<float*>(smem + Cfg::STG_OFF) + (warp - 4) * 1024, lane, rs);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -506,9 +534,10 @@ __global__ void __launch_bounds__(384, 1)
     uint32_t aphase = 0;
     for (int t = pair; t < tiles; t += npairs) {
       const int mb = t % num_m, nb = t / num_m;
+      const int m = mb * 2 * BM + (int)rank * BM + row;
+      const float rs = (g.f.rscale != nullptr && m < g.M) ? __ldcg(g.f.rscale + m) : 1.f;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const int m = mb * 2 * BM + (int)rank * BM + row;
 #pragma unroll 1
       for (int c = half; c < NCH; c += 2) {
         const int n0 = nb * BN + c * 32;
@@ -516,7 +545,7 @@ __global__ void __launch_bounds__(384, 1)
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256 + c * 32, v);
         epilogue32_staged<EPI>(g, m - lane, n0, v, reinterpret_cast<float*>(smem + Cfg::STG_OFF) + (warp - 4) * 1024,
-                               lane);
+                               lane, rs);
       }
       tc_fence_before();
       __syncwarp();
@@ -709,10 +738,16 @@ int gemm_tc_config(int M, int N, int K) {
 }
 
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M, int N,
-                    int K, int epi, int max_ctas, cudaStream_t s) {
+                    int K, int epi, int max_ctas, cudaStream_t s, const GemmFold* fold) {
   if (M <= 0) return cudaSuccess;
   if (N % 64 != 0 || K <= 0 || (lda % 8) || (ldw % 8) || (ldc % 8)) return cudaErrorInvalidValue;
-  GemmArgs g{C, bias, M, N, K, ldc};
+  GemmArgs g{C, bias, M, N, K, ldc, GemmFold{}};
+  if (fold) {
+    if (fold->nxout && (epi != EPI_F32_RESID || !fold->ngamma || !fold->nss || N % 32 || fold->ldnx % 4))
+      return cudaErrorInvalidValue;
+    if (fold->rscale && epi != EPI_BF16 && epi != EPI_BF16_SILUMUL) return cudaErrorInvalidValue;
+    g.f = *fold;
+  }
   const int ci = gemm_tc_config_index(M, N, K);
   if (ci < 0) return cudaErrorInvalidValue;
   const TileCfg& c = kTileCfgs[ci];

@@ -154,6 +154,7 @@ struct UArgs {
   const int* bt;
   int H, KV, layer, n_pages, max_pages;
   float log2_theta;
+  int ef;  // weights with the L2 evict-first policy (env NOVA_UMMA_EF, default 1)
 #ifdef NOVA_UMMA_TRACE
   int trace = 0;
 #endif
@@ -247,11 +248,17 @@ __global__ void __launch_bounds__(NTHR, UCfg<XHL, RING, EPI == EPI_QKV_ROPE_KV>:
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- producer: the k-steps of the range's items, in processing order
+      const uint64_t pol = l2_evict_first();
       auto load_w = [&](int st, int blk, int kb) {
         uint8_t* dst = smem + st * C::STAGE;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          bulk_load(dst + h * 8192, a.wblk + ((size_t)(2 * blk + h) * kblocks + kb) * (64 * KC), 8192, &full[st]);
+        for (int h = 0; h < 2; ++h) {
+          const bf16* src = a.wblk + ((size_t)(2 * blk + h) * kblocks + kb) * (64 * KC);
+          if (a.ef)
+            bulk_load_hint(dst + h * 8192, src, 8192, &full[st], pol);
+          else
+            bulk_load(dst + h * 8192, src, 8192, &full[st]);
+        }
       };
       auto load_x = [&](int st, int kb) {
         uint8_t* dst = smem + st * C::STAGE + W_BYTES;
@@ -683,6 +690,8 @@ cudaError_t gemv_umma(const bf16* X, int ldx, const bf16* W_blocked, int N, int 
     return cudaErrorInvalidValue;
   UArgs a{Y, W_blocked, bias, ws, tickets, N, K, B, ldy, pl.ks / KC, pl.P, N / RB, pl.units, 0, keys, norm_hid, norm_eps,
           ngamma, nxout, ldnx};
+  static const int ef = getenv("NOVA_UMMA_EF") ? atoi(getenv("NOVA_UMMA_EF")) : 1;
+  a.ef = ef;
   if (qa) {
     a.rows = qa->rows, a.pool = qa->pool, a.bt = qa->bt, a.H = qa->H, a.KV = qa->KV, a.layer = qa->layer;
     a.n_pages = qa->n_pages, a.max_pages = qa->max_pages, a.log2_theta = qa->log2_theta;

@@ -53,8 +53,26 @@ enum Epi {
 
 // tcgen05/TMEM/TMA persistent GEMM. A [M][K] (lda), W [N][K] (ldw), C [M][N] (ldc elems).
 // grid = min(tiles, max_ctas): max_ctas is the SM budget of the partition.
+// RMSNorm folded into the prefill GEMMs (DESIGN R25, the decode fold's GEMM form):
+//  * EPI_F32_RESID with nxout: besides C[m][n] += acc, write x~[m][n] = bf16(C_new[m][n] * ngamma[n]) and, per
+//    32-column chunk t = n / 32, nss[m * nss_ld + t] = sum of C_new[m][n]^2 over the chunk (fixed order);
+//  * EPI_BF16 / EPI_BF16_SILUMUL with rscale: A is x~ and every accumulator of row m is multiplied by
+//    rscale[m] (fold_rows: rsqrt(sum of the row's chunk sums / d + eps)) before the bias.
+struct GemmFold {
+  const bf16* ngamma = nullptr;
+  bf16* nxout = nullptr;
+  int ldnx = 0;
+  float* nss = nullptr;
+  int nss_ld = 0;
+  const float* rscale = nullptr;
+};
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M,
-                    int N, int K, int epi, int max_ctas, cudaStream_t s);
+                    int N, int K, int epi, int max_ctas, cudaStream_t s, const GemmFold* fold = nullptr);
+// x~ = bf16(x * g) and the 32-column partial sums of squares ss[r][t] (the first folded RMSNorm's inputs)
+cudaError_t rms_prep(const float* x, int ldx, const bf16* g, bf16* y, int ldy, float* ss, int ss_ld, int M, int d,
+                     cudaStream_t s);
+// rscale[m] = rsqrt((ss[m][0] + ... + ss[m][d / 32 - 1], in chunk order) / d + eps)
+cudaError_t fold_rows(const float* ss, int ss_ld, int d, float eps, float* rscale, int M, cudaStream_t s);
 
 // Tile-configuration override (0 auto, 1 single-CTA tiles only, 2 CTA-pair tiles only); returns
 // the previous mode.  Test / benchmark hook: a forced mode still picks its tile by shape only.

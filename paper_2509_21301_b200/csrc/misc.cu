@@ -244,10 +244,15 @@ __global__ void __launch_bounds__(256) vit_rope_kernel(bf16* __restrict__ qkv, i
 }
 
 // LLM M-RoPE (sections sec0 | sec1 | rest over the hd/2 frequencies) + paged KV write.
-__global__ void llm_rope_kv_kernel(bf16* __restrict__ qkv, int ld, int H, int KV, int hd, float log2_theta, int sec0,
-                                   int sec1, const int* __restrict__ pos3, int ld_pos,
-                                   const DecodeRow* __restrict__ rows, int slot, int ctx0, bf16* __restrict__ pool,
-                                   int layer, int n_pages, const int* __restrict__ bt, int max_pages) {
+// One CTA per row; a thread owns 8 consecutive frequencies i0..i0+7 of one q / k head (16-byte loads of
+// both halves) and writes a rotated k head straight into its page as well; v heads are 16-byte copies.
+// Same per-element arithmetic as the one-element-per-thread version (bitwise the same results).
+__global__ void __launch_bounds__(256) llm_rope_kv_kernel(bf16* __restrict__ qkv, int ld, int H, int KV, int hd,
+                                                          float log2_theta, int sec0, int sec1,
+                                                          const int* __restrict__ pos3, int ld_pos,
+                                                          const DecodeRow* __restrict__ rows, int slot, int ctx0,
+                                                          bf16* __restrict__ pool, int layer, int n_pages,
+                                                          const int* __restrict__ bt, int max_pages) {
   pdl_launch_dependents();
   pdl_wait();
   const int r = blockIdx.x;
@@ -264,29 +269,47 @@ __global__ void llm_rope_kv_kernel(bf16* __restrict__ qkv, int ld, int H, int KV
     cidx = ctx0 + r;
     sl = slot;
   }
-  const int half = hd / 2;
+  const int half = hd / 2, g8 = half / 8;
   bf16* row = qkv + (size_t)r * ld;
-  for (int idx = threadIdx.x; idx < (H + KV) * half; idx += blockDim.x) {
-    const int hh = idx / half, i = idx % half;
-    const int comp = i < sec0 ? 0 : (i < sec0 + sec1 ? 1 : 2);
-    const float inv = exp2f(-(2.0f * i / hd) * log2_theta);
-    const float ang = (float)p[comp] * inv;
-    float sn, cs;
-    sincosf(ang, &sn, &cs);
-    bf16* v = row + (size_t)hh * hd;
-    const float x1 = __bfloat162float(v[i]), x2 = __bfloat162float(v[i + half]);
-    v[i] = __float2bfloat16_rn(x1 * cs - x2 * sn);
-    v[i + half] = __float2bfloat16_rn(x2 * cs + x1 * sn);
-  }
-  __syncthreads();
-  // K (rotated) and V into page bt[slot][cidx / 64], offset cidx % 64
   const size_t page_stride = (size_t)2 * KV * 64 * hd;
   bf16* pg = pool + ((size_t)layer * n_pages + bt[(size_t)sl * max_pages + (cidx >> 6)]) * page_stride;
   const int off = cidx & 63;
-  for (int idx = threadIdx.x; idx < 2 * KV * hd; idx += blockDim.x) {
-    const int kv = idx / (KV * hd), rem = idx % (KV * hd);
-    const int hh = rem / hd, d = rem % hd;
-    pg[(((size_t)kv * KV + hh) * 64 + off) * hd + d] = row[(size_t)(H + kv * KV + hh) * hd + d];
+  const int nrot = (H + KV) * g8, nv = KV * hd / 8;
+  for (int u = threadIdx.x; u < nrot + nv; u += blockDim.x) {
+    if (u < nrot) {
+      const int hh = u / g8, i0 = (u % g8) * 8;
+      bf16* v = row + (size_t)hh * hd;
+      const uint4 a = *reinterpret_cast<const uint4*>(v + i0);
+      const uint4 b = *reinterpret_cast<const uint4*>(v + i0 + half);
+      const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+      uint32_t oa[4], ob[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 x1 = unpack_bf16(aw[q]), x2 = unpack_bf16(bw[q]);
+        float c[2], sn[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = i0 + 2 * q + e;
+          const int comp = i < sec0 ? 0 : (i < sec0 + sec1 ? 1 : 2);
+          const float inv = exp2f(-(2.0f * i / hd) * log2_theta);
+          sincosf((float)p[comp] * inv, &sn[e], &c[e]);
+        }
+        oa[q] = pack_bf16(x1.x * c[0] - x2.x * sn[0], x1.y * c[1] - x2.y * sn[1]);
+        ob[q] = pack_bf16(x2.x * c[0] + x1.x * sn[0], x2.y * c[1] + x1.y * sn[1]);
+      }
+      const uint4 A = make_uint4(oa[0], oa[1], oa[2], oa[3]), Bv = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+      *reinterpret_cast<uint4*>(v + i0) = A;
+      *reinterpret_cast<uint4*>(v + i0 + half) = Bv;
+      if (hh >= H) {  // rotated K head -> its page (K half of the page)
+        bf16* dst = pg + ((size_t)(hh - H) * 64 + off) * hd;
+        *reinterpret_cast<uint4*>(dst + i0) = A;
+        *reinterpret_cast<uint4*>(dst + i0 + half) = Bv;
+      }
+    } else {  // V head chunk -> its page (V half)
+      const int w = u - nrot, hh = w / (hd / 8), d0 = (w % (hd / 8)) * 8;
+      *reinterpret_cast<uint4*>(pg + (((size_t)KV + hh) * 64 + off) * hd + d0) =
+          *reinterpret_cast<const uint4*>(row + (size_t)(H + KV + hh) * hd + d0);
+    }
   }
 }
 
@@ -431,6 +454,60 @@ cudaError_t scale_rows_bf16(const float* x, int ldx, const bf16* g, bf16* y, int
   const int blocks = std::min(64, (M * d + 255) / 256);
   return launch_k(scale_rows_bf16_kernel, dim3(blocks), dim3(256), 0, s, true, x, ldx, g, y, ldy, M, d);
 }
+// one thread per (row, 32-column chunk): x~ = bf16(x * g), ss = sum of x^2 over the chunk in column order
+__global__ void rms_prep_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ g, bf16* __restrict__ y,
+                                int ldy, float* __restrict__ ss, int ss_ld, int M, int d) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int nt = d / 32;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M * nt) return;
+  const int r = i / nt, t = i % nt;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * ldx + t * 32);
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 v = xr[q];
+    s = (((s + v.x * v.x) + v.y * v.y) + v.z * v.z) + v.w * v.w;
+    const uint2 gg = *reinterpret_cast<const uint2*>(g + t * 32 + 4 * q);
+    const float2 g01 = unpack_bf16(gg.x), g23 = unpack_bf16(gg.y);
+    *reinterpret_cast<uint2*>(y + (size_t)r * ldy + t * 32 + 4 * q) =
+        make_uint2(pack_bf16(v.x * g01.x, v.y * g01.y), pack_bf16(v.z * g23.x, v.w * g23.y));
+  }
+  ss[(size_t)r * ss_ld + t] = s;
+}
+// one thread per row: the folded RMSNorm's row scale from the 32-column sums of squares
+__global__ void fold_rows_kernel(const float* __restrict__ ss, int ss_ld, int d, float eps, float* __restrict__ rscale,
+                                 int M) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const float4* p = reinterpret_cast<const float4*>(ss + (size_t)m * ss_ld);
+  const int n4 = d / 128;
+  float s = 0.f;
+  for (int t = 0; t < n4; t += 8) {
+    float4 q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = t + u < n4 ? p[t + u] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t + u < n4) s = (((s + q[u].x) + q[u].y) + q[u].z) + q[u].w;
+  }
+  rscale[m] = rsqrtf(s / (float)d + eps);
+}
+cudaError_t fold_rows(const float* ss, int ss_ld, int d, float eps, float* rscale, int M, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 128 || ss_ld % 4) return cudaErrorInvalidValue;
+  return launch_k(fold_rows_kernel, dim3((M + 127) / 128), dim3(128), 0, s, true, ss, ss_ld, d, eps, rscale, M);
+}
+cudaError_t rms_prep(const float* x, int ldx, const bf16* g, bf16* y, int ldy, float* ss, int ss_ld, int M, int d,
+                     cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 32 || ldx % 4 || ldy % 4) return cudaErrorInvalidValue;
+  const int n = M * (d / 32);
+  return launch_k(rms_prep_kernel, dim3((n + 127) / 128), dim3(128), 0, s, true, x, ldx, g, y, ldy, ss, ss_ld, M, d);
+}
 cudaError_t rmsnorm(const float* x, int ldx, const bf16* g, void* y, int y_f32, int ldy, int M, int d, float eps,
                     cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
@@ -454,7 +531,10 @@ cudaError_t llm_rope_kv(bf16* qkv, int ld, int nrows, int H, int KV, int hd, flo
                         const int* pos3, int ld_pos, const DecodeRow* rows, int slot, int ctx0, bf16* pool, int layer,
                         int n_pages, const int* bt, int max_pages, cudaStream_t s) {
   if (nrows <= 0) return cudaSuccess;
-  return launch_k(llm_rope_kv_kernel, dim3(nrows), dim3(256), 0, s, true, qkv, ld, H, KV, hd, log2f(theta), sec0,
+  if (hd % 16 || ld % 8) return cudaErrorInvalidValue;
+  const int work = (H + KV) * hd / 16 + KV * hd / 8;
+  const int thr = std::min(256, (work + 31) / 32 * 32);
+  return launch_k(llm_rope_kv_kernel, dim3(nrows), dim3(thr), 0, s, true, qkv, ld, H, KV, hd, log2f(theta), sec0,
                   sec1, pos3, ld_pos, rows, slot, ctx0, pool, layer, n_pages, bt, max_pages);
 }
 cudaError_t embed(const bf16* table, int d, const int* ids, const DecodeRow* rows, const int* last_tok, float* out,

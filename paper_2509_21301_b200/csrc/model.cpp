@@ -135,6 +135,8 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   f.attn = (bf16*)take(std::max(N * m.vit_dim, S * Hhd) * 2);
   f.act = (bf16*)take(std::max(std::max(N * m.vit_mlp, (N / 4) * d.merge_dim), S * F) * 2);
   f.hid = (float*)take(S * D * 4);
+  f.nss = (float*)take(S * ((D + 31) / 32) * 4);
+  f.rscale = (float*)take(S * 4);
   f.xf = (float*)take(D * 4);
   f.logits = (float*)take(V * 4);
   f.pos3 = (int*)take(3 * S * 4);
@@ -151,7 +153,9 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   const size_t nparts = std::max(nch, (size_t)(max_ctx + 127) / 128 * 4);  // >= 128-key chunks of the fused kernel  // decode attention partials per head
   // >= the fused decode's chunk partials: B x KV x ceil((max_ctx + 1) / 128) x (32 + (H / KV) hd)
   const size_t fused_parts = B * m.llm_kv_heads * ((max_ctx + 1 + 127) / 128) * (32 + (size_t)(m.llm_heads / m.llm_kv_heads) * m.head_dim);
-  w.attn_ws = (float*)take(std::max(B * m.llm_heads * nparts * (m.head_dim + 2), fused_parts) * 4);
+  // >= the virtual-CTA decode attention's warp states: B x H x (8 virtual CTAs x 6 warps) x (hd + 2)
+  const size_t vstates = B * m.llm_heads * 48 * (size_t)(m.head_dim + 2);
+  w.attn_ws = (float*)take(std::max(std::max(B * m.llm_heads * nparts * (m.head_dim + 2), fused_parts), vstates) * 4);
   // split partials: mma.sync GEMVs 16 x B x N, gemv_umma P x B x N with N * P <= 2^20 (gemv_umma_plan)
   w.gemv_ws = (float*)take(std::max((size_t)16 * std::max(std::max(D, F), (size_t)d.llm_qkv_n), (size_t)1 << 20) * B * 4);
   w.tickets = (int*)take(8192 * 4);

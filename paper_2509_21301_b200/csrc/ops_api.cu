@@ -15,6 +15,26 @@ int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ld
   return st(gemm_tc((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, (const bf16*)bias, M, N, K, epi, max_ctas,
                     S(stream)));
 }
+int nova_op_gemm_fold(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
+                      int K, int epi, int max_ctas, const void* ngamma, void* nxout, int ldnx, float* nss, int nss_ld,
+                      const float* rscale, void* stream) {
+  GemmFold f;
+  f.ngamma = (const bf16*)ngamma;
+  f.nxout = (bf16*)nxout;
+  f.ldnx = ldnx;
+  f.nss = nss;
+  f.nss_ld = nss_ld;
+  f.rscale = rscale;
+  return st(gemm_tc((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, (const bf16*)bias, M, N, K, epi, max_ctas,
+                    S(stream), &f));
+}
+int nova_op_rms_prep(const float* x, int ldx, const void* gamma, void* y, int ldy, float* ss, int ss_ld, int M, int d,
+                     void* stream) {
+  return st(rms_prep(x, ldx, (const bf16*)gamma, (bf16*)y, ldy, ss, ss_ld, M, d, S(stream)));
+}
+int nova_op_fold_rows(const float* ss, int ss_ld, int d, float eps, float* rscale, int M, void* stream) {
+  return st(fold_rows(ss, ss_ld, d, eps, rscale, M, S(stream)));
+}
 int nova_op_gemm_mode(int mode) { return gemm_tc_set_mode(mode); }
 int nova_op_gemm_config(int M, int N, int K) { return gemm_tc_config(M, N, K); }
 int nova_op_gemv(const void* X, int x_f32, int ldx, const void* W, int N, int K, void* Y, int ldy, const void* bias,

@@ -57,11 +57,12 @@ void KTimer::harvest(KStat* out, std::mutex& mu) {
 }
 
 static cudaError_t t_gemm(Engine* E, int role, int cls, const bf16* A, int lda, const bf16* W, int ldw, void* C,
-                          int ldc, const bf16* bias, int M, int N, int K, int epi, int sms, cudaStream_t s) {
+                          int ldc, const bf16* bias, int M, int N, int K, int epi, int sms, cudaStream_t s,
+                          const GemmFold* fold = nullptr) {
   const double w = 2.0 * M * N * K;
   E->pass_work[role] += w;
   const int i = E->ktimer[role].begin(s);
-  CUDA_TRY(gemm_tc(A, lda, W, ldw, C, ldc, bias, M, N, K, epi, sms, s));
+  CUDA_TRY(gemm_tc(A, lda, W, ldw, C, ldc, bias, M, N, K, epi, sms, s, fold));
   E->ktimer[role].end(i, cls, w, s);
   return cudaSuccess;
 }
@@ -215,11 +216,25 @@ cudaError_t Engine::run_prefill(Request* r, cudaStream_t& s, int sms, FrontRG* r
   CUDA_TRY(embed(W.embed, D, d_prompt + (size_t)r->slot * cfg.max_prompt, nullptr, nullptr, fw.hid + (size_t)nv * D,
                  D, r->n_prompt, s));
   bf16* pool = reinterpret_cast<bf16*>(buf.kv_dev);
+  // RMSNorm folded into the GEMMs (R25, the decode fold's GEMM form; experimental, env NOVA_PREFILL_FOLD=1):
+  // the residual GEMMs write the next norm's x~ = bf16(h * gamma) and 32-column sums of h^2, fold_rows turns
+  // them into row scales, qkv / gate|up scale their rows after the GEMM.  Measured 1-4% slower than the
+  // rmsnorm kernel it replaces (2B 4.71 vs 4.64 ms, 7B 16.4-16.7 vs 15.8-16.6 ms), so off.
+  static const int g_pfold = getenv("NOVA_PREFILL_FOLD") ? atoi(getenv("NOVA_PREFILL_FOLD")) : 0;
+  const bool pfold = g_pfold && g_fold_norm && D % 128 == 0;
+  GemmFold fin, fout;
+  fin.rscale = fw.rscale;
+  fout.nxout = fw.xb, fout.ldnx = D, fout.nss = fw.nss, fout.nss_ld = D / 32;
+  if (pfold) {
+    CUDA_TRY(rms_prep(fw.hid, D, W.llm[0].ln1, fw.xb, D, fw.nss, D / 32, S, D, s));
+    CUDA_TRY(fold_rows(fw.nss, D / 32, D, m.rms_eps, fw.rscale, S, s));
+  }
   for (int l = 0; l < m.llm_layers; ++l) {
     if (rg && l > 0 && l % rg->group == 0) CUDA_TRY(front_regroup(rg, s, sms));
     const LlmLayerW& L = W.llm[l];
-    CUDA_TRY(rmsnorm(fw.hid, D, L.ln1, fw.xb, 0, D, S, D, m.rms_eps, s));
-    CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.xb, D, L.qkv_w, D, fw.qkv, ldq, L.qkv_b, S, ldq, D, EPI_BF16, sms, s));
+    if (!pfold) CUDA_TRY(rmsnorm(fw.hid, D, L.ln1, fw.xb, 0, D, S, D, m.rms_eps, s));
+    CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.xb, D, L.qkv_w, D, fw.qkv, ldq, L.qkv_b, S, ldq, D, EPI_BF16, sms, s,
+                    pfold ? &fin : nullptr));
     CUDA_TRY(llm_rope_kv(fw.qkv, ldq, S, H, KV, hd, m.llm_theta, m.mrope_section[0], m.mrope_section[1], fw.pos3, S,
                          nullptr, r->slot, 0, pool, l, cfg.kv_pages, d_bt, max_pages_per_req, s));
     {
@@ -229,13 +244,19 @@ cudaError_t Engine::run_prefill(Request* r, cudaStream_t& s, int sms, FrontRG* r
       CUDA_TRY(flash_attn(fw.qkv, ldq, fw.attn, H * hd, S, H, KV, hd, 1, sms, s));
       ktimer[0].end(i, NOVA_K_PRE_ATTN, w, s);
     }
+    fout.ngamma = L.ln2;
     CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.attn, H * hd, L.o_w, H * hd, fw.hid, D, nullptr, S, D, H * hd,
-                    EPI_F32_RESID, sms, s));
-    CUDA_TRY(rmsnorm(fw.hid, D, L.ln2, fw.xb, 0, D, S, D, m.rms_eps, s));
+                    EPI_F32_RESID, sms, s, pfold ? &fout : nullptr));
+    if (pfold)
+      CUDA_TRY(fold_rows(fw.nss, D / 32, D, m.rms_eps, fw.rscale, S, s));
+    else
+      CUDA_TRY(rmsnorm(fw.hid, D, L.ln2, fw.xb, 0, D, S, D, m.rms_eps, s));
     CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.xb, D, L.gu_w, D, fw.act, F, nullptr, S, 2 * F, D, EPI_BF16_SILUMUL,
-                    sms, s));
+                    sms, s, pfold ? &fin : nullptr));
+    fout.ngamma = l + 1 < m.llm_layers ? W.llm[l + 1].ln1 : nullptr;  // the last layer's feeds only the final norm
     CUDA_TRY(t_gemm(this, 0, NOVA_K_LLM_GEMM, fw.act, F, L.down_w, F, fw.hid, D, nullptr, S, D, F, EPI_F32_RESID, sms,
-                    s));
+                    s, (pfold && fout.ngamma) ? &fout : nullptr));
+    if (pfold && fout.ngamma) CUDA_TRY(fold_rows(fw.nss, D / 32, D, m.rms_eps, fw.rscale, S, s));
   }
   // token 0: final RMSNorm of the last row (applied on load, f32) -> lm_head -> fused greedy argmax
   pass_work[0] += 2.0 * D * m.vocab;

@@ -27,6 +27,25 @@ def nova_op_gemm(A, W, C, bias, M, N, K, epi, max_ctas=148, lda=None, ldw=None, 
                              _p(bias), M, N, K, epi, max_ctas, _s(stream)), "gemm")
 
 
+def nova_op_gemm_fold(A, W, C, bias, M, N, K, epi, ngamma=None, nxout=None, nss=None, rscale=None, max_ctas=148,
+                      stream=None):
+    """nova_op_gemm with the RMSNorm fold (include/nova_ops.h): nxout / nss outputs of a NOVA_EPI_F32_RESID
+    GEMM, or the rscale [M] row scales (nova_op_fold_rows) of a NOVA_EPI_BF16(_SILUMUL) GEMM."""
+    check(lib().nova_op_gemm_fold(_p(A), A.stride(0), _p(W), W.stride(0), _p(C), C.stride(0), _p(bias), M, N, K, epi,
+                                  max_ctas, _p(ngamma), _p(nxout), nxout.stride(0) if nxout is not None else 0,
+                                  _p(nss), nss.stride(0) if nss is not None else 0, _p(rscale), _s(stream)), "gemm_fold")
+
+
+def nova_op_fold_rows(ss, d, eps, rscale, M, stream=None):
+    import ctypes as Ct
+    check(lib().nova_op_fold_rows(_p(ss), ss.stride(0), d, Ct.c_float(eps), _p(rscale), M, _s(stream)), "fold_rows")
+
+
+def nova_op_rms_prep(x, gamma, y, ss, M, d, stream=None):
+    check(lib().nova_op_rms_prep(_p(x), x.stride(0), _p(gamma), _p(y), y.stride(0), _p(ss), ss.stride(0), M, d,
+                                 _s(stream)), "rms_prep")
+
+
 def nova_op_gemm_mode(mode: int) -> int:
     """0 = automatic tile choice, 1 = single-CTA tiles only, 2 = CTA-pair tiles only; returns the previous mode."""
     return lib().nova_op_gemm_mode(mode)

@@ -1,0 +1,6 @@
+#!/bin/bash
+# virtual-CTA decode attention gated to > 3 waves: kernel tests + decode splits
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -k "decode" 2>&1 | tail -1
+timeout 300 python scripts/dec_splits.py --model 2b --B 2 8 16 --splits 0 16 24 32 48 72 2>&1 | grep '^{'
+timeout 300 python scripts/dec_splits.py --model 7b --B 2 8 16 --splits 0 16 24 48 72 2>&1 | grep '^{'

@@ -111,7 +111,8 @@ def bench_gemm(iters):
 
 def bench_attn(iters):
     for name, S, H, KV, hd, causal in [("vit_4888", 4888, 16, 16, 80, 0), ("vit_7920", 7920, 16, 16, 80, 0),
-                                        ("pre_1286", 1286, 28, 4, 128, 1), ("pre_2044", 2044, 28, 4, 128, 1)]:
+                                        ("pre_1286", 1286, 28, 4, 128, 1), ("pre_2044", 2044, 28, 4, 128, 1),
+                                        ("pre2b_1286", 1286, 12, 2, 128, 1)]:
         qkv = rnd((S, (H + 2 * KV) * hd))
         out = torch.empty(S, H * hd, device="cuda", dtype=torch.bfloat16)
         fl = (2.0 if causal else 4.0) * S * S * hd * H

@@ -274,8 +274,9 @@ def test_llm_rope_kv_and_decode_attention():
 
 @pytest.mark.parametrize("H,KV", [(28, 4), (12, 2)])
 def test_decode_attention_long_context_7b_shape(H, KV):
-    """7B / 2B head shapes vs the oracle; bitwise equal on the whole GPU (2-stage ring) and on an 8-SM
-    budget (1-stage ring, two CTAs per SM)."""
+    """7B / 2B head shapes vs the oracle; bitwise equal on the whole GPU (cluster kernel, 2-stage ring) and
+    on 8- / 24- / 40-SM budgets (1-stage ring, two CTAs per SM; the virtual-CTA kernel with fewer physical
+    CTAs per (request, KV head) and the workspace merge)."""
     rng = np.random.default_rng(12)
     hd, n_pages = 128, 128
     ctxs = [1333, 17, 640, 2047]
@@ -289,10 +290,12 @@ def test_decode_attention_long_context_7b_shape(H, KV):
     out = torch.empty(B, H * hd, dtype=torch.bfloat16, device="cuda")
     ws = torch.empty(B * H * 80 * (hd + 2), dtype=torch.float32, device="cuda")
     O.nova_op_decode_attn(bf16_dev(qd), out, pool, 0, n_pages, H, KV, hd, bt, rows, B, max(ctxs), ws)
-    out8 = torch.empty_like(out)
-    O.nova_op_decode_attn(bf16_dev(qd), out8, pool, 0, n_pages, H, KV, hd, bt, rows, B, max(ctxs), ws, max_ctas=8)
-    torch.cuda.synchronize()
-    assert torch.equal(out.view(torch.int16), out8.view(torch.int16))
+    for ctas in (4, 8, 24, 40):   # virtual-CTA kernel (1 / 2 physical CTAs per (request, KV head)); 1-stage ring
+        out8 = torch.empty_like(out)
+        O.nova_op_decode_attn(bf16_dev(qd), out8, pool, 0, n_pages, H, KV, hd, bt, rows, B, max(ctxs), ws,
+                              max_ctas=ctas)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), out8.view(torch.int16)), ctas
     btn = bt.cpu().numpy()
     for b, ctx in enumerate(ctxs):
         kc = np.stack([pool_np[0, btn[b, t // 64], 0, :, t % 64] for t in range(ctx + 1)]).astype(np.float64)
@@ -376,13 +379,14 @@ def test_flash_attn_vit_shape_grid_invariant():
         assert rel_inf(got[:, h:h + 1], ref) <= 2e-2, h
 
 
-@pytest.mark.parametrize("S", [1286, 2044, 257])
-def test_flash_attn_prefill_causal_grid_invariant(S):
-    """7B prefill shape (28 query / 4 KV heads, hd 128, causal): the persistent tcgen05 kernel
-    runs the Q-tile pairs longest first in a snake order over the CTAs; output must not depend
-    on the SM budget and matches the oracle on the first and last head of two KV groups."""
-    rng = np.random.default_rng(S)
-    H, KV, hd = 28, 4, 128
+@pytest.mark.parametrize("S,H,KV", [(1286, 28, 4), (2044, 28, 4), (257, 28, 4), (1286, 12, 2), (700, 12, 2)])
+def test_flash_attn_prefill_causal_grid_invariant(S, H, KV):
+    """7B / 2B prefill shapes (hd 128, causal): the persistent tcgen05 kernel runs the Q-tile pairs
+    longest first in a snake order over the CTAs, the longest cut into key chunks merged in chunk
+    order (shape-only plan); output must not depend on the SM budget and matches the oracle on the
+    first and last head of two KV groups."""
+    rng = np.random.default_rng(S + H)
+    hd = 128
     qkv = rand_bf16(rng, (S, (H + 2 * KV) * hd))
     d = bf16_dev(qkv)
     outs = []
@@ -397,7 +401,75 @@ def test_flash_attn_prefill_causal_grid_invariant(S):
     q = qkv[:, :H * hd].reshape(S, H, hd).astype(np.float64)
     k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd).astype(np.float64)
     v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd).astype(np.float64)
-    for h in (0, 6, 7, 27):
+    for h in (0, H // KV - 1, H // KV, H - 1):
         g = h // (H // KV)
         ref = V.attention_causal_gqa(q[:, h:h + 1], k[:, g:g + 1], v[:, g:g + 1], hd ** -0.5, 0)
         assert rel_inf(got[:, h:h + 1], ref) <= 2e-2, h
+
+
+@pytest.mark.parametrize("M,D,F,ctas", [(1286, 1536, 8960, 148), (300, 3584, 18944, 40), (12, 128, 384, 148)])
+def test_prefill_rmsnorm_fold_gemms(M, D, F, ctas):
+    """DESIGN R25 on the prefill GEMMs: (1) rms_prep: x~ = bf16(h * ln1) bitwise, 32-column sums of squares;
+    (2) a residual GEMM (o-proj shape) writing h_new, the next x~ = bf16(h_new * ln2) (bitwise vs the host
+    rounding of the GPU's h_new) and its chunk sums; (3) qkv (bias) and gate|up (SiLU * up) GEMMs on x~ with
+    the row scale folded after the GEMM vs the oracle's rms_norm -> linear (bf16 rel-inf <= 8e-3); and the
+    results bitwise independent of the SM budget."""
+    from synth.weights import bf16_bits_to_f32, f32_to_bf16_bits
+    rng = np.random.default_rng(M + D)
+    eps = 1e-6
+    g1 = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (D,), 0.1) + 1.0))
+    g2 = bf16_bits_to_f32(f32_to_bf16_bits(rand_bf16(rng, (D,), 0.1) + 1.0))
+    h = (rng.standard_normal((M, D)) * 2).astype(np.float32)
+    nt = D // 32
+    dh = torch.from_numpy(h).cuda()
+    xt = torch.empty(M, D, dtype=torch.bfloat16, device="cuda")
+    ss = torch.empty(M, nt, dtype=torch.float32, device="cuda")
+    O.nova_op_rms_prep(dh, bf16_dev(g1), xt, ss, M, D)
+    torch.cuda.synchronize()
+    assert np.array_equal(xt.view(torch.int16).cpu().numpy().view(np.uint16), f32_to_bf16_bits(h * g1))
+    ref_ss = (h.astype(np.float64) ** 2).reshape(M, nt, 32).sum(-1)
+    assert np.abs(ss.cpu().numpy() - ref_ss).max() <= 1e-5 * ref_ss.max()
+    # (2) residual GEMM + next-norm outputs
+    Wo = rand_bf16(rng, (D, D), D ** -0.5)
+    Xa = rand_bf16(rng, (M, D))
+    outs = []
+    for c in (ctas, 24):
+        Y = dh.clone()
+        nx = torch.empty(M, D, dtype=torch.bfloat16, device="cuda")
+        nss = torch.empty(M, nt, dtype=torch.float32, device="cuda")
+        O.nova_op_gemm_fold(bf16_dev(Xa), bf16_dev(Wo), Y, None, M, D, D, O.EPI_F32_RESID, ngamma=bf16_dev(g2),
+                            nxout=nx, nss=nss, max_ctas=c)
+        torch.cuda.synchronize()
+        outs.append((Y, nx, nss))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    Y, nx, nss = outs[0]
+    hn = Y.cpu().numpy()
+    ref = h.astype(np.float64) + V.linear(Xa.astype(np.float64), Wo.astype(np.float64))
+    assert rel_inf(hn, ref) <= 1e-4
+    assert np.array_equal(nx.view(torch.int16).cpu().numpy().view(np.uint16), f32_to_bf16_bits(hn * g2))
+    ref_ss = (hn.astype(np.float64) ** 2).reshape(M, nt, 32).sum(-1)
+    assert np.abs(nss.cpu().numpy() - ref_ss).max() <= 1e-5 * ref_ss.max()
+    # (3) consumers with the folded row scale (fold_rows: rsqrt(sum of the chunk sums / D + eps))
+    rsc = torch.empty(M, dtype=torch.float32, device="cuda")
+    O.nova_op_fold_rows(nss, D, eps, rsc, M)
+    torch.cuda.synchronize()
+    ref_rs = 1.0 / np.sqrt((hn.astype(np.float64) ** 2).mean(-1) + eps)
+    assert np.abs(rsc.cpu().numpy() / ref_rs - 1).max() <= 1e-5
+    xn = V.rms_norm(hn.astype(np.float64), g2, eps)
+    Wq = rand_bf16(rng, (256, D), D ** -0.5)
+    bq = rand_bf16(rng, (256,), 0.05)
+    q = torch.empty(M, 256, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_gemm_fold(nx, bf16_dev(Wq), q, bf16_dev(bq), M, 256, D, O.EPI_BF16, rscale=rsc, max_ctas=ctas)
+    G = rand_bf16(rng, (F, D), D ** -0.5)
+    U = rand_bf16(rng, (F, D), D ** -0.5)
+    Wgu = np.empty((2 * F, D), dtype=np.float32)
+    for i in range(F // 16):
+        Wgu[32 * i:32 * i + 16] = G[16 * i:16 * i + 16]
+        Wgu[32 * i + 16:32 * i + 32] = U[16 * i:16 * i + 16]
+    act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    O.nova_op_gemm_fold(nx, bf16_dev(Wgu), act, None, M, 2 * F, D, O.EPI_BF16_SILUMUL, rscale=rsc, max_ctas=ctas)
+    torch.cuda.synchronize()
+    assert rel_inf(bf16_host(q), V.linear(xn, Wq.astype(np.float64), bq.astype(np.float64))) <= 8e-3
+    ref_act = V.silu(V.linear(xn, G.astype(np.float64))) * V.linear(xn, U.astype(np.float64))
+    assert rel_inf(bf16_host(act), ref_act) <= 8e-3
