@@ -20,7 +20,9 @@ def classify(name, stage):
         if "decode_attn" in name:
             return "dec_attn"
         if "gemv" in name:
-            return "lm_head" if ("7, 1>" in name or "1, 1, 7" in name or "ARGMAX" in name) else "dec_gemv"
+            # lm_head = the EPI_F32_ARGMAX (7) instantiation: gemv_umma_kernel<7, 1, RING>, gemv_tma <..7..>
+            return "lm_head" if ("_kernel<7," in name or "7, 1>" in name or "1, 1, 7" in name or "ARGMAX" in name) \
+                else "dec_gemv"
     if stage == "vit":
         if "gemm_tc" in name:
             return "vit_gemm"
