@@ -53,6 +53,14 @@ int nova_op_gemm(const void* A, int lda, const void* W, int ldw, void* C, int ld
 int nova_op_gemm_fold(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M, int N,
                       int K, int epi, int max_ctas, const void* ngamma, void* nxout, int ldnx, float* nss, int nss_ld,
                       const float* rscale, void* stream);
+/* ViT qkv projection with the 2D RoPE in the GEMM epilogue (SURVEY §8(a) a5 "QKV GEMM (+bias) -> 2D-RoPE(q,k)";
+ * PAPER.md P:468 "kernel fusion ... RoPE"): C = A W^T + bias in bf16, the columns [0, qk_cols) being q | k
+ * heads of hd = 80 rotated by the 2D RoPE of row m's patch -- rows merge-group-major over a grid gw patches
+ * wide (merge x merge groups), as nova_op_vit_rope -- on the f32 accumulators before the one bf16 rounding.
+ * N and qk_cols multiples of 160 (the kernel takes 256 x 160 CTA-pair tiles: two heads per tile); M = gh * gw.
+ * Bitwise independent of max_ctas. */
+int nova_op_gemm_rope2d(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M,
+                        int N, int K, int qk_cols, int gw, int merge, float theta, int max_ctas, void* stream);
 /* rscale[m] = rsqrt((ss[m * ss_ld + 0] + ... + ss[m * ss_ld + d / 32 - 1], in that order) / d + eps) for
  * M rows (d % 128 == 0, ss_ld % 4 == 0): the folded RMSNorm's row scales from the chunk sums. */
 int nova_op_fold_rows(const float* ss, int ss_ld, int d, float eps, float* rscale, int M, void* stream);

@@ -22,6 +22,7 @@ OPS_SIGNATURES = {
     "nova_op_gemm": [P, I, P, I, P, I, P, I, I, I, I, I, P],
     "nova_op_gemm_fold": [P, I, P, I, P, I, P, I, I, I, I, I, P, P, I, P, I, P, P],
     "nova_op_fold_rows": [P, I, I, F, P, I, P],
+    "nova_op_gemm_rope2d": [P, I, P, I, P, I, P, I, I, I, I, I, I, F, I, P],
     "nova_op_rms_prep": [P, I, P, P, I, P, I, I, I, P],
     "nova_op_gemm_mode": [I],
     "nova_op_gemm_config": [I, I, I],

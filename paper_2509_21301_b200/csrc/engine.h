@@ -213,6 +213,7 @@ class Engine {
     float *hid, *vhid, *xf, *logits;
     float* nss;     // prefill RMSNorm fold (R25): [S][D / 32] partial sums of squares
     float* rscale;  // ... and the row scales [S]
+    float2* rope_tab;  // ViT 2D RoPE (cos, sin) table [max grid side][20] for the fused qkv epilogue
     int *pos3, *tok;
     unsigned long long* keys;  // greedy argmax (EPI_F32_ARGMAX), zero between passes
     int* h_pos3;  // pinned

@@ -28,7 +28,55 @@ struct GemmArgs {
   const bf16* bias;
   int M, N, K, ldc;
   GemmFold f;  // RMSNorm fold (DESIGN R25; all null = off)
+  GemmRope r;  // EPI_BF16_ROPE2D
 };
+
+// 32 lanes x 8 consecutive f32 columns of TMEM (no wait: the caller waits once for several loads)
+NOVA_DEV void tmem_ld8_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// ViT qkv epilogue (EPI_BF16_ROPE2D) of one 80-column head at column hc of the tile for row m: pairs
+// (i, i + 40), angle = (i < 20 ? row : col of the patch) * theta^(-4 (i mod 20) / 80) -- vit_rope's
+// arithmetic (cos / sin from the per-pass rope2d_table), applied to the f32 accumulator + bias before
+// the one bf16 rounding.
+NOVA_DEV void rope2d_head80(const GemmArgs& g, uint32_t tbase, int m, int n0) {
+  const GemmRope& R = g.r;
+  const int grp = m / (R.merge * R.merge), in = m % (R.merge * R.merge);
+  const int gi = grp / (R.gw / R.merge), gj = grp % (R.gw / R.merge);
+  const float2* th = R.tab + (size_t)(gi * R.merge + in / R.merge) * 20;  // angles of the patch row
+  const float2* tw = R.tab + (size_t)(gj * R.merge + in % R.merge) * 20;  // ... and column
+  bf16* crow = reinterpret_cast<bf16*>(g.C) + (size_t)m * g.ldc + n0;
+#pragma unroll 1
+  for (int i0 = 0; i0 < 40; i0 += 8) {
+    uint32_t a[8], b[8];
+    tmem_ld8_nw(tbase + i0, a);
+    tmem_ld8_nw(tbase + 40 + i0, b);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float o1[8], o2[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j;
+      float x1 = __uint_as_float(a[j]), x2 = __uint_as_float(b[j]);
+      if (g.bias != nullptr) {
+        x1 += __bfloat162float(g.bias[n0 + i]);
+        x2 += __bfloat162float(g.bias[n0 + 40 + i]);
+      }
+      const float2 t = i < 20 ? th[i] : tw[i - 20];
+      const float cs = t.x, sn = t.y;
+      o1[j] = x1 * cs - x2 * sn;
+      o2[j] = x2 * cs + x1 * sn;
+    }
+    if (m < g.M) {
+      *reinterpret_cast<uint4*>(crow + i0) = make_uint4(pack_bf16(o1[0], o1[1]), pack_bf16(o1[2], o1[3]),
+                                                        pack_bf16(o1[4], o1[5]), pack_bf16(o1[6], o1[7]));
+      *reinterpret_cast<uint4*>(crow + 40 + i0) = make_uint4(pack_bf16(o2[0], o2[1]), pack_bf16(o2[2], o2[3]),
+                                                             pack_bf16(o2[4], o2[5]), pack_bf16(o2[6], o2[7]));
+    }
+  }
+}
 
 template <int BN>
 struct GemmCfg {
@@ -538,6 +586,22 @@ __global__ void __launch_bounds__(384, 1)
       const float rs = (g.f.rscale != nullptr && m < g.M) ? __ldcg(g.f.rscale + m) : 1.f;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
+      if constexpr (EPI == EPI_BF16_ROPE2D) {
+        if (nb * BN < g.r.qk_cols) {  // q / k tile: warp half h takes head h of the tile (BN = 160)
+          rope2d_head80(g, tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256 + half * 80, m,
+                        nb * BN + half * 80);
+        } else {  // v tile: plain bf16 epilogue
+#pragma unroll 1
+          for (int c = half; c < NCH; c += 2) {
+            const int n0 = nb * BN + c * 32;
+            if (n0 >= g.N) break;
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256 + c * 32, v);
+            epilogue32_staged<EPI_BF16>(g, m - lane, n0, v,
+                                        reinterpret_cast<float*>(smem + Cfg::STG_OFF) + (warp - 4) * 1024, lane);
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int c = half; c < NCH; c += 2) {
         const int n0 = nb * BN + c * 32;
@@ -546,6 +610,7 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256 + c * 32, v);
         epilogue32_staged<EPI>(g, m - lane, n0, v, reinterpret_cast<float*>(smem + Cfg::STG_OFF) + (warp - 4) * 1024,
                                lane, rs);
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -738,10 +803,17 @@ int gemm_tc_config(int M, int N, int K) {
 }
 
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M, int N,
-                    int K, int epi, int max_ctas, cudaStream_t s, const GemmFold* fold) {
+                    int K, int epi, int max_ctas, cudaStream_t s, const GemmFold* fold, const GemmRope* rope) {
   if (M <= 0) return cudaSuccess;
   if (N % 64 != 0 || K <= 0 || (lda % 8) || (ldw % 8) || (ldc % 8)) return cudaErrorInvalidValue;
-  GemmArgs g{C, bias, M, N, K, ldc, GemmFold{}};
+  GemmArgs g{C, bias, M, N, K, ldc, GemmFold{}, GemmRope{}};
+  if (epi == EPI_BF16_ROPE2D) {  // two 80-wide heads per 256 x 160 pair tile (shape-only choice)
+    if (!rope || !rope->tab || N % 160 || rope->qk_cols % 160 || rope->qk_cols > N || rope->merge < 1 ||
+        rope->gw % rope->merge || fold)
+      return cudaErrorInvalidValue;
+    g.r = *rope;
+    return launch_pair<160, EPI_BF16_ROPE2D>(A, lda, W, ldw, g, max_ctas, s);
+  }
   if (fold) {
     if (fold->nxout && (epi != EPI_F32_RESID || !fold->ngamma || !fold->nss || N % 32 || fold->ldnx % 4))
       return cudaErrorInvalidValue;

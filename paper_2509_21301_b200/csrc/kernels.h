@@ -49,6 +49,7 @@ enum Epi {
   EPI_F32_STORE = 5,    // out f32 = result
   EPI_QKV_ROPE_KV = 6,  // decode qkv: bias + M-RoPE on q/k; q -> out bf16, k/v -> paged KV cache (GemvAux)
   EPI_F32_ARGMAX = 7,   // logits f32 = result, and greedy argmax into GemvAux::keys (64-bit atomicMax)
+  EPI_BF16_ROPE2D = 8,  // ViT qkv: out bf16 = result + bias, 2D RoPE on the q / k columns (GemmRope; hd 80)
 };
 
 // tcgen05/TMEM/TMA persistent GEMM. A [M][K] (lda), W [N][K] (ldw), C [M][N] (ldc elems).
@@ -66,8 +67,19 @@ struct GemmFold {
   int nss_ld = 0;
   const float* rscale = nullptr;
 };
+// EPI_BF16_ROPE2D (ViT qkv, hd 80): columns [0, qk_cols) are q | k heads of 80, rotated by the 2D RoPE of
+// their row's patch (merge-group-major rows of a grid gw patches wide: as vit_rope) in the epilogue, on
+// the f32 accumulators + bias; the tile is forced to the 256 x 160 CTA pair (two heads per tile).
+struct GemmRope {
+  int qk_cols = 0, gw = 0, merge = 2;
+  float log2_theta = 0.f;
+  const float2* tab = nullptr;  // rope2d_table: (cos, sin)[pos][j] for j < 20, pos < npos (required)
+};
+// (cos, sin) of pos * theta^(-4 j / 80) for pos < npos, j < 20 (the ViT 2D RoPE angles at hd 80)
+cudaError_t rope2d_table(float2* tab, int npos, float log2_theta, cudaStream_t s);
 cudaError_t gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, void* C, int ldc, const bf16* bias, int M,
-                    int N, int K, int epi, int max_ctas, cudaStream_t s, const GemmFold* fold = nullptr);
+                    int N, int K, int epi, int max_ctas, cudaStream_t s, const GemmFold* fold = nullptr,
+                    const GemmRope* rope = nullptr);
 // x~ = bf16(x * g) and the 32-column partial sums of squares ss[r][t] (the first folded RMSNorm's inputs)
 cudaError_t rms_prep(const float* x, int ldx, const bf16* g, bf16* y, int ldy, float* ss, int ss_ld, int M, int d,
                      cudaStream_t s);

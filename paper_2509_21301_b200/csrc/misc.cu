@@ -438,6 +438,21 @@ cudaError_t layernorm(const float* x, int ldx, const bf16* g, const bf16* b, bf1
   if (d % 4) return cudaErrorInvalidValue;
   return launch_k(layernorm_kernel, dim3((M + 7) / 8), dim3(256), 0, s, true, x, ldx, g, b, y, ldy, M, d, eps);
 }
+__global__ void rope2d_table_kernel(float2* __restrict__ tab, int npos, float log2_theta) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npos * 20) return;
+  const int pos = i / 20, j = i % 20;
+  const float inv = exp2f(-(4.0f * j / 80.0f) * log2_theta);
+  float sn, cs;
+  sincosf((float)pos * inv, &sn, &cs);
+  tab[i] = make_float2(cs, sn);
+}
+cudaError_t rope2d_table(float2* tab, int npos, float log2_theta, cudaStream_t s) {
+  if (npos <= 0) return cudaSuccess;
+  return launch_k(rope2d_table_kernel, dim3((npos * 20 + 127) / 128), dim3(128), 0, s, true, tab, npos, log2_theta);
+}
 // x~ = bf16(x * g) rows (DESIGN R25: the input of a GEMV whose RMSNorm row scale is folded after it)
 __global__ void scale_rows_bf16_kernel(const float* __restrict__ x, int ldx, const bf16* __restrict__ g,
                                        bf16* __restrict__ y, int ldy, int M, int d) {

@@ -137,6 +137,7 @@ size_t Engine::plan_workspace(const Dims& d, const nova_engine_config& c, Engine
   f.hid = (float*)take(S * D * 4);
   f.nss = (float*)take(S * ((D + 31) / 32) * 4);
   f.rscale = (float*)take(S * 4);
+  f.rope_tab = (float2*)take((size_t)std::max<size_t>(N, 64) * 20 * 8);  // a grid side is at most N patches
   f.xf = (float*)take(D * 4);
   f.logits = (float*)take(V * 4);
   f.pos3 = (int*)take(3 * S * 4);

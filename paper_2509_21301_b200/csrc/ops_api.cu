@@ -32,6 +32,31 @@ int nova_op_rms_prep(const float* x, int ldx, const void* gamma, void* y, int ld
                      void* stream) {
   return st(rms_prep(x, ldx, (const bf16*)gamma, (bf16*)y, ldy, ss, ss_ld, M, d, S(stream)));
 }
+int nova_op_gemm_rope2d(const void* A, int lda, const void* W, int ldw, void* C, int ldc, const void* bias, int M,
+                        int N, int K, int qk_cols, int gw, int merge, float theta, int max_ctas, void* stream) {
+  GemmRope r;
+  r.qk_cols = qk_cols;
+  r.gw = gw;
+  r.merge = merge;
+  r.log2_theta = log2f(theta);
+  // the per-pass angle table (the engine keeps one in its front workspace; this test-facing op keeps a
+  // process-wide one, grown on demand -- not for concurrent use)
+  static float2* tab = nullptr;
+  static int cap = 0;
+  if (gw <= 0 || M % gw) return st(cudaErrorInvalidValue);
+  const int npos = std::max(gw, M / gw);
+  if (npos > cap) {
+    if (tab) cudaFree(tab);
+    tab = nullptr;
+    if (cudaMalloc(&tab, (size_t)npos * 20 * sizeof(float2)) != cudaSuccess) return st(cudaErrorMemoryAllocation);
+    cap = npos;
+  }
+  cudaError_t e = rope2d_table(tab, npos, r.log2_theta, S(stream));
+  if (e != cudaSuccess) return st(e);
+  r.tab = tab;
+  return st(gemm_tc((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, (const bf16*)bias, M, N, K, EPI_BF16_ROPE2D,
+                    max_ctas, S(stream), nullptr, &r));
+}
 int nova_op_fold_rows(const float* ss, int ss_ld, int d, float eps, float* rscale, int M, void* stream) {
   return st(fold_rows(ss, ss_ld, d, eps, rscale, M, S(stream)));
 }

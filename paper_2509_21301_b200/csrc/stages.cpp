@@ -58,11 +58,11 @@ void KTimer::harvest(KStat* out, std::mutex& mu) {
 
 static cudaError_t t_gemm(Engine* E, int role, int cls, const bf16* A, int lda, const bf16* W, int ldw, void* C,
                           int ldc, const bf16* bias, int M, int N, int K, int epi, int sms, cudaStream_t s,
-                          const GemmFold* fold = nullptr) {
+                          const GemmFold* fold = nullptr, const GemmRope* rope = nullptr) {
   const double w = 2.0 * M * N * K;
   E->pass_work[role] += w;
   const int i = E->ktimer[role].begin(s);
-  CUDA_TRY(gemm_tc(A, lda, W, ldw, C, ldc, bias, M, N, K, epi, sms, s, fold));
+  CUDA_TRY(gemm_tc(A, lda, W, ldw, C, ldc, bias, M, N, K, epi, sms, s, fold, rope));
   E->ktimer[role].end(i, cls, w, s);
   return cudaSuccess;
 }
@@ -144,6 +144,14 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t& s, int sms, FrontRG* rg
   CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.x0, dims.patch_dim, W.patch_w, dims.patch_dim, fw.vhid, Dv, nullptr, N,
                   Dv, dims.patch_dim, EPI_F32_STORE, sms, s));
   const int L = m.vit_depth;
+  // 2D RoPE fused into the qkv GEMM epilogue where a 160-column tile holds whole heads (hd 80, the
+  // Qwen2-VL ViT; env NOVA_VIT_ROPE_FUSED=0 restores the separate vit_rope kernel)
+  static const int g_vrf = getenv("NOVA_VIT_ROPE_FUSED") ? atoi(getenv("NOVA_VIT_ROPE_FUSED")) : 1;
+  const bool rope_fused = g_vrf && hd == 80 && (3 * Dv) % 160 == 0 && (2 * Dv) % 160 == 0 && gw % m.merge == 0;
+  GemmRope vrope;
+  vrope.qk_cols = 2 * Dv, vrope.gw = gw, vrope.merge = m.merge, vrope.log2_theta = log2f(m.vit_theta);
+  vrope.tab = fw.rope_tab;
+  if (rope_fused) CUDA_TRY(rope2d_table(fw.rope_tab, std::max(gh, gw), vrope.log2_theta, s));
   for (int l = 0; l < L; ++l) {
     if (rg && l > 0 && l % rg->group == 0) CUDA_TRY(front_regroup(rg, s, sms));
     bf16* blk;
@@ -157,9 +165,14 @@ cudaError_t Engine::run_encode(Request* r, cudaStream_t& s, int sms, FrontRG* rg
       blk = W.vit_dev[l];
     }
     CUDA_TRY(layernorm(fw.vhid, Dv, blk + vl.n1g, blk + vl.n1b, fw.xb, Dv, N, Dv, m.ln_eps, s));
-    CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.xb, Dv, blk + vl.qkv_w, Dv, fw.qkv, 3 * Dv, blk + vl.qkv_b, N, 3 * Dv,
-                    Dv, EPI_BF16, sms, s));
-    CUDA_TRY(vit_rope(fw.qkv, N, m.vit_heads, hd, gw, m.merge, m.vit_theta, s));
+    if (rope_fused) {  // 2D RoPE in the qkv GEMM epilogue (hd 80: two heads per 256 x 160 tile)
+      CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.xb, Dv, blk + vl.qkv_w, Dv, fw.qkv, 3 * Dv, blk + vl.qkv_b, N,
+                      3 * Dv, Dv, EPI_BF16_ROPE2D, sms, s, nullptr, &vrope));
+    } else {
+      CUDA_TRY(t_gemm(this, 0, NOVA_K_VIT_GEMM, fw.xb, Dv, blk + vl.qkv_w, Dv, fw.qkv, 3 * Dv, blk + vl.qkv_b, N,
+                      3 * Dv, Dv, EPI_BF16, sms, s));
+      CUDA_TRY(vit_rope(fw.qkv, N, m.vit_heads, hd, gw, m.merge, m.vit_theta, s));
+    }
     {
       const double w = 4.0 * N * N * hd * m.vit_heads;
       pass_work[0] += w;

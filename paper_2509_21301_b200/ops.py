@@ -36,6 +36,12 @@ def nova_op_gemm_fold(A, W, C, bias, M, N, K, epi, ngamma=None, nxout=None, nss=
                                   _p(nss), nss.stride(0) if nss is not None else 0, _p(rscale), _s(stream)), "gemm_fold")
 
 
+def nova_op_gemm_rope2d(A, W, C, bias, M, N, K, qk_cols, gw, merge, theta, max_ctas=148, stream=None):
+    import ctypes as Ct
+    check(lib().nova_op_gemm_rope2d(_p(A), A.stride(0), _p(W), W.stride(0), _p(C), C.stride(0), _p(bias), M, N, K,
+                                    qk_cols, gw, merge, Ct.c_float(theta), max_ctas, _s(stream)), "gemm_rope2d")
+
+
 def nova_op_fold_rows(ss, d, eps, rscale, M, stream=None):
     import ctypes as Ct
     check(lib().nova_op_fold_rows(_p(ss), ss.stride(0), d, Ct.c_float(eps), _p(rscale), M, _s(stream)), "fold_rows")

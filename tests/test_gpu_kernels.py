@@ -473,3 +473,33 @@ def test_prefill_rmsnorm_fold_gemms(M, D, F, ctas):
     assert rel_inf(bf16_host(q), V.linear(xn, Wq.astype(np.float64), bq.astype(np.float64))) <= 8e-3
     ref_act = V.silu(V.linear(xn, G.astype(np.float64))) * V.linear(xn, U.astype(np.float64))
     assert rel_inf(bf16_host(act), ref_act) <= 8e-3
+
+
+@pytest.mark.parametrize("gh,gw", [(52, 94), (6, 10)])
+def test_vit_qkv_gemm_with_fused_2d_rope(gh, gw):
+    """ViT qkv GEMM with the 2D RoPE in its epilogue (hd 80, Qwen2-VL ViT width): q / k heads rotated by
+    their patch's (row, col) angles (oracle patchify positions + vit_rope_tables / apply_rope), v untouched,
+    bias added before the rotation; bf16 rel-inf <= 8e-3 against the f64 oracle; bitwise independent of the
+    SM budget."""
+    from synth import Q2B
+    rng = np.random.default_rng(gh * gw)
+    Dv, heads, hd, theta = 1280, 16, 80, 1e4
+    M, N = gh * gw, 3 * Dv
+    X = rand_bf16(rng, (M, Dv))
+    Wq = rand_bf16(rng, (N, Dv), Dv ** -0.5)
+    b = rand_bf16(rng, (N,), 0.05)
+    dX, dW, db = bf16_dev(X), bf16_dev(Wq), bf16_dev(b)
+    outs = []
+    for ctas in (148, 40):
+        C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        O.nova_op_gemm_rope2d(dX, dW, C, db, M, N, Dv, 2 * Dv, gw, 2, theta, max_ctas=ctas)
+        torch.cuda.synchronize()
+        outs.append(C)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    _, _, hp, wp = V.patchify(np.zeros((3, gh * 14, gw * 14), np.float32), Q2B)
+    c, s = V.vit_rope_tables(hp, wp, hd, theta, np.float64)
+    y = V.linear(X.astype(np.float64), Wq.astype(np.float64), b.astype(np.float64)).reshape(M, 3, heads, hd)
+    got = bf16_host(outs[0]).reshape(M, 3, heads, hd)
+    assert rel_inf(got[:, 0], V.apply_rope(y[:, 0], c, s)) <= 8e-3
+    assert rel_inf(got[:, 1], V.apply_rope(y[:, 1], c, s)) <= 8e-3
+    assert rel_inf(got[:, 2], y[:, 2]) <= 8e-3
