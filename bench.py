@@ -116,8 +116,11 @@ def build_engine(shape, device, seed=2):
     from synth.models import weight_specs
     from synth.weights import device_tensor
     from paper_2509_21301_b200 import engine as E
+    # NOVA_BENCH_GREEN=0: partitions as SM-budget-limited grids on primary-context streams, for ncu launch
+    # lists only (ncu does not profile kernels launched into green contexts); never for a bench number
+    green = int(os.environ.get("NOVA_BENCH_GREEN", "1"))
     opts = E.EngineOptions(device=device, max_requests=64, max_decode_batch=16, kv_pages=2600, max_patches=7920,
-                           max_prompt=128, max_gen=64, use_green_ctx=1)
+                           max_prompt=128, max_gen=64, use_green_ctx=green)
     eng = E.Engine(shape, opts)
     for name, shp, init in weight_specs(shape):
         t = device_tensor(name, shp, init, seed, device=f"cuda:{device}")
@@ -515,6 +518,7 @@ def main():
     if prof_range:
         torch.cuda.cudart().cudaProfilerStop()
     ks = eng.kernel_stats()
+    ks_sm = eng.kernel_stats_sm()
     eng.kernel_timing(0)
     # end-to-end: pinned host screenshots, H2D inside the timed region
     res_e2e = []
@@ -613,14 +617,24 @@ def main():
         if n == 0 or ms <= 0:
             continue
         unit = E.KERNEL_UNITS[name]
+        # SURVEY §8(d) d2 "partition-normalized": the same rate over the SM-share-weighted time (each
+        # launch's ms x its pass's SM budget / 148), i.e. what the per-SM rate would give on the whole GPU
+        sm_ms = ks_sm.get(name, 0.0)
+        share = sm_ms / ms if sm_ms > 0 else None
         if unit == "bytes":
             ach = work / (ms / 1e3) / 1e9
             kernels[name] = {"ms_per_launch": ms / n, "launches_timed": n, "achieved": round(ach, 1),
                              "unit": "GB/s", "frac": round(ach / hbm, 4)}
+            if share:
+                kernels[name]["mean_sm_share"] = round(share, 3)
+                kernels[name]["frac_partition_normalized"] = round(ach / share / hbm, 4)
         else:
             ach = work / (ms / 1e3) / 1e12
             kernels[name] = {"ms_per_launch": ms / n, "launches_timed": n, "achieved": round(ach, 1),
                              "unit": "TFLOP/s", "frac": round(ach / tfl, 4)}
+            if share:
+                kernels[name]["mean_sm_share"] = round(share, 3)
+                kernels[name]["frac_partition_normalized"] = round(ach / share / tfl, 4)
     kern_only = {k: v for k, v in kernels.items() if not k.endswith("_pass")}
     dom = max(kern_only, key=lambda k: ks[k][0]) if kern_only else None
     traffic = None
@@ -635,6 +649,10 @@ def main():
         roof = {"kernel": dom, "bound": "hbm" if d["unit"] == "GB/s" else "tensor", "achieved": d["achieved"],
                 "peak": hbm if d["unit"] == "GB/s" else tfl, "unit": d["unit"], "frac": d["frac"],
                 "traffic": traffic,
+                # timed inside the serving replay on the decode / front partition; the same over the
+                # SM-share-weighted time, and the mean SM share of those launches
+                "frac_partition_normalized": d.get("frac_partition_normalized"),
+                "mean_sm_share": d.get("mean_sm_share"),
                 "peak_source": "MEASURED_PEAKS.json" + (" (fallback)" if pk.get("_fallback") else "") +
                 ("" if d["unit"] == "GB/s" else " bf16_tflops_sustained")}
     stages = {k: v for k, v in kernels.items() if k.endswith("_pass")}
@@ -673,6 +691,8 @@ def main():
                      "sm_min": plan["sm_min"], "alpha_dv": round(plan["alpha_dv"], 3),
                      "alpha_dp": round(plan["alpha_dp"], 3)},
             "compare": compare, "mg1": mg1, "clocks": clk}
+    if os.environ.get("NOVA_BENCH_GREEN", "1") == "0":
+        line["config"]["partitions"] = "NOT green contexts (NOVA_BENCH_GREEN=0, ncu launch-list run): not a bench number"
     if kind == "poisson" and not args.no_solo_7b and world == 1:
         # the §8(d) stage bars are stated at the cfg 3 (7B) shapes: time those solo passes too
         try:

@@ -273,6 +273,10 @@ enum {
 nova_status nova_kernel_timing(nova_engine* e, int32_t every_n);
 /* out[0] = summed device ms, out[1] = summed algorithmic work, out[2] = launches. */
 nova_status nova_kernel_stats(nova_engine* e, int32_t cls, double* out3);
+/* *sm_ms = sum over the same launches of ms x (SM budget of the launching pass / total SMs): the time a
+ * stage running on a partition would take on the whole GPU at the same per-SM rate, so work / sm_ms is the
+ * partition-normalized rate (SURVEY.md §8(d) d2 "Partition-normalized: the same / (s / 148)"). */
+nova_status nova_kernel_stats_sm(nova_engine* e, int32_t cls, double* sm_ms);
 nova_status nova_kernel_stats_reset(nova_engine* e);
 /* Total libnova kernel launches in this process so far (all engines and nova_op_*). */
 uint64_t nova_launch_count(void);

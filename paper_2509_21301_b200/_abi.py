@@ -106,6 +106,7 @@ ENGINE_SIGNATURES = {
     "nova_sim_set_curves": (R, [E, C.POINTER(SimCurves)]),
     "nova_kernel_timing": (R, [E, I32]),
     "nova_kernel_stats": (R, [E, I32, C.POINTER(F64)]),
+    "nova_kernel_stats_sm": (R, [E, I32, C.POINTER(F64)]),
     "nova_kernel_stats_reset": (R, [E]),
     "nova_launch_count": (U64, []),
 }

@@ -135,6 +135,7 @@ struct Partition {
 struct KStat {
   double ms = 0, work = 0;
   int64_t launches = 0;
+  double sm_ms = 0;  // sum of ms x (the pass's SM budget / total SMs): the partition-normalized time
 };
 struct KTimer {
   std::vector<cudaEvent_t> ev;
@@ -146,6 +147,7 @@ struct KTimer {
   std::vector<Rec> recs;
   int n = 0;
   bool on = false;
+  double share = 1.0;  // SM budget of the current pass / total SMs
   void init(int pairs);
   void destroy();
   int begin(cudaStream_t s);

@@ -169,6 +169,11 @@ void Worker::run() {
     cudaError_t e = cudaSuccess;
     const bool timing = eng->sample_every > 0;
     eng->ktimer[role].on = timing && (eng->pass_count[role]++ % eng->sample_every == 0);
+    {  // the pass's SM budget (partition-normalized rooflines)
+      const int psms = role == 0 ? (c.kind == NOVA_DEC_HYBRID ? eng->part.total : eng->front_sms(c.s_dec))
+                                 : eng->dec_sms(c.ctx, c.s_dec);
+      eng->ktimer[role].share = (double)psms / (double)eng->part.total;
+    }
     if (timing) cudaEventRecord(p0, s);
     Event done;
     done.reqs = c.reqs;
@@ -209,6 +214,7 @@ void Worker::run() {
         eng->kstats[cls].ms += ms;
         eng->kstats[cls].work += eng->pass_work[role];
         eng->kstats[cls].launches += 1;
+        eng->kstats[cls].sm_ms += ms * eng->ktimer[role].share;
       }
       eng->ktimer[role].harvest(eng->kstats, eng->kmu);
     }

@@ -284,6 +284,13 @@ nova_status nova_kernel_stats(nova_engine* e, int32_t cls, double* out3) {
   return NOVA_OK;
 }
 
+nova_status nova_kernel_stats_sm(nova_engine* e, int32_t cls, double* sm_ms) {
+  if (!e || !sm_ms || cls < 0 || cls >= NOVA_K_COUNT) return NOVA_E_INVAL;
+  std::lock_guard<std::mutex> g(e->e.kmu);
+  *sm_ms = e->e.kstats[cls].sm_ms;
+  return NOVA_OK;
+}
+
 uint64_t nova_launch_count(void) { return g_kernel_launches.load(); }
 
 nova_status nova_kernel_stats_reset(nova_engine* e) {

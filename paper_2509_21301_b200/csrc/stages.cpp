@@ -50,6 +50,7 @@ void KTimer::harvest(KStat* out, std::mutex& mu) {
       out[r.cls].ms += ms;
       out[r.cls].work += r.work;
       out[r.cls].launches += 1;
+      out[r.cls].sm_ms += ms * share;
     }
   }
   recs.clear();

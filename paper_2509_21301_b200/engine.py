@@ -251,6 +251,15 @@ class Engine:
             out[name] = (buf[0], buf[1], int(buf[2]))
         return out
 
+    def kernel_stats_sm(self) -> dict:
+        """{class: SM-share-weighted device ms} (partition-normalized time, include/nova.h)."""
+        out = {}
+        v = A.F64(0.0)
+        for cls, name in enumerate(KERNEL_CLASSES):
+            self._check(self.lib.nova_kernel_stats_sm(self.h, cls, C.byref(v)), "nova_kernel_stats_sm")
+            out[name] = v.value
+        return out
+
     def kernel_stats_reset(self) -> None:
         self._check(self.lib.nova_kernel_stats_reset(self.h), "nova_kernel_stats_reset")
 
