@@ -783,10 +783,11 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
     sS[row * PW + d] = acc;
   }
   cluster_sync_all();  // CTA states visible cluster-wide
-  if (rank == 0) {
+  {  // every rank merges HD / CL of the columns (the same operations per element as one merging rank)
     const uint32_t base = smem_u32(sS);
-    for (int i = tid; i < G * HD; i += 32 * DA_W) {
-      const int row = i / HD, d = i % HD;
+    constexpr int DW = HD / CL;
+    for (int i = tid; i < G * DW; i += 32 * DA_W) {
+      const int row = i / DW, d = rank * DW + i % DW;
       float m[CL], l[CL], v[CL];
 #pragma unroll
       for (int q = 0; q < CL; ++q) {
@@ -808,7 +809,7 @@ __global__ void __launch_bounds__(32 * DA_W) decode_attn_tc_kernel(const bf16* _
       out[(size_t)b * ldo + (size_t)(kvh * G + row) * HD + d] = __float2bfloat16_rn(num / den);
     }
   }
-  cluster_sync_all();  // peers keep their shared memory alive until rank 0 has read it
+  cluster_sync_all();  // peers keep their shared memory alive until every rank has read it
 }
 
 // The same decode attention with CLP < VC physical CTAs per (request, KV head) (session 3): the

@@ -191,3 +191,31 @@ def test_chunked_prefill_full_width_reduced_depth():
     hyb = [r for r in e.decision_log() if not r[1] and r[2] == 4]
     assert len(hyb) == 11 and sum(r[4] for r in hyb) == 1286
     e.close()
+
+
+def test_kernel_stats_partition_share(tiny_setup):
+    """bench.py's partition-normalized roofline input (nova_kernel_stats_sm): every timed launch's ms is
+    weighted by its pass's SM budget / total SMs -- under a static split with 16 decode SMs the decode
+    classes' weight lies in [16 / total, 1] (1 = solo passes on the whole GPU), the front's in
+    [(total - 16) / total, 1], and never exceeds the plain device time."""
+    from paper_2509_21301_b200 import engine as E
+    bits, _, _ = tiny_setup
+    reqs = [make_request(TINY, (4, 4), 8, 6, 300 + i) for i in range(6)]
+    e = _engine(TINY, bits)
+    total = e.query_sms()[0]
+    e.set_partition(mode=E.STATIC, sm_decode_dv=16, sm_decode_dp=16)
+    e.kernel_stats_reset()
+    e.kernel_timing(1)
+    _run(e, reqs)
+    e.kernel_timing(0)
+    ks, sm = e.kernel_stats(), e.kernel_stats_sm()
+    e.close()
+    seen = 0
+    for name, (ms, work, n) in ks.items():
+        if n == 0:
+            continue
+        seen += 1
+        share = sm[name] / ms
+        lo = 16 / total if name.startswith("dec") or name == "lm_head" else (total - 16) / total
+        assert lo - 1e-6 <= share <= 1 + 1e-6, (name, share)
+    assert seen >= 4
