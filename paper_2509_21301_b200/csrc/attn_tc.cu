@@ -564,9 +564,14 @@ NOVA_DEV void tmem_ld_wait32(uint32_t* r) {
 // (KC = 148 / rem, >= 2 tiles per chunk) whose (m, l, O) partials are merged in chunk order by
 // the last chunk to finish.  So the numerics are identical for any SM budget, and on the full
 // GPU the tail wave is ~148 short chunks instead of `rem` full-length units.
+constexpr int FMHA_WS_SLOTS = 320;  // partial slots (2 FBM rows each) in the split workspace
+constexpr int FMHA_TICKETS = 256;
 struct Fmha3Plan {
   int n_q2, n_tiles, units, full, rem, KC, total, causal, H, kt;
-  __host__ __device__ Fmha3Plan(int S, int H_, int split = 1, int causal_ = 0, int kt_ = FBN) {
+  int T = 0;  // causal split: target key tiles per chunk (0 = off)
+  __host__ __device__ int len(int pr) const { return min(n_tiles, (2 * pr + 2) * FBM / kt); }
+  __host__ __device__ int kc_of(int pr) const { return T ? min(4, max(1, (len(pr) + T - 1) / T)) : 1; }
+  __host__ __device__ Fmha3Plan(int S, int H_, int split = 1, int causal_ = 0, int kt_ = FBN, int csplit = 0) {
     H = H_;
     causal = causal_;
     kt = kt_;
@@ -588,11 +593,54 @@ struct Fmha3Plan {
       rem = 0;
     }
     total = full + rem * KC;
+    if (causal && csplit && split) {
+      int all = 0;
+      for (int pr = 0; pr < n_q2; ++pr) all += H * len(pr);
+      for (T = max(4, (all + 147) / 148);; ++T) {
+        int slots = 0, groups = 0, tot = 0;
+        for (int pr = 0; pr < n_q2; ++pr) {
+          const int kc = kc_of(pr);
+          tot += H * kc;
+          if (kc > 1) slots += H * kc, groups += H;
+        }
+        if (slots <= FMHA_WS_SLOTS && groups <= FMHA_TICKETS) {
+          total = tot;
+          break;
+        }
+      }
+    }
   }
   // unit -> (head, q pair, key tiles [t0, t1), split slot or -1, chunk index).
   // Causal: units run longest first (q pair n_q2-1 down to 0, heads fastest); the pair's key
   // range ends at its B tile's diagonal.
   __host__ __device__ void decode(int u, int& h, int& pr, int& t0, int& t1, int& slot, int& ch) const {
+    int grp, kc;
+    decode(u, h, pr, t0, t1, slot, ch, grp, kc);
+  }
+  __host__ __device__ void decode(int u, int& h, int& pr, int& t0, int& t1, int& slot, int& ch, int& grp,
+                                  int& kc) const {
+    grp = -1;
+    kc = 1;
+    if (causal && T) {
+      int u0 = 0, s0 = 0, g0 = 0;
+      for (pr = n_q2 - 1; pr >= 0; --pr) {
+        const int k = kc_of(pr), n = H * k;
+        if (u < u0 + n) {
+          const int w = u - u0, L = len(pr);
+          h = w / k;
+          ch = w % k;
+          t0 = (ch * L) / k;
+          t1 = ((ch + 1) * L) / k;
+          slot = -1;
+          if (k > 1) slot = s0 + h * k + ch, grp = g0 + h, kc = k;
+          return;
+        }
+        u0 += n;
+        if (k > 1) s0 += n, g0 += H;
+      }
+      pr = 0, h = 0, t0 = t1 = 0, slot = -1, ch = 0;
+      return;
+    }
     if (causal) {
       pr = n_q2 - 1 - u / H;
       h = u % H;
@@ -614,6 +662,7 @@ struct Fmha3Plan {
     pr = base % n_q2;
     t0 = slot < 0 ? 0 : (ch * n_tiles) / KC;
     t1 = slot < 0 ? n_tiles : ((ch + 1) * n_tiles) / KC;
+    if (slot >= 0) grp = (u - full) / KC, kc = KC;
   }
   // k-th unit of CTA c out of G: snake order over rounds (c, then G-1-c, ...), so with units
   // sorted longest first the per-CTA sums even out; -1 = no unit this round, -2 = done.
@@ -1004,7 +1053,7 @@ __global__ void __launch_bounds__(384, 1)
   // warp index through a shuffle: provably warp-uniform, so warp-role code keeps its scalars in
   // uniform registers (MMA descriptors without per-lane R2UR waterfalls)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const Fmha3Plan plan(S, H, split, CAUSAL ? 1 : 0, KT4);
+  const Fmha3Plan plan(S, H, split & 255, CAUSAL ? 1 : 0, KT4, CAUSAL ? (split >> 8) & 1 : 0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
@@ -1146,8 +1195,8 @@ __global__ void __launch_bounds__(384, 1)
     int g = 0, nu = 0;
     for (int k = 0, u; (u = plan.unit_of(k, blockIdx.x, gridDim.x)) != -2; ++k) {
       if (u < 0) continue;
-      int h, pr, t0, t1, slot, ch;
-      plan.decode(u, h, pr, t0, t1, slot, ch);
+      int h, pr, t0, t1, slot, ch, grp, kcn;
+      plan.decode(u, h, pr, t0, t1, slot, ch, grp, kcn);
       const int qrow = pr * 2 * FBM + x * FBM + row;
       const int qlo = pr * 2 * FBM + x * FBM;
       float m = -1e30f, l = 0.f;
@@ -1182,7 +1231,8 @@ __global__ void __launch_bounds__(384, 1)
           for (int a = 0; a < 8; ++a) mxa[a] = fmaxf(mxa[a], __uint_as_float(sv[i + a]));
         const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-        const float mnew = fmaxf(m, mx * scale_log2);
+        const bool none = CAUSAL && mx == -1e30f && m == -1e30f;
+        const float mnew = none ? m : fmaxf(m, mx * scale_log2);
         const bool need = (mnew - m) > 8.0f;
         if (__any_sync(0xffffffffu, need) && j > t0) {  // lazy rescale of O: PV_x(g-1) must be complete
           mbar_wait(&o_ready[x], (g - 1) & 1);
@@ -1207,7 +1257,8 @@ __global__ void __launch_bounds__(384, 1)
         }
         // exponent arguments and row sums on the packed f32x2 pipe (FFMA2 / FADD2): the MUFU is the
         // bottleneck, so the rest of the phase must issue in as few slots as possible
-        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+        const float sl = none ? 0.f : scale_log2, nmv = none ? -200.f : -m;
+        const float2 sc2 = make_float2(sl, sl), nm2 = make_float2(nmv, nmv);
         float2 ls2[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) ls2[a] = make_float2(0.f, 0.f);
@@ -1263,56 +1314,69 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         mbar_arrive(q_empty);
       } else {  // key chunk: (m, l, O) partial; the last chunk of the unit merges in chunk order
-        float* wr = ws + ((size_t)slot * 2 * FBM + x * FBM + row) * PW;
-        *reinterpret_cast<float4*>(wr) = make_float4(m, l, 0.f, 0.f);
+        // partial slot layout column-major, rows fastest: element (d, r) at d * 2 FBM + r (d 0 = m, 1 = l,
+        // 4.. = O), so each warp store / load is one coalesced 128-byte access (a row-major slot made
+        // every warp access touch 32 rows: ~33 x 32 L1 wavefronts per thread block, the split's cost)
+        constexpr int R2 = 2 * FBM;
+        float* wr = ws + (size_t)slot * R2 * PW + x * FBM + row;
+        wr[0] = m;
+        wr[R2] = l;
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
           float o[16];
           tmem_ld16(tO + c * 16, o);
 #pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(wr + 4 + c * 16 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+          for (int i = 0; i < 16; ++i) wr[(size_t)(4 + c * 16 + i) * R2] = o[i];
         }
         tc_fence_before();
         mbar_arrive(q_empty);
         __threadfence();
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        const int grp = (u - plan.full) / plan.KC;
-        if (threadIdx.x == 128) *s_last = atomicAdd(&tickets[grp], 1) == plan.KC - 1;
+        if (threadIdx.x == 128) *s_last = atomicAdd(&tickets[grp], 1) == kcn - 1;
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (*s_last) {
           __threadfence();
-          const float* base = ws + ((size_t)grp * plan.KC * 2 * FBM + x * FBM + row) * PW;
-          const size_t cstride = (size_t)2 * FBM * PW;
+          const float* base = ws + (size_t)(slot - ch) * R2 * PW + x * FBM + row;
+          const size_t cstride = (size_t)R2 * PW;
           float M = -1e30f;
-          for (int c2 = 0; c2 < plan.KC; ++c2) M = fmaxf(M, __ldcg(base + c2 * cstride));
-          float den = 0.f, acc[HD];
+          float mc[16];
 #pragma unroll
-          for (int d = 0; d < HD; ++d) acc[d] = 0.f;
-          for (int c2 = 0; c2 < plan.KC; ++c2) {
-            const float* pr2 = base + c2 * cstride;
-            const float4 ml = __ldcg(reinterpret_cast<const float4*>(pr2));
-            float4 ov[HD / 4];
+          for (int c2 = 0; c2 < 16; ++c2) {
+            mc[c2] = c2 < kcn ? __ldcg(base + c2 * cstride) : -1e30f;
+            if (c2 < kcn) M = fmaxf(M, mc[c2]);
+          }
+          float fc[16], den = 0.f;
 #pragma unroll
-            for (int q = 0; q < HD / 4; ++q) ov[q] = __ldcg(reinterpret_cast<const float4*>(pr2 + 4) + q);
-            const float f = exp2f(ml.x - M);
-            den += f * ml.y;
-#pragma unroll
-            for (int q = 0; q < HD / 4; ++q) {
-              acc[4 * q] += f * ov[q].x;
-              acc[4 * q + 1] += f * ov[q].y;
-              acc[4 * q + 2] += f * ov[q].z;
-              acc[4 * q + 3] += f * ov[q].w;
+          for (int c2 = 0; c2 < 16; ++c2) {
+            fc[c2] = 0.f;
+            if (c2 < kcn) {
+              fc[c2] = exp2f(mc[c2] - M);
+              den += fc[c2] * __ldcg(base + c2 * cstride + R2);
             }
           }
           const float inv = 1.0f / den;
           bf16* orow = out + (size_t)qrow * ldo + (size_t)h * HD;
-          if (qrow < S) {
+#pragma unroll 1
+          for (int d0 = 0; d0 < HD; d0 += 16) {  // 16 columns x every chunk per round trip
+            float acc[16];
 #pragma unroll
-            for (int d0 = 0; d0 < HD; d0 += 8)
+            for (int d = 0; d < 16; ++d) acc[d] = 0.f;
+            for (int c2 = 0; c2 < kcn; ++c2) {
+              const float* pc = base + c2 * cstride + (size_t)(4 + d0) * R2;
+              float v[16];
+#pragma unroll
+              for (int d = 0; d < 16; ++d) v[d] = __ldcg(pc + (size_t)d * R2);
+#pragma unroll
+              for (int d = 0; d < 16; ++d) acc[d] += fc[c2] * v[d];
+            }
+            if (qrow < S) {
               *reinterpret_cast<uint4*>(orow + d0) =
-                  make_uint4(pack_bf16(acc[d0] * inv, acc[d0 + 1] * inv), pack_bf16(acc[d0 + 2] * inv, acc[d0 + 3] * inv),
-                             pack_bf16(acc[d0 + 4] * inv, acc[d0 + 5] * inv), pack_bf16(acc[d0 + 6] * inv, acc[d0 + 7] * inv));
+                  make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                             pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+              *reinterpret_cast<uint4*>(orow + d0 + 8) =
+                  make_uint4(pack_bf16(acc[8] * inv, acc[9] * inv), pack_bf16(acc[10] * inv, acc[11] * inv),
+                             pack_bf16(acc[12] * inv, acc[13] * inv), pack_bf16(acc[14] * inv, acc[15] * inv));
+            }
           }
           if (threadIdx.x == 128) tickets[grp] = 0;
         }
@@ -1402,9 +1466,9 @@ cudaError_t fmha3_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int
     set = true;
   }
   if (!g_fmha_ws) {  // once per process (one device per engine process)
-    if (cudaMalloc(&g_fmha_ws, (size_t)148 * 2 * FBM * (128 + 4) * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&g_fmha_tickets, 256 * sizeof(int)) != cudaSuccess ||
-        cudaMemset(g_fmha_tickets, 0, 256 * sizeof(int)) != cudaSuccess)
+    if (cudaMalloc(&g_fmha_ws, (size_t)FMHA_WS_SLOTS * 2 * FBM * (128 + 4) * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&g_fmha_tickets, FMHA_TICKETS * sizeof(int)) != cudaSuccess ||
+        cudaMemset(g_fmha_tickets, 0, FMHA_TICKETS * sizeof(int)) != cudaSuccess)
       return cudaErrorMemoryAllocation;
   }
   static const int split = getenv("NOVA_FMHA_SPLIT") ? atoi(getenv("NOVA_FMHA_SPLIT")) : 1;  // experiments only
@@ -1429,19 +1493,21 @@ cudaError_t fmha4_launch(const bf16* qkv, int ld, bf16* out, int ldo, int S, int
     set = true;
   }
   if (!g_fmha_ws) {
-    if (cudaMalloc(&g_fmha_ws, (size_t)148 * 2 * FBM * (128 + 4) * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&g_fmha_tickets, 256 * sizeof(int)) != cudaSuccess ||
-        cudaMemset(g_fmha_tickets, 0, 256 * sizeof(int)) != cudaSuccess)
+    if (cudaMalloc(&g_fmha_ws, (size_t)FMHA_WS_SLOTS * 2 * FBM * (128 + 4) * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&g_fmha_tickets, FMHA_TICKETS * sizeof(int)) != cudaSuccess ||
+        cudaMemset(g_fmha_tickets, 0, FMHA_TICKETS * sizeof(int)) != cudaSuccess)
       return cudaErrorMemoryAllocation;
   }
   static const int split = getenv("NOVA_FMHA_SPLIT") ? atoi(getenv("NOVA_FMHA_SPLIT")) : 1;
-  const Fmha3Plan plan(S, H, split, CAUSAL ? 1 : 0, KT4);
+  static const int csplit = getenv("NOVA_FMHA_CSPLIT") ? atoi(getenv("NOVA_FMHA_CSPLIT")) : 0;
+  const int split_arg = (split & 255) | ((CAUSAL && csplit) ? 256 : 0);
+  const Fmha3Plan plan(S, H, split & 255, CAUSAL ? 1 : 0, KT4, (CAUSAL && csplit) ? 1 : 0);
   int grid = max_ctas > 0 ? max_ctas : 148;
   if (grid > plan.total) grid = plan.total;
   const float sl2 = LOG2E_F / sqrtf((float)HD);
   static const int turns = getenv("NOVA_FMHA_TURN") ? atoi(getenv("NOVA_FMHA_TURN")) : 1;  // experiments
   return launch_k(kern, dim3(grid), dim3(384), Ft4Cfg<HD>::SMEM, s, false, tm, out, ldo, S, H, KV, sl2, g_fmha_ws,
-                  g_fmha_tickets, split, turns);
+                  g_fmha_tickets, split_arg, turns);
 }
 
 // ld (the qkv row length in elements) must be a multiple of 8; hd in {80, 128} (64-col SW128 chunks).
