@@ -93,6 +93,8 @@ def test_coexec_bitwise_equals_serial(tiny_setup):
     e = _engine(TINY, bits)
     for name, pol in [("serial", dict(mode=E.SERIAL)),
                       ("static16", dict(mode=E.STATIC, sm_decode_dv=16, sm_decode_dp=16)),
+                      # 8 decode SMs: large batches take the virtual-CTA decode attention (> 3 waves)
+                      ("static8", dict(mode=E.STATIC, sm_decode_dv=8, sm_decode_dp=8)),
                       ("static56", dict(mode=E.STATIC, sm_decode_dv=56, sm_decode_dp=104)),
                       ("adaptive", dict(mode=E.ADAPTIVE, sm_op_dv=48, sm_op_dp=40, sm_min=8, alpha_dv=13.0,
                                         alpha_dp=10.0, b_max=5)),
